@@ -1,0 +1,587 @@
+#!/usr/bin/env python
+"""bench.py — the kernelweave B200 hot path on BASELINE.json's configs.
+
+Headline (the JSON line's metric/value): AXPY fp32, n = 2^28 (BASELINE.json configs[1]), inputs
+resident in HBM, index-sharded across ranks under torchrun (strong scaling: total n fixed).
+The same line carries:
+  e2e          the same metric through the public API with host (pinned) buffers: H2D of X, Y
+               and D2H of Y inside the timed region (Queue.enqueue + wait, like runner.cpp:114-117)
+  roofline     AXPY kernel vs MEASURED_PEAKS.json hbm_gbs (algorithmic 12 B/element)
+  cpu_baseline the reference's own CPU AXPY (oracle/_ref: reference runtime, BlocksParallel,
+               all host cores) on the same inputs, rank 0 at N = 1 only; its output is also the
+               parity check of the GPU result (bitwise)
+  dgemm        DGEMM fp64 TFLOP/s: 8192^3 (north-star headline) and 4096^3 (configured point)
+               at N = 1; 16384^3 row-block sharded with NCCL broadcast of B at N > 1
+  clocks, gpu_launches
+
+`--impl reference` runs only the reference CPU implementation (rank 0) on the same config.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+N_AXPY = 1 << 28
+BYTES_PER_ELEM = 12  # read X, read Y, write Y (fp32)
+FP64_NOMINAL_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # 37.2: 148 SMs x 64 FP64 FMA/clk x 1.965 GHz
+
+
+def env_int(name, default):
+    v = os.environ.get(name)
+    return int(v) if v else default
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get("hbm_gbs", 6650.0), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def traffic_from_profiles(kernel: str):
+    """dram bytes per launch from the committed ncu --set full summary, or None."""
+    p = ROOT / "profiles" / "traffic.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        v = d.get(kernel)
+        if isinstance(v, dict):
+            return v.get("dram_bytes_per_launch")
+    return None
+
+
+class ClockSampler:
+    """nvidia-smi samples (200 ms..50 ms period) during the timed regions."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+        self.active = False
+        self.samples = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.gpu), "-lms", "50"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+            return
+        threading.Thread(target=self._reader, daemon=True).start()
+
+    def _reader(self):
+        for line in self.proc.stdout:
+            if self.active:
+                self.samples.append(line.strip())
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for s in self.samples:
+            f = [x.strip() for x in s.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------------------------
+# distributed plumbing
+# --------------------------------------------------------------------------------------------
+class Dist:
+    def __init__(self, n_gpus: int):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(self.local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            self.dist = dist
+            self.torch = torch
+        if n_gpus != self.world and self.rank == 0:
+            print(f"warning: --gpus {n_gpus} but WORLD_SIZE={self.world}", file=sys.stderr)
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier(device_ids=[self.local])
+
+    def max(self, v: float) -> float:
+        if self.world == 1:
+            return v
+        t = self.torch.tensor([v], dtype=self.torch.float64, device="cuda")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, v: float) -> float:
+        if self.world == 1:
+            return v
+        t = self.torch.tensor([v], dtype=self.torch.float64, device="cuda")
+        self.dist.all_reduce(t)
+        return float(t.item())
+
+    def bcast_bytes(self, b: bytes | None) -> bytes:
+        if self.world == 1:
+            return b
+        obj = [b]
+        self.dist.broadcast_object_list(obj, src=0)
+        return obj[0]
+
+    def close(self):
+        if self.world > 1:
+            self.dist.destroy_process_group()
+
+
+def shard(n: int, world: int, rank: int, align: int = 4):
+    """Contiguous index range of `rank`, boundaries multiples of `align` elements (16 B)."""
+    per = -(-n // world)
+    per = -(-per // align) * align
+    lo = min(n, rank * per)
+    return lo, min(n, lo + per)
+
+
+# --------------------------------------------------------------------------------------------
+# product arm
+# --------------------------------------------------------------------------------------------
+def run_ours(args, dist: Dist) -> dict:
+    from paper_1602_08477_b200 import _lib as L
+    from paper_1602_08477_b200 import kernelweave as kw
+
+    lib = L.lib()
+    dev = kw.Device.gpu(dist.local)
+    gpu_index = dist.local
+    GPU = kw.BackendKind.GpuCudaRt
+    q = kw.Queue(dev, kw.QueueFlavor.Async)
+
+    lo, hi = shard(N_AXPY, dist.world, dist.rank)
+    n = hi - lo
+    rng = np.random.default_rng(1234)
+    # synthetic data of the configured shape (same bytes on every rank count: one global draw)
+    x_all = (rng.random(N_AXPY, dtype=np.float32) * 10).astype(np.float32)
+    y_all = (rng.random(N_AXPY, dtype=np.float32) * 10).astype(np.float32)
+    alpha = np.float32(9.096465)
+    xs, ys = x_all[lo:hi], y_all[lo:hi]
+
+    x = kw.Buffer(dev, kw.IndexVec(n), 4)
+    y = kw.Buffer(dev, kw.IndexVec(n), 4)
+    y0 = kw.Buffer(dev, kw.IndexVec(n), 4)
+    x.upload(xs)
+    y.upload(ys)
+    y0.upload(ys)
+    wd = kw.axpyWorkDiv(GPU, n, args.tpb, args.ept)
+    task = kw.createExec(GPU, wd, kw.AxpyKernel(), kw.AxpyArgs(n, float(alpha), x, y))
+
+    # parity step from pristine inputs (checked against the reference CPU result below)
+    q.enqueue(task)
+    q.wait()
+    y_first = y.download() if (dist.world == 1 and not args.no_cpu) else None
+
+    sampler = ClockSampler(gpu_index)
+    sampler.start()
+    time.sleep(0.3)
+
+    for _ in range(args.warmup):
+        q.enqueue(task)
+    q.wait()
+    evs = []
+
+    def rec():
+        ev = C.c_void_p()
+        L.check(lib.kw_event_record(q.handle(), C.byref(ev)))
+        return ev
+
+    dist.barrier()
+    q.wait()
+    launches0 = lib.kw_launch_count()
+    sampler.active = True
+    evs.append(rec())
+    for _ in range(args.steps):
+        q.enqueue(task)
+        evs.append(rec())
+    q.wait()
+    dist.barrier()
+    sampler.active = False
+    launches = lib.kw_launch_count() - launches0
+    per = []
+    for a, b in zip(evs[:-1], evs[1:]):
+        ms = C.c_float()
+        L.check(lib.kw_event_elapsed_ms(a, b, C.byref(ms)))
+        per.append(ms.value)
+    for e in evs:
+        lib.kw_event_destroy(e)
+    local_ms = sum(per)
+    total_ms = dist.max(local_ms)
+    total_bytes = BYTES_PER_ELEM * N_AXPY * args.steps
+    value = total_bytes / (total_ms / 1e3) / 1e9
+    peak, peak_src = peaks()
+    achieved = BYTES_PER_ELEM * n / (statistics.mean(per) / 1e3) / 1e9
+
+    # ---- e2e: host (pinned) buffers through the public API, copies inside the timed region
+    e2e_steps = max(3, min(args.e2e_steps, args.steps))
+    hx = kw.Buffer(kw.Device.host(), kw.IndexVec(n), 4)
+    hy = kw.Buffer(kw.Device.host(), kw.IndexVec(n), 4)
+    hx.host_view()[:] = xs
+    hy.host_view()[:] = ys
+    del x_all, y_all
+    htask = kw.createExec(GPU, wd, kw.AxpyKernel(), kw.AxpyArgs(n, float(alpha), hx, hy))
+    q.enqueue(htask)
+    q.wait()
+    dist.barrier()
+    sampler.active = True
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        q.enqueue(htask)
+        q.wait()
+    t1 = time.perf_counter()
+    sampler.active = False
+    e2e_s = dist.max(t1 - t0)
+    e2e_value = BYTES_PER_ELEM * N_AXPY * e2e_steps / e2e_s / 1e9
+
+    # ---- secondary: DGEMM
+    dg = run_dgemm(args, dist, kw, L, lib, dev, q, sampler)
+
+    sampler.stop()
+    clocks = sampler.summary()
+
+    out = {
+        "metric": "AXPY fp32 HBM GB/s (n=2^28, Y=alpha*X+Y, 12 B/elem)",
+        "value": round(value, 1),
+        "unit": "GB/s",
+        "n_gpus": dist.world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(total_ms / args.steps, 5),
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic (numpy uniform [0,10), seed 1234; identical global input at every N)",
+        "config": {"workload": "AXPY fp32 n=2^28 index-sharded (BASELINE.json configs[1])", "n": N_AXPY,
+                   "n_per_rank": n, "workdiv": {"threads": args.tpb, "elems": args.ept,
+                                                "blocks": wd.blocksPerGrid()[0]},
+                   "parallelism": f"index-shard x{dist.world} (no collective)",
+                   "l2": "inputs larger than L2 (2.15 GB read+write per step vs 132 MB L2); no flush needed"},
+        "e2e": {"value": round(e2e_value, 2), "unit": "GB/s", "steps": e2e_steps,
+                "h2d_bytes_per_step": 8 * N_AXPY, "d2h_bytes_per_step": 4 * N_AXPY,
+                "how": "executeTask-equivalent Queue.enqueue(createExec(GpuCudaRt, AxpyKernel, host pinned "
+                       "buffers)) + wait, wall clock; chunked H2D/kernel/D2H on two streams"},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "peak_source": peak_src,
+                     "traffic": traffic_from_profiles("axpy_f32"),
+                     "kernel": "axpy_vec_kernel<float,4>", "bytes_per_launch": BYTES_PER_ELEM * n},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+        "dgemm": dg,
+    }
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu:
+        cb, parity = cpu_baseline_axpy(xs, ys, alpha, y_first)
+        out["cpu_baseline"] = cb
+        out["parity"] = parity
+    return out
+
+
+def run_dgemm(args, dist, kw, L, lib, dev, q, sampler) -> dict:
+    """DGEMM fp64: N = 1 -> 8192^3 (headline) + 4096^3; N > 1 -> 16384^3 row-sharded with NCCL
+    broadcast of B in column panels (kw_dgemm_rowsharded)."""
+    if args.no_dgemm:
+        return None
+    GPU = kw.BackendKind.GpuCudaRt
+    res = {"metric": "DGEMM fp64 TFLOP/s (2*M*N*K)", "unit": "TFLOP/s",
+           "peak_nominal_tflops": round(FP64_NOMINAL_TFLOPS, 2),
+           "peak_source": "nominal 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (DMMA measured 37.16 TF on this "
+                          "pool: tools/probe/probe.cu)"}
+
+    def timed(fn, steps, warm=2):
+        for _ in range(warm):
+            fn()
+        q.wait()
+        dist.barrier()
+        a, b = C.c_void_p(), C.c_void_p()
+        sampler.active = True
+        L.check(lib.kw_event_record(q.handle(), C.byref(a)))
+        for _ in range(steps):
+            fn()
+        L.check(lib.kw_event_record(q.handle(), C.byref(b)))
+        q.wait()
+        sampler.active = False
+        ms = C.c_float()
+        L.check(lib.kw_event_elapsed_ms(a, b, C.byref(ms)))
+        lib.kw_event_destroy(a)
+        lib.kw_event_destroy(b)
+        dist.barrier()
+        return dist.max(ms.value)
+
+    rng = np.random.default_rng(77)
+    if dist.world == 1:
+        for size, steps in ((8192, args.dgemm_steps), (4096, args.dgemm_steps * 4)):
+            a = rng.random((size, size)) * 10
+            b = rng.random((size, size)) * 10
+            c = rng.random((size, size)) * 10
+            A, B, Cb = (kw.Buffer(dev, kw.IndexVec(size, size), 8) for _ in range(3))
+            A.upload(a)
+            B.upload(b)
+            Cb.upload(c)
+            task = kw.createExec(GPU, kw.gemmTiledWorkDiv(GPU, size, size, 128), kw.GemmTiledKernel(),
+                                 kw.GemmArgs(size, size, size, 1.25, 0.75, A, B, Cb))
+            ms = timed(lambda: q.enqueue(task), steps)
+            tflops = 2 * size ** 3 * steps / (ms / 1e3) / 1e12
+            entry = {"value": round(tflops, 3), "ms_per_step": round(ms / steps, 4), "steps": steps,
+                     "roofline": {"bound": "fp64", "achieved": round(tflops, 3),
+                                  "peak": round(FP64_NOMINAL_TFLOPS, 2), "unit": "TFLOP/s",
+                                  "frac": round(tflops / FP64_NOMINAL_TFLOPS, 4),
+                                  "traffic": traffic_from_profiles(f"dgemm_{size}")}}
+            # e2e: host pinned buffers, H2D of A, B, C and D2H of C per step
+            hA, hB, hC = (kw.Buffer(kw.Device.host(), kw.IndexVec(size, size), 8) for _ in range(3))
+            for hb, src in ((hA, a), (hB, b), (hC, c)):
+                hb.host_view()[:, :size] = src
+            htask = kw.createExec(GPU, kw.gemmTiledWorkDiv(GPU, size, size, 128), kw.GemmTiledKernel(),
+                                  kw.GemmArgs(size, size, size, 1.25, 0.75, hA, hB, hC))
+            q.enqueue(htask)
+            q.wait()
+            e2e_steps = 3
+            sampler.active = True
+            t0 = time.perf_counter()
+            for _ in range(e2e_steps):
+                q.enqueue(htask)
+                q.wait()
+            e2e_s = time.perf_counter() - t0
+            sampler.active = False
+            entry["e2e"] = {"value": round(2 * size ** 3 * e2e_steps / e2e_s / 1e12, 3), "unit": "TFLOP/s",
+                            "steps": e2e_steps, "h2d_bytes_per_step": 3 * size * size * 8,
+                            "d2h_bytes_per_step": size * size * 8}
+            if size == 8192 and not args.no_cpu:
+                entry["cpu_baseline"], entry["parity"] = cpu_baseline_dgemm(a, b, c, 1.25, 0.75, Cb, q, task)
+            res[f"n{size}"] = entry
+            del A, B, Cb, hA, hB, hC
+        res["value"] = res["n8192"]["value"]
+        res["config"] = "DGEMM fp64 M=N=K=8192 (north-star headline) and 4096 (BASELINE configs[2]), 1 GPU"
+        return res
+
+    # N > 1: 16384^3, A/C row blocks per rank, B broadcast from rank 0 in column panels.
+    size = 16384
+    r0, r1 = shard(size, dist.world, dist.rank, align=128)
+    ml = r1 - r0
+    A = kw.Buffer(dev, kw.IndexVec(max(ml, 1), size), 8)
+    Cb = kw.Buffer(dev, kw.IndexVec(max(ml, 1), size), 8)
+    B = kw.Buffer(dev, kw.IndexVec(size, size), 8)
+    panels = kw.Buffer(dev, kw.IndexVec(size * size), 8)
+    blk = np.random.default_rng(1000 + dist.rank)
+    A.upload(blk.random((max(ml, 1), size)) * 10)
+    Cb.upload(blk.random((max(ml, 1), size)) * 10)
+    if dist.rank == 0:
+        B.upload(rng.random((size, size)) * 10)
+    uid = (C.c_char * 128)()
+    if dist.rank == 0:
+        L.check(lib.kw_comm_unique_id(uid))
+    raw = dist.bcast_bytes(bytes(uid) if dist.rank == 0 else None)
+    uid = (C.c_char * 128).from_buffer_copy(raw)
+    comm = C.c_void_p()
+    L.check(lib.kw_comm_init(C.byref(comm), dist.local, dist.world, dist.rank, uid))
+
+    def step():
+        L.check(lib.kw_dgemm_rowsharded(comm, q.handle(), ml, size, size, 1.25, A.data(), A.leadingDim(),
+                                        B.data(), B.leadingDim(), 0.75, Cb.data(), Cb.leadingDim(), panels.data(),
+                                        args.panels, 0))
+
+    steps = max(2, args.dgemm_steps // 2)
+    ms = timed(step, steps, warm=1)
+    lib.kw_comm_destroy(comm)
+    tflops = 2 * size ** 3 * steps / (ms / 1e3) / 1e12
+    res.update({"value": round(tflops, 3), "ms_per_step": round(ms / steps, 3), "steps": steps,
+                "config": f"DGEMM fp64 16384^3 row-block sharded x{dist.world}, ncclBroadcast of B in "
+                          f"{args.panels} column panels overlapped with compute (BASELINE configs[3])",
+                "roofline": {"bound": "fp64", "achieved": round(tflops / dist.world, 3),
+                             "peak": round(FP64_NOMINAL_TFLOPS, 2), "unit": "TFLOP/s per GPU",
+                             "frac": round(tflops / dist.world / FP64_NOMINAL_TFLOPS, 4)}})
+    return res
+
+
+# --------------------------------------------------------------------------------------------
+# CPU baseline / reference arm (the only place bench.py executes oracle/)
+# --------------------------------------------------------------------------------------------
+def cpu_threads():
+    return len(os.sched_getaffinity(0))
+
+
+def _ref_axpy_f32(xs, ys, alpha, reps, warm=1):
+    """The reference's own runtime (oracle/_ref) running the AxpyKernel functor restated for
+    float on BlocksParallel with every host core; returns (median seconds, output, kind)."""
+    from oracle import oracle as O
+    n = xs.size
+    if O.ref_available():
+        r = O.ref()
+        os.environ.setdefault("KERNELWEAVE_POOL_SIZE", str(cpu_threads()))
+        h = r.kwref_axpy_session_new(1, 1, n, float(alpha), xs.ctypes.data, ys.ctypes.data, 16, 4096)
+        assert h, r.kwref_last_error()
+        sec = C.c_double()
+        times = []
+        first = None
+        for i in range(warm + reps):
+            assert r.kwref_axpy_session_run(h, C.byref(sec)) == 0
+            if i == 0:
+                first = np.empty(n, np.float32)
+                r.kwref_axpy_session_read(h, first.ctypes.data)
+            if i >= warm:
+                times.append(sec.value)
+        r.kwref_axpy_session_free(h)
+        return statistics.median(times), first, "reference"
+    out = ys.copy()
+    first = None
+    times = []
+    for i in range(warm + reps):
+        t = time.perf_counter()
+        O.lib().kw_oracle_axpy_threaded(n, float(alpha), xs.ctypes.data, out.ctypes.data, 1, cpu_threads())
+        dt = time.perf_counter() - t
+        if i == 0:
+            first = out.copy()
+        if i >= warm:
+            times.append(dt)
+    return statistics.median(times), first, "port"
+
+
+def cpu_baseline_axpy(xs, ys, alpha, y_gpu_first):
+    reps = 5
+    sec, first, kind = _ref_axpy_f32(xs, ys, alpha, reps)
+    value = BYTES_PER_ELEM * xs.size / sec / 1e9
+    cb = {"value": round(value, 2), "unit": "GB/s", "cores": cpu_threads(), "kind": kind,
+          "sample": f"full workload n=2^28 fp32, 1 warm-up + median of {reps} reps of enqueue+wait "
+                    f"(reference AxpyKernel functor (float) on the reference BlocksParallel engine, ept=4096)"}
+    parity = {"check": "GPU Y after one step == reference CPU Y (bitwise, 2^28 elements)",
+              "match": bool(y_gpu_first is not None and np.array_equal(first, y_gpu_first))}
+    return cb, parity
+
+
+def cpu_baseline_dgemm(a, b, c, alpha, beta, Cb, q, task):
+    """Reference GemmTiledKernel (tile 32, BlocksParallel, all cores) on a 64-row sample of
+    the 8192^3 workload; rows of the GPU result (from pristine C) checked against it."""
+    from oracle import oracle as O
+    rows = 64
+    size = a.shape[0]
+    # GPU result from pristine C for the parity rows
+    Cb.upload(c)
+    q.enqueue(task)
+    q.wait()
+    gpu_rows = Cb.download()[:rows]
+    out = np.ascontiguousarray(c[:rows]).copy()
+    sec = C.c_double()
+    kind = "reference" if O.ref_available() else "port"
+    if kind == "reference":
+        r = O.ref()
+        os.environ.setdefault("KERNELWEAVE_POOL_SIZE", str(cpu_threads()))
+        assert r.kwref_gemm_kernel(1, 1, rows, size, size, alpha, beta, np.ascontiguousarray(a[:rows]).ctypes.data,
+                                   size, b.ctypes.data, size, out.ctypes.data, size, 32, 16, 8, C.byref(sec)) == 0
+        secs = sec.value
+    else:
+        t = time.perf_counter()
+        out = O.gemm(alpha, beta, a[:rows], b, c[:rows], threads=cpu_threads())
+        secs = time.perf_counter() - t
+    tf = 2 * rows * size * size / secs / 1e12
+    err = np.abs(gpu_rows - out)
+    ok = bool(np.all(err <= (size + 4) * 2.0 ** -53 * np.abs(out)))
+    cb = {"value": round(tf * 1e3, 3), "unit": "GFLOP/s", "cores": cpu_threads(), "kind": kind,
+          "sample": f"{rows} of {size} rows of the 8192^3 workload (GemmTiledKernel tile 32, BlocksParallel); "
+                    f"{secs:.2f} s"}
+    return cb, {"check": "|dC| <= (K+4)*2^-53*|C_ref| on the sampled rows", "match": ok}
+
+
+def run_reference(args, dist: Dist) -> dict | None:
+    if dist.rank != 0:
+        return None
+    rng = np.random.default_rng(1234)
+    xs = (rng.random(N_AXPY, dtype=np.float32) * 10).astype(np.float32)
+    ys = (rng.random(N_AXPY, dtype=np.float32) * 10).astype(np.float32)
+    alpha = np.float32(9.096465)
+    steps = max(1, min(args.steps, args.ref_steps))
+    sec, _, kind = _ref_axpy_f32(xs, ys, alpha, steps, warm=max(1, min(args.warmup, 2)))
+    value = BYTES_PER_ELEM * N_AXPY / sec / 1e9
+    cb = {"value": round(value, 2), "unit": "GB/s", "cores": cpu_threads(), "kind": kind,
+          "sample": f"full workload n=2^28 fp32, median of {steps} reps (reference BlocksParallel engine, "
+                    f"AxpyKernel functor for float, ept=4096)"}
+    return {"impl": "reference", "metric": "AXPY fp32 HBM GB/s (n=2^28, Y=alpha*X+Y, 12 B/elem)",
+            "value": round(value, 2), "unit": "GB/s", "n_gpus": dist.world, "steps": steps,
+            "warmup": args.warmup, "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "AXPY fp32 n=2^28 index-sharded (BASELINE.json configs[1])", "n": N_AXPY},
+            "cpu_baseline": cb, "e2e": {"value": round(value, 2), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                                        "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--tpb", type=int, default=256)
+    ap.add_argument("--ept", type=int, default=16)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--dgemm-steps", type=int, default=10)
+    ap.add_argument("--panels", type=int, default=8)
+    ap.add_argument("--ref-steps", type=int, default=10)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--no-dgemm", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: --warmup < 3 violates the timing rules; using 3", file=sys.stderr)
+        args.warmup = 3
+    if args.impl == "reference":
+        rank = int(os.environ.get("RANK", "0"))
+        if rank != 0:
+            return 0
+        class _D:  # no process group needed: rank 0 alone runs the CPU reference
+            world = int(os.environ.get("WORLD_SIZE", "1"))
+            rank = 0
+        out = run_reference(args, _D())
+        print(json.dumps(out), flush=True)
+        return 0
+    dist = Dist(args.gpus)
+    try:
+        out = run_ours(args, dist)
+    finally:
+        pass
+    if dist.rank == 0:
+        print(json.dumps(out), flush=True)
+    dist.close()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

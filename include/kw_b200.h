@@ -1,0 +1,202 @@
+/*
+ * kw_b200.h — the C-ABI boundary of the B200-native kernelweave path (libkw_b200.so).
+ *
+ * The reference (kernelweave, /root/reference/proj) has exactly one compiled dispatch point
+ * for kernels, `detail::runGrid(BackendKind, const WorkDiv&, const KernelBody&)`
+ * (core/include/kernelweave/exec.hpp:23, core/src/accel.cpp:251-265). A host std::function
+ * cannot run on a GPU, so this build replaces that seam — and the buffer / copy / queue
+ * services the kernels are fed through — with the plain-pointer entry points below. The C++
+ * drop-in headers (include/kernelweave/*.hpp) translate the reference's classes onto them;
+ * INTEGRATION.md shows the ctypes / C++ bindings a maintainer adds.
+ *
+ * Conventions: no exceptions cross this boundary; every entry point returns a kw_status and
+ * leaves a thread-local message in kw_last_error() on failure. Precondition violations are
+ * reported before anything is enqueued (the reference's UsageError contract, e.g.
+ * core/src/buffer.cpp:101-107, core/src/work_div.cpp:53-63). Index vectors are ordered
+ * slowest-varying first with the LAST component fastest (index_vec.hpp:15-24); the last
+ * component maps to CUDA x.
+ *
+ * There is no CPU fallback: every compute entry point runs a hand-written sm_100a kernel.
+ */
+#ifndef KW_B200_H
+#define KW_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define KW_EXPORT __attribute__((visibility("default")))
+#else
+#define KW_EXPORT
+#endif
+
+/* Status codes. Mirrors the reference's error taxonomy (core/include/kernelweave/error.hpp):
+ * KW_USAGE ~ UsageError (:13), KW_RESOURCE ~ ResourceError (:19), KW_TASK ~ TaskError (:26-40). */
+typedef int kw_status;
+#define KW_OK 0
+#define KW_USAGE 1
+#define KW_RESOURCE 2
+#define KW_TASK 3
+
+/* Queue flavours: QueueFlavor::Sync / ::Async (core/include/kernelweave/queue.hpp:21-24). */
+#define KW_QUEUE_SYNC 0
+#define KW_QUEUE_ASYNC 1
+
+/* Task states: TaskState (queue.hpp:26-31). */
+#define KW_TASK_PENDING 0
+#define KW_TASK_RUNNING 1
+#define KW_TASK_DONE 2
+#define KW_TASK_FAILED 3
+
+/* Memory kinds reported by kw_pointer_kind. */
+#define KW_MEM_PAGEABLE 0 /* ordinary host memory unknown to CUDA */
+#define KW_MEM_PINNED 1   /* page-locked host memory */
+#define KW_MEM_DEVICE 2   /* device memory (any GPU) */
+
+typedef struct kw_queue_s* kw_queue;
+typedef struct kw_event_s* kw_event;
+
+/* WorkDiv{blocksPerGrid, threadsPerBlock, elementsPerThread} (core/include/kernelweave/
+ * work_div.hpp:33-53). `dim` in 1..3; unused trailing components must be 1. */
+typedef struct {
+    uint32_t dim;
+    size_t blocks[3];
+    size_t threads[3];
+    size_t elems[3];
+} kw_workdiv;
+
+typedef struct {
+    char name[96];
+    int sm_count;
+    int cc_major, cc_minor;
+    size_t l2_bytes;
+    size_t global_mem_bytes;
+    size_t smem_per_block_optin;
+    int sm_clock_khz;
+    int mem_clock_khz;
+    int mem_bus_width_bits;
+} kw_device_props;
+
+/* ---- errors ----------------------------------------------------------------------------- */
+KW_EXPORT const char* kw_last_error(void);
+KW_EXPORT const char* kw_version(void);
+
+/* ---- devices (replaces Device::logical(i), core/include/kernelweave/device.hpp:14-37) ---- */
+KW_EXPORT kw_status kw_device_count(int* n);
+KW_EXPORT kw_status kw_device_props_get(int device, kw_device_props* props);
+KW_EXPORT kw_status kw_device_synchronize(int device);
+
+/* ---- buffers (replaces Buffer::Buffer / ~Buffer, core/src/buffer.cpp:25-46) --------------
+ * device >= 0: device memory on that CUDA device; device == -1: page-locked host memory.
+ * Pitch rule of buffer.cpp:37: 1-D dense; 2-D/3-D rows padded to row_align (power of two).
+ * Returns the row pitch in bytes; storage = rowCount * pitch. */
+KW_EXPORT kw_status kw_buffer_alloc(int device, uint32_t dim, const size_t extent[3], size_t elem_size,
+                                    size_t row_align, void** ptr, size_t* row_pitch);
+KW_EXPORT kw_status kw_buffer_free(int device, void* ptr);
+KW_EXPORT kw_status kw_pointer_kind(const void* ptr, int* kind, int* device);
+KW_EXPORT kw_status kw_memset(kw_queue q, void* ptr, int value, size_t bytes);
+
+/* ---- queues (replaces Queue, queue.hpp:94-137 / core/src/queue.cpp) ----------------------
+ * One CUDA stream per queue. Sync: every enqueue completes before returning. Async: enqueue
+ * returns immediately. Launch failures are collected and surfaced by kw_queue_wait() as
+ * KW_TASK with "task failed: <msg>" / "<n> tasks failed; first: <msg>" (error.hpp:26-40,
+ * queue.cpp:108-131); the counters reset after a report. */
+KW_EXPORT kw_status kw_queue_create(int device, int flavor, kw_queue* q);
+KW_EXPORT kw_status kw_queue_destroy(kw_queue q);
+KW_EXPORT kw_status kw_queue_wait(kw_queue q);
+KW_EXPORT kw_status kw_queue_device(kw_queue q, int* device);
+KW_EXPORT kw_status kw_queue_flavor(kw_queue q, int* flavor);
+KW_EXPORT kw_status kw_queue_stream(kw_queue q, void** cuda_stream);
+KW_EXPORT kw_status kw_queue_shutdown(kw_queue q);
+
+/* TaskHandle (queue.hpp:36-52) as a CUDA event recorded after the last enqueued task. */
+KW_EXPORT kw_status kw_event_record(kw_queue q, kw_event* ev);
+KW_EXPORT kw_status kw_event_state(kw_event ev, int* state);
+KW_EXPORT kw_status kw_event_destroy(kw_event ev);
+/* Milliseconds between two recorded events of the same device (timing helper). */
+KW_EXPORT kw_status kw_event_elapsed_ms(kw_event start, kw_event stop, float* ms);
+
+/* ---- copies (replaces createCopy/copyBuffer, core/src/buffer.cpp:99-151) -----------------
+ * Deep copy of `extent` elements from the origin corner of src to the origin corner of dst.
+ * Each side's rows are located via its own extent and pitch; bytes outside the copied box
+ * are never touched. Any combination of host / pinned / device memory (UVA). */
+KW_EXPORT kw_status kw_copy(kw_queue q, void* dst, size_t dst_pitch, const size_t dst_extent[3],
+                            const void* src, size_t src_pitch, const size_t src_extent[3], uint32_t dim,
+                            const size_t extent[3], size_t elem_size);
+
+/* ---- work division helpers (work_div.cpp:65-119) ---------------------------------------- */
+/* totalExtent(wd, origin, unit); origin 0 Grid,1 Block,2 Thread; unit 0 Blocks,1 Threads,2 Elems */
+KW_EXPORT kw_status kw_total_extent(const kw_workdiv* wd, int origin, int unit, size_t out[3]);
+/* divideForBackend for the GPU: thread-level shape ceil(N/(B*V)) x B x V (work_div.cpp:96-119). */
+KW_EXPORT kw_status kw_divide_for_gpu(uint32_t dim, const size_t problem[3], const size_t threads_hint[3],
+                                      const size_t elems_hint[3], kw_workdiv* out);
+/* The library's preferred division for each kernel (NULL wd in the calls below uses it). */
+KW_EXPORT kw_status kw_axpy_default_workdiv(size_t n, int elem_size, kw_workdiv* out);
+KW_EXPORT kw_status kw_dgemm_default_workdiv(size_t m, size_t n, size_t tile, kw_workdiv* out);
+
+/* ---- K1: AXPY  Y = alpha*X + Y  (AxpyKernel, core/src/kernels/axpy.cpp:10-23) ------------
+ * Bit-exact against axpyReference (reference.cpp:8-12): product and sum rounded separately
+ * (no FMA contraction). wd covers n with its grid element extent; elements >= n are never
+ * touched (axpy.cpp:15-17). Device pointers run the HBM kernel; host pointers (pinned or
+ * pageable) are streamed through the device in chunks with copies overlapped on two
+ * streams (e2e path). wd == NULL: kw_axpy_default_workdiv. */
+KW_EXPORT kw_status kw_axpy_f32(kw_queue q, const kw_workdiv* wd, size_t n, float alpha, const float* x,
+                                float* y);
+KW_EXPORT kw_status kw_axpy_f64(kw_queue q, const kw_workdiv* wd, size_t n, double alpha, const double* x,
+                                double* y);
+
+/* ---- K2: tiled DGEMM  C = alpha*A*B + beta*C  (GemmTiledKernel, gemm.cpp:40-118) ----------
+ * Row-major pitched fp64; lda/ldb/ldc in elements. FP64 DMMA tensor-core kernel, cp.async
+ * multistage smem pipeline. Within |dC| <= (K+4)*2^-53*|C_ref| of gemmReference
+ * (reference.cpp:14-26); the epilogue is fl(fl(alpha*acc) + fl(beta*c)) as in gemm.cpp:115.
+ * beta multiplies C even when 0 (C is always read). wd == NULL: default tile. Host pointers
+ * are staged through the device (e2e path). */
+KW_EXPORT kw_status kw_dgemm(kw_queue q, const kw_workdiv* wd, size_t m, size_t n, size_t k, double alpha,
+                             const double* A, size_t lda, const double* B, size_t ldb, double beta, double* C,
+                             size_t ldc);
+
+/* ---- K3: naive DGEMM (GemmNaiveKernel, gemm.cpp:11-38) — BIT-EXACT mode --------------------
+ * One dot product per output, ascending p, products and sums rounded separately, acc from
+ * +0.0: bitwise identical to gemmReference. Honors the (rows, cols) work division exactly
+ * like the reference: thread (r, c) of the grid owns rows [r*er, r*er+er) x cols [c*ec, ...). */
+KW_EXPORT kw_status kw_dgemm_naive(kw_queue q, const kw_workdiv* wd, size_t m, size_t n, size_t k,
+                                   double alpha, const double* A, size_t lda, const double* B, size_t ldb,
+                                   double beta, double* C, size_t ldc);
+
+/* ---- multi-GPU (one process per GPU) -------------------------------------------------------
+ * NCCL communicator for the row-sharded DGEMM's broadcast of B. The 128-byte unique id is
+ * produced by rank 0 (kw_comm_unique_id) and exchanged by the caller (torch.distributed
+ * store, MPI, a file). */
+typedef struct kw_comm_s* kw_comm;
+KW_EXPORT kw_status kw_comm_unique_id(unsigned char id[128]);
+KW_EXPORT kw_status kw_comm_init(kw_comm* comm, int device, int world, int rank, const unsigned char id[128]);
+KW_EXPORT kw_status kw_comm_destroy(kw_comm comm);
+KW_EXPORT kw_status kw_comm_broadcast(kw_comm comm, kw_queue q, void* buf, size_t bytes, int root);
+
+/* Row-block shard of C = alpha*A*B + beta*C across `world` ranks: this rank holds
+ * rows [row0, row0+m_local) of A (lda) and C (ldc); B (k x n, ldb) is valid on `root` and is
+ * broadcast in `panels` column panels into the caller's b_panels scratch (k*n doubles,
+ * panel-major: panel j is k x w_j dense), each panel's broadcast overlapped with the
+ * previous panel's DGEMM on a second stream. Every output element is reduced entirely on
+ * one rank in the single-GPU kernel's order, so the gathered C is bitwise identical to the
+ * 1-GPU kw_dgemm result. */
+KW_EXPORT kw_status kw_dgemm_rowsharded(kw_comm comm, kw_queue q, size_t m_local, size_t n, size_t k,
+                                        double alpha, const double* A, size_t lda, const double* B, size_t ldb,
+                                        double beta, double* C, size_t ldc, double* b_panels, int panels,
+                                        int root);
+
+/* ---- measurement helpers (bench / tests) --------------------------------------------------- */
+/* Writes a device scratch buffer larger than L2 (flush between timed iterations). */
+KW_EXPORT kw_status kw_l2_flush(kw_queue q);
+/* Number of kernels this library launched in the process so far (gpu_launches claim). */
+KW_EXPORT uint64_t kw_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KW_B200_H */

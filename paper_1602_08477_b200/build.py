@@ -1,0 +1,82 @@
+"""In-tree build of libkw_b200.so (sm_100a) and of the C++ drop-in test programs.
+
+Everything is compiled with nvcc / g++ directly (no JIT cache): the built .so files sit in the
+package directory so they travel to the GPU box with the repository snapshot.
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import os
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+INCLUDE = ROOT / "include"
+BUILD = PKG / "_build"
+LIB = PKG / "libkw_b200.so"
+
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
+              "-Xptxas", "-v", f"-I{INCLUDE}", f"-I{CSRC}"]
+SOURCES = ["kw_runtime.cu", "kw_axpy.cu", "kw_dgemm.cu", "kw_comm.cu"]
+
+
+def _run(cmd: list[str]) -> str:
+    p = subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
+    if p.returncode != 0:
+        raise RuntimeError(f"command failed ({p.returncode}): {' '.join(cmd)}\n{p.stdout}")
+    return p.stdout
+
+
+def _stale(target: Path, deps: list[Path]) -> bool:
+    if not target.exists():
+        return True
+    t = target.stat().st_mtime
+    return any(d.stat().st_mtime > t for d in deps)
+
+
+def build_lib(force: bool = False, verbose: bool = False) -> Path:
+    """Compile csrc/*.cu for sm_100a and link libkw_b200.so (links NCCL for the broadcast)."""
+    BUILD.mkdir(exist_ok=True)
+    headers = list(CSRC.glob("*.cuh")) + [INCLUDE / "kw_b200.h"]
+    objs = []
+    jobs = []
+    for src in SOURCES:
+        s = CSRC / src
+        o = BUILD / (s.stem + ".o")
+        objs.append(o)
+        if force or _stale(o, [s] + headers):
+            jobs.append([NVCC, *ARCH, *NVCC_FLAGS, "-c", str(s), "-o", str(o)])
+    if jobs:
+        with cf.ThreadPoolExecutor(max_workers=len(jobs)) as ex:
+            for out in ex.map(_run, jobs):
+                if verbose:
+                    print(out)
+                (BUILD / "ptxas.log").open("a").write(out)
+    if force or jobs or _stale(LIB, objs):
+        _run([NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart", "-lnccl"])
+    return LIB
+
+
+def build_cpp_tests(force: bool = False) -> list[Path]:
+    """Builds the C++ drop-in programs under tests/cpp against include/ and libkw_b200.so."""
+    out = []
+    cpp_dir = ROOT / "tests" / "cpp"
+    hdrs = list((INCLUDE / "kernelweave").rglob("*.hpp")) + [INCLUDE / "kw_b200.h"]
+    for src in sorted(cpp_dir.glob("*.cpp")):
+        exe = BUILD / src.stem
+        if force or _stale(exe, [src, LIB] + hdrs):
+            _run(["g++", "-O2", "-std=c++20", "-Wall", "-Wextra", f"-I{INCLUDE}", str(src), "-o", str(exe),
+                  f"-L{PKG}", "-lkw_b200", f"-Wl,-rpath,{PKG}", "-Wl,-rpath,$ORIGIN/..", "-lpthread"])
+        out.append(exe)
+    return out
+
+
+if __name__ == "__main__":
+    build_lib(force="--force" in sys.argv, verbose=True)
+    print(build_cpp_tests(force="--force" in sys.argv))

@@ -1,0 +1,293 @@
+// kw_axpy.cu — K1: AXPY  Y = alpha*X + Y  on sm_100a.
+//
+// Reference: AxpyKernel::operator() (/root/reference/proj/core/src/kernels/axpy.cpp:10-23) and
+// the oracle axpyReference (core/src/kernels/reference.cpp:8-12).
+//
+// Arithmetic: y = fl(fl(alpha*x) + y) — __fmul_rn/__fadd_rn (__dmul_rn/__dadd_rn) so nvcc cannot
+// contract into FFMA/DFMA; the reference's objects contain mulpd/addpd and no vfmadd, so this is
+// the only choice that is bit-exact (SURVEY.md §7 "Hard parts" 1).
+//
+// Work division → hardware mapping (the element level becomes 128-bit vectors):
+//   blocksPerGrid[0]  → gridDim.x        (block b covers elements [b*T*V, (b+1)*T*V), exactly the
+//   threadsPerBlock[0]→ blockDim.x        reference block's coverage, work_div.cpp:96-119)
+//   elementsPerThread → V elements per thread, issued as V/W vectors of W = 16/sizeof(T)
+//                       elements; vector j of thread t sits at b*T*V + (j*T + t)*W so every
+//                       warp-wide LDG.128/STG.128 is fully coalesced. The reference's "thread
+//                       owns a contiguous run" is an ownership detail of an elementwise update:
+//                       no bit of any result depends on which hardware lane computed it.
+//   Elements >= n are never read or written (axpy.cpp:15-17 tail guard).
+//
+// Bytes per element (algorithmic): read X, read Y, write Y = 3*sizeof(T) (12 B for fp32).
+#include "kw_common.cuh"
+
+#include <climits>
+
+namespace {
+
+template <typename T>
+struct Vec;
+template <>
+struct Vec<float> {
+    using type = float4;
+    static constexpr int W = 4;
+};
+template <>
+struct Vec<double> {
+    using type = double2;
+    static constexpr int W = 2;
+};
+
+__device__ __forceinline__ float axpy1(float a, float x, float y) { return __fadd_rn(__fmul_rn(a, x), y); }
+__device__ __forceinline__ double axpy1(double a, double x, double y) { return __dadd_rn(__dmul_rn(a, x), y); }
+
+__device__ __forceinline__ float4 axpyv(float a, float4 x, float4 y)
+{
+    return make_float4(axpy1(a, x.x, y.x), axpy1(a, x.y, y.y), axpy1(a, x.z, y.z), axpy1(a, x.w, y.w));
+}
+__device__ __forceinline__ double2 axpyv(double a, double2 x, double2 y)
+{
+    return make_double2(axpy1(a, x.x, y.x), axpy1(a, x.y, y.y));
+}
+
+// Streaming loads/stores: X and Y are touched exactly once per launch.
+__device__ __forceinline__ float4 ld_stream(const float4* p) { return __ldcs(p); }
+__device__ __forceinline__ double2 ld_stream(const double2* p) { return __ldcs(p); }
+__device__ __forceinline__ void st_stream(float4* p, float4 v) { __stcs(p, v); }
+__device__ __forceinline__ void st_stream(double2* p, double2 v) { __stcs(p, v); }
+
+// Vector path. `limit` = min(n, grid element extent). U vectors per thread in flight.
+template <typename T, int U>
+__global__ void __launch_bounds__(1024) axpy_vec_kernel(size_t limit, T alpha, const T* __restrict__ x,
+                                                       T* __restrict__ y, uint32_t vecs_per_thread)
+{
+    using V = typename Vec<T>::type;
+    constexpr int W = Vec<T>::W;
+    const size_t threads = blockDim.x;
+    const size_t block_elems = threads * vecs_per_thread * W;
+    const size_t base = static_cast<size_t>(blockIdx.x) * block_elems;
+    if (base >= limit)
+        return;
+    const size_t end = limit - base < block_elems ? limit : base + block_elems;
+    const size_t nvec = (end - base) / W; // whole vectors inside [base, end)
+    const V* xv = reinterpret_cast<const V*>(x + base);
+    V* yv = reinterpret_cast<V*>(y + base);
+    for (uint32_t j0 = 0; j0 < vecs_per_thread; j0 += U) {
+        V xr[U], yr[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const size_t idx = (j0 + u) * threads + threadIdx.x;
+            if (j0 + u < vecs_per_thread && idx < nvec) {
+                xr[u] = ld_stream(xv + idx);
+                yr[u] = ld_stream(yv + idx);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const size_t idx = (j0 + u) * threads + threadIdx.x;
+            if (j0 + u < vecs_per_thread && idx < nvec)
+                st_stream(yv + idx, axpyv(alpha, xr[u], yr[u]));
+        }
+    }
+    // Ragged end of the last covered block: fewer than W elements remain.
+    for (size_t e = base + nvec * W + threadIdx.x; e < end; e += threads)
+        y[e] = axpy1(alpha, x[e], y[e]);
+}
+
+// Scalar path (misaligned pointers or V not a multiple of W): element j*T + t of the block.
+template <typename T>
+__global__ void __launch_bounds__(1024) axpy_scalar_kernel(size_t limit, T alpha, const T* __restrict__ x,
+                                                          T* __restrict__ y, uint32_t elems_per_thread)
+{
+    const size_t threads = blockDim.x;
+    const size_t base = static_cast<size_t>(blockIdx.x) * threads * elems_per_thread;
+    for (uint32_t j = 0; j < elems_per_thread; ++j) {
+        const size_t e = base + j * threads + threadIdx.x;
+        if (e < limit)
+            y[e] = axpy1(alpha, x[e], y[e]);
+    }
+}
+
+template <typename T>
+kw_status validate_wd(const kw_workdiv* wd, size_t n, size_t& blocks, uint32_t& threads, uint32_t& elems,
+                      size_t& limit)
+{
+    if (wd->dim != 1)
+        return kw::usage("axpy: the AXPY kernel runs on a 1-D work division");
+    if (wd->blocks[0] == 0 || wd->threads[0] == 0 || wd->elems[0] == 0)
+        return kw::usage("WorkDiv: every level extent is at least 1");
+    if (wd->threads[0] > 1024)
+        return kw::usage("axpy: threadsPerBlock " + std::to_string(wd->threads[0]) +
+                         " exceeds the sm_100a block limit of 1024");
+    if (wd->blocks[0] > static_cast<size_t>(INT_MAX))
+        return kw::usage("axpy: blocksPerGrid exceeds the grid limit");
+    if (wd->elems[0] > (1u << 30))
+        return kw::usage("axpy: elementsPerThread too large");
+    blocks = wd->blocks[0];
+    threads = static_cast<uint32_t>(wd->threads[0]);
+    elems = static_cast<uint32_t>(wd->elems[0]);
+    const size_t covered = blocks * threads * static_cast<size_t>(elems);
+    limit = covered < n ? covered : n; // only covered indices are computed (axpy.cpp:12-17)
+    return KW_OK;
+}
+
+template <typename T>
+void launch_device(cudaStream_t s, size_t blocks, uint32_t threads, uint32_t elems, size_t limit, T alpha,
+                   const T* x, T* y)
+{
+    constexpr int W = Vec<T>::W;
+    const bool aligned = (reinterpret_cast<uintptr_t>(x) % 16 == 0) && (reinterpret_cast<uintptr_t>(y) % 16 == 0);
+    // Blocks entirely beyond `limit` have nothing to do: do not launch them.
+    const size_t block_elems = static_cast<size_t>(threads) * elems;
+    const size_t useful = kw::ceil_div(limit, block_elems);
+    const unsigned grid = static_cast<unsigned>(useful < blocks ? useful : blocks);
+    if (grid == 0)
+        return;
+    if (aligned && elems % W == 0) {
+        const uint32_t vpt = elems / W;
+        if (vpt >= 4)
+            axpy_vec_kernel<T, 4><<<grid, threads, 0, s>>>(limit, alpha, x, y, vpt);
+        else if (vpt >= 2)
+            axpy_vec_kernel<T, 2><<<grid, threads, 0, s>>>(limit, alpha, x, y, vpt);
+        else
+            axpy_vec_kernel<T, 1><<<grid, threads, 0, s>>>(limit, alpha, x, y, vpt);
+    }
+    else {
+        axpy_scalar_kernel<T><<<grid, threads, 0, s>>>(limit, alpha, x, y, elems);
+    }
+    kw::g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+// Host-resident operands (the e2e path: executeTask on Device::host() buffers): stream the
+// vectors through device scratch in chunks. H2D + kernel on the queue's stream, D2H on the
+// aux stream, a ring of slots with events so the H2D of chunk c+1 overlaps the D2H of chunk c
+// (PCIe is full duplex). The queue stream finally joins the aux stream, so later tasks on the
+// queue observe the completed Y (in-order FIFO, queue.hpp:86-93).
+template <typename T>
+kw_status run_staged(kw::Queue* q, uint32_t threads, uint32_t elems, size_t limit, T alpha, const T* x, T* y,
+                     bool x_dev, bool y_dev)
+{
+    constexpr size_t kChunkBytes = 32u << 20; // per operand per slot
+    const size_t chunk = kChunkBytes / sizeof(T);
+    const int ring = 3;
+    const size_t slot_elems = chunk * 2;
+    kw_status st = kw::ensure_scratch(q, ring * slot_elems * sizeof(T));
+    if (st != KW_OK)
+        return st;
+    T* scratch = static_cast<T*>(q->scratch);
+    const size_t block_elems = static_cast<size_t>(threads) * elems;
+    const size_t nchunks = kw::ceil_div(limit, chunk);
+    cudaError_t e = cudaSuccess;
+    for (size_t c = 0; c < nchunks && e == cudaSuccess; ++c) {
+        const int s = static_cast<int>(c % ring);
+        const size_t off = c * chunk;
+        const size_t len = limit - off < chunk ? limit - off : chunk;
+        T* xs = scratch + s * slot_elems;
+        T* ys = xs + chunk;
+        if (c >= static_cast<size_t>(ring))
+            e = cudaStreamWaitEvent(q->stream, q->ev_free[s], 0);
+        const T* xd = x + off;
+        T* yd = y + off;
+        if (e == cudaSuccess && !x_dev) {
+            e = cudaMemcpyAsync(xs, x + off, len * sizeof(T), cudaMemcpyHostToDevice, q->stream);
+            xd = xs;
+        }
+        if (e == cudaSuccess && !y_dev) {
+            e = cudaMemcpyAsync(ys, y + off, len * sizeof(T), cudaMemcpyHostToDevice, q->stream);
+            yd = ys;
+        }
+        if (e != cudaSuccess)
+            break;
+        launch_device<T>(q->stream, kw::ceil_div(len, block_elems), threads, elems, len, alpha, xd, yd);
+        e = cudaGetLastError();
+        if (e == cudaSuccess && !y_dev) {
+            e = cudaEventRecord(q->ev_ready[s], q->stream);
+            if (e == cudaSuccess)
+                e = cudaStreamWaitEvent(q->aux, q->ev_ready[s], 0);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(y + off, ys, len * sizeof(T), cudaMemcpyDeviceToHost, q->aux);
+            if (e == cudaSuccess)
+                e = cudaEventRecord(q->ev_free[s], q->aux);
+        }
+        else if (e == cudaSuccess) {
+            e = cudaEventRecord(q->ev_free[s], q->stream);
+        }
+    }
+    if (e == cudaSuccess) {
+        e = cudaEventRecord(q->ev_join, q->aux);
+        if (e == cudaSuccess)
+            e = cudaStreamWaitEvent(q->stream, q->ev_join, 0);
+    }
+    if (e != cudaSuccess)
+        return kw::task_fail(q, std::string("axpy (host-staged): ") + cudaGetErrorString(e));
+    return kw::after_enqueue(q, "axpy");
+}
+
+template <typename T>
+kw_status axpy_entry(kw_queue qh, const kw_workdiv* wd, size_t n, T alpha, const T* x, T* y)
+{
+    KW_CHECK_QUEUE(qh);
+    auto* q = reinterpret_cast<kw::Queue*>(qh);
+    kw_workdiv def;
+    if (wd == nullptr) {
+        kw_status st = kw_axpy_default_workdiv(n, static_cast<int>(sizeof(T)), &def);
+        if (st != KW_OK)
+            return st;
+        wd = &def;
+    }
+    size_t blocks, limit;
+    uint32_t threads, elems;
+    kw_status st = validate_wd<T>(wd, n, blocks, threads, elems, limit);
+    if (st != KW_OK)
+        return st;
+    if (limit == 0)
+        return KW_OK;
+    if (x == nullptr || y == nullptr)
+        return kw::usage("axpy: null buffer");
+    kw::DeviceGuard g(q->device);
+    int xdev = -1, ydev = -1;
+    const bool x_dev = kw::pointer_kind(x, &xdev) == KW_MEM_DEVICE;
+    const bool y_dev = kw::pointer_kind(y, &ydev) == KW_MEM_DEVICE;
+    if ((x_dev && xdev != q->device) || (y_dev && ydev != q->device))
+        return kw::usage("axpy: buffer lives on a different device than the queue");
+    if (x_dev && y_dev) {
+        launch_device<T>(q->stream, blocks, threads, elems, limit, alpha, x, y);
+        return kw::after_enqueue(q, "axpy");
+    }
+    return run_staged<T>(q, threads, elems, limit, alpha, x, y, x_dev, y_dev);
+}
+
+} // namespace
+
+extern "C" {
+
+kw_status kw_axpy_default_workdiv(size_t n, int elem_size, kw_workdiv* out)
+{
+    if (!out)
+        return kw::usage("kw_axpy_default_workdiv: null output");
+    if (elem_size != 4 && elem_size != 8)
+        return kw::usage("kw_axpy_default_workdiv: element size must be 4 or 8");
+    // 256 threads x 4 vectors of 16 B per thread: 8 independent 128-bit loads in flight per
+    // thread, ~65k blocks at n = 2^28 (many waves over 148 SMs, no tail effect).
+    const size_t threads = 256, elems = elem_size == 4 ? 16 : 8;
+    kw_workdiv wd = {};
+    wd.dim = 1;
+    for (int k = 0; k < 3; ++k)
+        wd.blocks[k] = wd.threads[k] = wd.elems[k] = 1;
+    wd.threads[0] = threads;
+    wd.elems[0] = elems;
+    wd.blocks[0] = n == 0 ? 1 : kw::ceil_div(n, threads * elems);
+    *out = wd;
+    return KW_OK;
+}
+
+kw_status kw_axpy_f32(kw_queue q, const kw_workdiv* wd, size_t n, float alpha, const float* x, float* y)
+{
+    return axpy_entry<float>(q, wd, n, alpha, x, y);
+}
+
+kw_status kw_axpy_f64(kw_queue q, const kw_workdiv* wd, size_t n, double alpha, const double* x, double* y)
+{
+    return axpy_entry<double>(q, wd, n, alpha, x, y);
+}
+
+} // extern "C"

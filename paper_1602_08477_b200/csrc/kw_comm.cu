@@ -1,0 +1,192 @@
+// kw_comm.cu — multi-GPU plumbing of the row-sharded DGEMM (one process per GPU).
+//
+// The reference is single-process and has no collective at all; the B200
+// build adds exactly one: ncclBroadcast of DGEMM's B over NVLink 5 / NVSwitch.
+// AXPY shards by index range and needs no communication.
+//
+// Row-sharded DGEMM: rank r owns row block r of A and C. B (k x n) lives on the root and is
+// broadcast in column panels; panel j's broadcast (comm stream) overlaps panel j-1's DGEMM
+// (queue stream). Each C element is reduced entirely on one rank by the single-GPU kernel in
+// the same k order, so gathering the C row blocks reproduces the 1-GPU result bit for bit.
+#include "kw_common.cuh"
+
+#include <nccl.h>
+
+#include <cstring>
+#include <vector>
+
+namespace kw {
+kw_status dgemm_device(cudaStream_t s, int tile, size_t m, size_t n, size_t k, double alpha, const double* A,
+                       size_t lda, const double* B, size_t ldb, double beta, double* C, size_t ldc);
+}
+
+struct kw_comm_s {
+    ncclComm_t comm = nullptr;
+    int device = 0, world = 1, rank = 0;
+    cudaStream_t stream = nullptr; // broadcasts
+    std::vector<cudaEvent_t> panel_ready;
+    cudaEvent_t start = nullptr;
+};
+
+namespace {
+
+kw_status nccl_fail(const char* what, ncclResult_t r)
+{
+    kw::set_error(std::string(what) + ": " + ncclGetErrorString(r));
+    return KW_TASK;
+}
+
+kw_status ensure_events(kw_comm_s* c, int n)
+{
+    while (static_cast<int>(c->panel_ready.size()) < n) {
+        cudaEvent_t e;
+        cudaError_t err = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+        if (err != cudaSuccess)
+            return kw::cuda_fail("comm event", err);
+        c->panel_ready.push_back(e);
+    }
+    return KW_OK;
+}
+
+} // namespace
+
+extern "C" {
+
+kw_status kw_comm_unique_id(unsigned char id[128])
+{
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    if (!id)
+        return kw::usage("kw_comm_unique_id: null output");
+    ncclUniqueId uid;
+    ncclResult_t r = ncclGetUniqueId(&uid);
+    if (r != ncclSuccess)
+        return nccl_fail("ncclGetUniqueId", r);
+    std::memcpy(id, &uid, sizeof(uid));
+    return KW_OK;
+}
+
+kw_status kw_comm_init(kw_comm* out, int device, int world, int rank, const unsigned char id[128])
+{
+    if (!out || !id)
+        return kw::usage("kw_comm_init: null argument");
+    if (world < 1 || rank < 0 || rank >= world)
+        return kw::usage("kw_comm_init: rank must lie in [0, world)");
+    kw::DeviceGuard g(device);
+    auto* c = new kw_comm_s;
+    c->device = device;
+    c->world = world;
+    c->rank = rank;
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    ncclResult_t r = ncclCommInitRank(&c->comm, world, uid, rank);
+    if (r != ncclSuccess) {
+        delete c;
+        return nccl_fail("ncclCommInitRank", r);
+    }
+    cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess)
+        e = cudaEventCreateWithFlags(&c->start, cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+        ncclCommDestroy(c->comm);
+        delete c;
+        return kw::cuda_fail("comm stream", e);
+    }
+    *out = c;
+    return KW_OK;
+}
+
+kw_status kw_comm_destroy(kw_comm c)
+{
+    if (!c)
+        return KW_OK;
+    kw::DeviceGuard g(c->device);
+    cudaStreamSynchronize(c->stream);
+    for (cudaEvent_t e : c->panel_ready)
+        cudaEventDestroy(e);
+    cudaEventDestroy(c->start);
+    cudaStreamDestroy(c->stream);
+    ncclCommDestroy(c->comm);
+    delete c;
+    return KW_OK;
+}
+
+kw_status kw_comm_broadcast(kw_comm c, kw_queue qh, void* buf, size_t bytes, int root)
+{
+    KW_CHECK_QUEUE(qh);
+    if (!c)
+        return kw::usage("kw_comm_broadcast: null communicator");
+    if (root < 0 || root >= c->world)
+        return kw::usage("kw_comm_broadcast: root out of range");
+    auto* q = reinterpret_cast<kw::Queue*>(qh);
+    kw::DeviceGuard g(q->device);
+    ncclResult_t r = ncclBroadcast(buf, buf, bytes, ncclChar, root, c->comm, q->stream);
+    if (r != ncclSuccess)
+        return kw::task_fail(q, std::string("ncclBroadcast: ") + ncclGetErrorString(r));
+    return kw::after_enqueue(q, "broadcast");
+}
+
+kw_status kw_dgemm_rowsharded(kw_comm c, kw_queue qh, size_t m_local, size_t n, size_t k, double alpha,
+                              const double* A, size_t lda, const double* B, size_t ldb, double beta, double* C,
+                              size_t ldc, double* b_panels, int panels, int root)
+{
+    KW_CHECK_QUEUE(qh);
+    if (!c)
+        return kw::usage("dgemm_rowsharded: null communicator");
+    auto* q = reinterpret_cast<kw::Queue*>(qh);
+    if (q->device != c->device)
+        return kw::usage("dgemm_rowsharded: queue and communicator are on different devices");
+    if (root < 0 || root >= c->world)
+        return kw::usage("dgemm_rowsharded: root out of range");
+    if (panels < 1)
+        return kw::usage("dgemm_rowsharded: panels must be >= 1");
+    if (n == 0)
+        return KW_OK;
+    if (!b_panels || (k > 0 && !A) || (m_local > 0 && !C))
+        return kw::usage("dgemm_rowsharded: null buffer");
+    if (c->rank == root && k > 0 && (!B || ldb < n))
+        return kw::usage("dgemm_rowsharded: root needs B with ldb >= n");
+    if (k > 0 && lda < k)
+        return kw::usage("dgemm_rowsharded: lda smaller than k");
+    if (m_local > 0 && ldc < n)
+        return kw::usage("dgemm_rowsharded: ldc smaller than n");
+    // Panel widths: multiples of the 128-column tile so every panel starts on a tile boundary.
+    const size_t tile = 128;
+    size_t w = kw::ceil_div(kw::ceil_div(n, static_cast<size_t>(panels)), tile) * tile;
+    const int np = static_cast<int>(kw::ceil_div(n, w));
+    kw::DeviceGuard g(q->device);
+    kw_status st = ensure_events(c, np);
+    if (st != KW_OK)
+        return st;
+    cudaError_t e = cudaEventRecord(c->start, q->stream); // B and C may come from earlier tasks
+    if (e == cudaSuccess)
+        e = cudaStreamWaitEvent(c->stream, c->start, 0);
+    ncclResult_t r = ncclSuccess;
+    size_t off = 0;
+    for (int j = 0; j < np && e == cudaSuccess && r == ncclSuccess; ++j) {
+        const size_t n0 = static_cast<size_t>(j) * w, wj = n - n0 < w ? n - n0 : w;
+        double* panel = b_panels + off; // k x wj dense
+        if (k > 0) {
+            if (c->rank == root)
+                e = cudaMemcpy2DAsync(panel, wj * 8, B + n0, ldb * 8, wj * 8, k, cudaMemcpyDeviceToDevice, c->stream);
+            if (e == cudaSuccess && c->world > 1)
+                r = ncclBroadcast(panel, panel, k * wj * sizeof(double), ncclChar, root, c->comm, c->stream);
+        }
+        if (e == cudaSuccess)
+            e = cudaEventRecord(c->panel_ready[j], c->stream);
+        if (e == cudaSuccess)
+            e = cudaStreamWaitEvent(q->stream, c->panel_ready[j], 0);
+        if (e == cudaSuccess && m_local > 0) {
+            st = kw::dgemm_device(q->stream, 128, m_local, wj, k, alpha, A, lda, panel, wj, beta, C + n0, ldc);
+            if (st != KW_OK)
+                return kw::task_fail(q, kw::last_error());
+        }
+        off += k * wj;
+    }
+    if (r != ncclSuccess)
+        return kw::task_fail(q, std::string("ncclBroadcast: ") + ncclGetErrorString(r));
+    if (e != cudaSuccess)
+        return kw::task_fail(q, std::string("dgemm_rowsharded: ") + cudaGetErrorString(e));
+    return kw::after_enqueue(q, "dgemm_rowsharded");
+}
+
+} // extern "C"

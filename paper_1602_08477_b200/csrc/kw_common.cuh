@@ -1,0 +1,88 @@
+// kw_common.cuh — shared plumbing of libkw_b200.so: status/error reporting across the C-ABI,
+// the queue object (a CUDA stream standing in for kernelweave's Queue, queue.hpp:94-137) and
+// the launch bookkeeping every kernel entry point goes through.
+#pragma once
+
+#include "kw_b200.h"
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdio>
+#include <mutex>
+#include <string>
+
+namespace kw {
+
+// Thread-local message behind kw_last_error().
+void set_error(const std::string& msg);
+const std::string& last_error();
+
+// Number of kernels launched by this library (the bench's gpu_launches claim).
+extern std::atomic<uint64_t> g_launches;
+
+struct Queue {
+    int device = 0;
+    int flavor = KW_QUEUE_SYNC;
+    cudaStream_t stream = nullptr; // in-order FIFO of the queue
+    cudaStream_t aux = nullptr;    // second stream for overlapped copies (host-staged paths)
+    std::mutex mu;
+    size_t failed = 0;
+    std::string first_failure;
+    bool shut = false;
+    // Device scratch for host-staged execution (grown on demand, freed with the queue).
+    void* scratch = nullptr;
+    size_t scratch_bytes = 0;
+    static constexpr int kRing = 4;
+    cudaEvent_t ev_ready[kRing] = {};  // chunk computed -> D2H may start
+    cudaEvent_t ev_free[kRing] = {};   // chunk drained  -> slot reusable
+    cudaEvent_t ev_join = nullptr;
+};
+
+// RAII device selector: the reference's queues are bound to one device; every entry point
+// makes that device current for its duration.
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev)
+    {
+        cudaGetDevice(&prev);
+        if (prev != dev)
+            cudaSetDevice(dev);
+    }
+    ~DeviceGuard()
+    {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev)
+            cudaSetDevice(prev);
+    }
+};
+
+kw_status usage(const std::string& msg);
+kw_status resource(const std::string& msg);
+kw_status cuda_fail(const char* what, cudaError_t e);
+
+// Records a failed task on the queue (reported by the next kw_queue_wait) and returns KW_TASK.
+kw_status task_fail(Queue* q, const std::string& msg);
+
+// After enqueuing one task: surfaces launch errors into the queue's failure list and, for a
+// Sync queue, completes the task before returning (queue.cpp:21-23, 57-72).
+kw_status after_enqueue(Queue* q, const char* what);
+
+// Ensures q->scratch holds at least `bytes` of device memory on q's device.
+kw_status ensure_scratch(Queue* q, size_t bytes);
+
+// Classifies a pointer: KW_MEM_PAGEABLE / KW_MEM_PINNED / KW_MEM_DEVICE.
+int pointer_kind(const void* p, int* device);
+
+inline size_t ceil_div(size_t a, size_t b) { return (a + b - 1) / b; }
+
+} // namespace kw
+
+#define KW_CHECK_QUEUE(q)                                                                          \
+    do {                                                                                           \
+        if ((q) == nullptr)                                                                        \
+            return kw::usage("null queue");                                                        \
+        if (reinterpret_cast<kw::Queue*>(q)->shut)                                                 \
+            return kw::usage("queue: enqueue after shutdown");                                     \
+    } while (0)

@@ -1,0 +1,592 @@
+// kw_dgemm.cu — K2 tiled DGEMM (FP64 DMMA tensor cores) and K3 naive bit-exact DGEMM, sm_100a.
+//
+// Reference: GemmTiledKernel (/root/reference/proj/core/src/kernels/gemm.cpp:40-118),
+// GemmNaiveKernel (gemm.cpp:11-38), gemmReference oracle (core/src/kernels/reference.cpp:14-26).
+//
+// K2 design (FP64 on Blackwell): tcgen05.mma has no f64 kind, so FP64 tensor work is the legacy
+// DMMA.8x8x4 (mma.sync.m8n8k4.f64). Measured on this pool's B200: DMMA 37.2 TFLOP/s vs DFMA
+// 34.1 TFLOP/s peak (tools/probe/probe.cu), and DMMA needs 8x fewer operand registers per FMA,
+// so the block tile is computed with DMMA fed from shared memory.
+//   * block tile BM x BN (128 x 128), k-tile BK = 16, 8 warps each owning a 64 x 32 warp tile
+//     = 8 x 4 DMMA accumulators (64 fp64 registers per lane);
+//   * global -> shared through a STAGES-deep cp.async (LDGSTS) ring, zero-filling ragged
+//     edges in hardware (src-size < cp-size), which is the reference's zero-padded staging
+//     (gemm.cpp:77-92) without any branch in the math loop;
+//   * shared layouts XOR-swizzled at 16-byte granularity so every fragment load (LDS.64) is
+//     conflict-free: A[m][k] chunk (k/2) ^ (m & 7); B[k][n] chunk (n/2) ^ ((k & 1) << 2);
+//   * epilogue fl(fl(alpha*acc) + fl(beta*c)) exactly as gemm.cpp:115 / reference.cpp:24
+//     (C is always read, also for beta == 0);
+//   * blocks rasterised in groups of 8 tile-rows so co-resident CTAs share A and B panels in L2.
+// Numerics: per output element the K products are accumulated in ascending k-tile order by
+// DMMA (fused multiply-add), hence |dC| <= (K+4)*2^-53*|C_ref| instead of bit equality
+// (SURVEY.md §7 "Hard parts" 6). K3 below is the bit-exact mode.
+#include "kw_common.cuh"
+
+#include <climits>
+
+namespace {
+
+// ------------------------------------------------------------------------------------------
+// PTX helpers
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p)
+{
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int src_bytes)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(src_bytes));
+}
+
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src, int src_bytes)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(src_bytes));
+}
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+
+template <int N>
+__device__ __forceinline__ void cp_async_wait()
+{
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// D += A(8x4, row) * B(4x8, col), fp64. Lane (g = lane/4, t = lane%4) supplies A[g][t] and
+// B[t][g] and owns D[g][2t], D[g][2t+1].
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b)
+{
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+        : "+d"(d0), "+d"(d1)
+        : "d"(a), "d"(b));
+}
+
+// ------------------------------------------------------------------------------------------
+// K2: DMMA tiled kernel
+// ------------------------------------------------------------------------------------------
+template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_>
+struct TileCfg {
+    static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_;
+    static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
+    static constexpr int THREADS = 32 * WARPS_M * WARPS_N;
+    static constexpr int MT = WM / 8, NT = WN / 8; // DMMA tiles per warp
+    static constexpr int A_STAGE = BM * BK, B_STAGE = BK * BN; // doubles
+    static constexpr size_t SMEM = static_cast<size_t>(STAGES) * (A_STAGE + B_STAGE) * sizeof(double);
+    static_assert(BK == 16, "A swizzle assumes 8 16-byte chunks per A row");
+    static_assert(BN % 16 == 0 && BM % 8 == 0, "tile shape");
+    static_assert((BM * BK / 2) % THREADS == 0 && (BK * BN / 2) % THREADS == 0, "load split");
+};
+
+// Element offsets (in doubles) inside one stage.
+template <int BK>
+__device__ __forceinline__ int a_off(int m, int k)
+{
+    return m * BK + ((((k >> 1) ^ (m & 7))) << 1) + (k & 1);
+}
+template <int BN>
+__device__ __forceinline__ int b_off(int k, int n)
+{
+    return k * BN + ((((n >> 1) ^ ((k & 1) << 2))) << 1) + (n & 1);
+}
+
+struct GemmParams {
+    int m, n, k;
+    double alpha, beta;
+    const double* a;
+    long long lda;
+    const double* b;
+    long long ldb;
+    double* c;
+    long long ldc;
+    int tiles_m, tiles_n;
+};
+
+template <class Cfg, bool VEC16>
+__device__ __forceinline__ void load_stage(const GemmParams& p, double* sA, double* sB, int bm, int bn, int k0,
+                                           int tid)
+{
+    // A tile: BM rows x BK cols = BM * (BK/2) chunks of two doubles.
+    constexpr int A_CHUNKS = Cfg::BM * Cfg::BK / 2;
+#pragma unroll
+    for (int i = 0; i < A_CHUNKS / Cfg::THREADS; ++i) {
+        const int c = tid + i * Cfg::THREADS;
+        const int row = c / (Cfg::BK / 2), kc = c % (Cfg::BK / 2);
+        const int gm = bm + row, gk = k0 + kc * 2;
+        int valid = 0;
+        if (gm < p.m) {
+            valid = p.k - gk;
+            valid = valid < 0 ? 0 : (valid > 2 ? 2 : valid);
+        }
+        const double* src = valid > 0 ? p.a + gm * p.lda + gk : p.a;
+        const uint32_t dst = smem_u32(sA + a_off<Cfg::BK>(row, kc * 2));
+        if (VEC16) {
+            cp_async16(dst, src, valid * 8);
+        }
+        else {
+            cp_async8(dst, src, valid >= 1 ? 8 : 0);
+            cp_async8(dst + 8, valid >= 2 ? src + 1 : p.a, valid >= 2 ? 8 : 0);
+        }
+    }
+    // B tile: BK rows x BN cols.
+    constexpr int B_CHUNKS = Cfg::BK * Cfg::BN / 2;
+#pragma unroll
+    for (int i = 0; i < B_CHUNKS / Cfg::THREADS; ++i) {
+        const int c = tid + i * Cfg::THREADS;
+        const int row = c / (Cfg::BN / 2), nc = c % (Cfg::BN / 2);
+        const int gk = k0 + row, gn = bn + nc * 2;
+        int valid = 0;
+        if (gk < p.k) {
+            valid = p.n - gn;
+            valid = valid < 0 ? 0 : (valid > 2 ? 2 : valid);
+        }
+        const double* src = valid > 0 ? p.b + gk * p.ldb + gn : p.b;
+        const uint32_t dst = smem_u32(sB + b_off<Cfg::BN>(row, nc * 2));
+        if (VEC16) {
+            cp_async16(dst, src, valid * 8);
+        }
+        else {
+            cp_async8(dst, src, valid >= 1 ? 8 : 0);
+            cp_async8(dst + 8, valid >= 2 ? src + 1 : p.b, valid >= 2 ? 8 : 0);
+        }
+    }
+}
+
+template <class Cfg, bool VEC16>
+__global__ void __launch_bounds__(Cfg::THREADS, 1) dgemm_dmma_kernel(GemmParams p)
+{
+    extern __shared__ __align__(128) double smem[];
+    double* sA = smem;
+    double* sB = smem + Cfg::STAGES * Cfg::A_STAGE;
+
+    // Grouped rasterisation: runs of 8 tile-rows sweep the tile-columns together.
+    constexpr int GROUP = 8;
+    const int tile = blockIdx.x;
+    const int per_group = GROUP * p.tiles_n;
+    const int group = tile / per_group;
+    const int first_m = group * GROUP;
+    const int gsize = (p.tiles_m - first_m) < GROUP ? (p.tiles_m - first_m) : GROUP;
+    const int in_group = tile - group * per_group;
+    const int tm = first_m + in_group % gsize;
+    const int tn = in_group / gsize;
+    const int bm = tm * Cfg::BM, bn = tn * Cfg::BN;
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int wm = (warp / Cfg::WARPS_N) * Cfg::WM;
+    const int wn = (warp % Cfg::WARPS_N) * Cfg::WN;
+    const int g = lane >> 2, t = lane & 3;
+
+    double acc[Cfg::MT][Cfg::NT][2];
+#pragma unroll
+    for (int i = 0; i < Cfg::MT; ++i)
+#pragma unroll
+        for (int j = 0; j < Cfg::NT; ++j)
+            acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    const int ktiles = (p.k + Cfg::BK - 1) / Cfg::BK;
+#pragma unroll
+    for (int s = 0; s < Cfg::STAGES - 1; ++s) {
+        if (s < ktiles)
+            load_stage<Cfg, VEC16>(p, sA + s * Cfg::A_STAGE, sB + s * Cfg::B_STAGE, bm, bn, s * Cfg::BK, tid);
+        cp_async_commit();
+    }
+
+    for (int kt = 0; kt < ktiles; ++kt) {
+        cp_async_wait<Cfg::STAGES - 2>();
+        __syncthreads();
+        {
+            const int nk = kt + Cfg::STAGES - 1;
+            if (nk < ktiles) {
+                const int s = nk % Cfg::STAGES;
+                load_stage<Cfg, VEC16>(p, sA + s * Cfg::A_STAGE, sB + s * Cfg::B_STAGE, bm, bn, nk * Cfg::BK, tid);
+            }
+            cp_async_commit();
+        }
+        const int s = kt % Cfg::STAGES;
+        const double* a_s = sA + s * Cfg::A_STAGE;
+        const double* b_s = sB + s * Cfg::B_STAGE;
+#pragma unroll
+        for (int kk = 0; kk < Cfg::BK / 4; ++kk) {
+            double af[Cfg::MT], bf[Cfg::NT];
+            const int k = kk * 4 + t;
+#pragma unroll
+            for (int i = 0; i < Cfg::MT; ++i)
+                af[i] = a_s[a_off<Cfg::BK>(wm + i * 8 + g, k)];
+#pragma unroll
+            for (int j = 0; j < Cfg::NT; ++j)
+                bf[j] = b_s[b_off<Cfg::BN>(k, wn + j * 8 + g)];
+#pragma unroll
+            for (int i = 0; i < Cfg::MT; ++i)
+#pragma unroll
+                for (int j = 0; j < Cfg::NT; ++j)
+                    dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
+    }
+    cp_async_wait<0>();
+
+    // Epilogue: C = fl(fl(alpha*acc) + fl(beta*c)).
+    const bool c_vec = (p.ldc % 2 == 0) && (reinterpret_cast<uintptr_t>(p.c) % 16 == 0);
+#pragma unroll
+    for (int i = 0; i < Cfg::MT; ++i) {
+        const int row = bm + wm + i * 8 + g;
+        if (row >= p.m)
+            continue;
+        double* crow = p.c + row * p.ldc;
+#pragma unroll
+        for (int j = 0; j < Cfg::NT; ++j) {
+            const int col = bn + wn + j * 8 + 2 * t;
+            if (c_vec && col + 1 < p.n) {
+                double2 old = *reinterpret_cast<const double2*>(crow + col);
+                double2 out;
+                out.x = __dadd_rn(__dmul_rn(p.alpha, acc[i][j][0]), __dmul_rn(p.beta, old.x));
+                out.y = __dadd_rn(__dmul_rn(p.alpha, acc[i][j][1]), __dmul_rn(p.beta, old.y));
+                *reinterpret_cast<double2*>(crow + col) = out;
+            }
+            else {
+                if (col < p.n)
+                    crow[col] = __dadd_rn(__dmul_rn(p.alpha, acc[i][j][0]), __dmul_rn(p.beta, crow[col]));
+                if (col + 1 < p.n)
+                    crow[col + 1] = __dadd_rn(__dmul_rn(p.alpha, acc[i][j][1]), __dmul_rn(p.beta, crow[col + 1]));
+            }
+        }
+    }
+}
+
+using Cfg128 = TileCfg<128, 128, 16, 64, 32, 4>;
+using Cfg64 = TileCfg<64, 64, 16, 32, 32, 4>;
+
+template <class Cfg>
+kw_status launch_dmma(cudaStream_t s, const GemmParams& p0)
+{
+    GemmParams p = p0;
+    p.tiles_m = static_cast<int>(kw::ceil_div(p.m, Cfg::BM));
+    p.tiles_n = static_cast<int>(kw::ceil_div(p.n, Cfg::BN));
+    const long long tiles = static_cast<long long>(p.tiles_m) * p.tiles_n;
+    if (tiles > INT_MAX)
+        return kw::usage("dgemm: problem too large for the tile grid");
+    const bool vec16 = (p.lda % 2 == 0) && (p.ldb % 2 == 0) && (reinterpret_cast<uintptr_t>(p.a) % 16 == 0) &&
+                       (reinterpret_cast<uintptr_t>(p.b) % 16 == 0);
+    static bool attr_set[2] = {false, false};
+    auto kern = vec16 ? dgemm_dmma_kernel<Cfg, true> : dgemm_dmma_kernel<Cfg, false>;
+    if (!attr_set[vec16]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(Cfg::SMEM));
+        if (e != cudaSuccess)
+            return kw::cuda_fail("dgemm: cudaFuncSetAttribute", e);
+        attr_set[vec16] = true;
+    }
+    kern<<<static_cast<unsigned>(tiles), Cfg::THREADS, Cfg::SMEM, s>>>(p);
+    kw::g_launches.fetch_add(1, std::memory_order_relaxed);
+    return KW_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// K3: GemmNaiveKernel on the GPU — bit-exact. Grid thread (r, c) owns rows [r*er, r*er+er) x
+// cols [c*ec, c*ec+ec) clamped at (m, n) (gemm.cpp:13-22); per element one ascending-p dot
+// product from +0.0 with separately rounded products and sums, then the two-rounding epilogue
+// (gemm.cpp:30-36). Axis rule: the last (fastest) work-division component is CUDA x.
+// ------------------------------------------------------------------------------------------
+__global__ void dgemm_naive_kernel(GemmParams p, int er, int ec)
+{
+    const long long r = static_cast<long long>(blockIdx.y) * blockDim.y + threadIdx.y;
+    const long long c = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const long long row_first = r * er, col_first = c * ec;
+    if (row_first >= p.m || col_first >= p.n)
+        return;
+    const long long row_end = row_first + er < p.m ? row_first + er : p.m;
+    const long long col_end = col_first + ec < p.n ? col_first + ec : p.n;
+    for (long long row = row_first; row < row_end; ++row) {
+        for (long long col = col_first; col < col_end; ++col) {
+            double acc = 0.0;
+            const double* ap = p.a + row * p.lda;
+            const double* bp = p.b + col;
+            for (int q = 0; q < p.k; ++q)
+                acc = __dadd_rn(acc, __dmul_rn(ap[q], bp[q * p.ldb]));
+            double* cp = p.c + row * p.ldc + col;
+            *cp = __dadd_rn(__dmul_rn(p.alpha, acc), __dmul_rn(p.beta, *cp));
+        }
+    }
+}
+
+kw_status validate_gemm(size_t m, size_t n, size_t k, const double* A, size_t lda, const double* B, size_t ldb,
+                        const double* C, size_t ldc)
+{
+    if (m > INT_MAX || n > INT_MAX || k > INT_MAX)
+        return kw::usage("dgemm: extents exceed 2^31-1");
+    if (m == 0 || n == 0)
+        return KW_OK;
+    if (!A && k > 0)
+        return kw::usage("dgemm: null A");
+    if (!B && k > 0)
+        return kw::usage("dgemm: null B");
+    if (!C)
+        return kw::usage("dgemm: null C");
+    if (k > 0 && lda < k)
+        return kw::usage("dgemm: lda smaller than k");
+    if (k > 0 && ldb < n)
+        return kw::usage("dgemm: ldb smaller than n");
+    if (ldc < n)
+        return kw::usage("dgemm: ldc smaller than n");
+    return KW_OK;
+}
+
+// Picks the DMMA tile configuration named by a GPU work division (gemmTiledWorkDiv for the
+// GPU back-end): threadsPerBlock x elementsPerThread == (BM, BN) and one block per tile.
+kw_status tile_from_wd(const kw_workdiv* wd, size_t m, size_t n, int* tile)
+{
+    if (wd == nullptr) {
+        *tile = 128;
+        return KW_OK;
+    }
+    if (wd->dim != 2)
+        return kw::usage("dgemm: the tiled kernel runs on a 2-D (rows, cols) work division");
+    const size_t tm = wd->threads[0] * wd->elems[0], tn = wd->threads[1] * wd->elems[1];
+    const size_t thr = wd->threads[0] * wd->threads[1];
+    int t = 0;
+    if (tm == 128 && tn == 128 && thr == static_cast<size_t>(Cfg128::THREADS))
+        t = 128;
+    else if (tm == 64 && tn == 64 && thr == static_cast<size_t>(Cfg64::THREADS))
+        t = 64;
+    else
+        return kw::usage("dgemm: unsupported GPU tile configuration (supported: 128x128 tile with 256 threads, "
+                         "64x64 tile with 128 threads; use gemmTiledWorkDiv(GpuCudaRt, m, n, tile))");
+    if (wd->blocks[0] * tm < m || wd->blocks[1] * tn < n)
+        return kw::usage("dgemm: work division does not cover the m x n output");
+    *tile = t;
+    return KW_OK;
+}
+
+kw_status launch_tiled(cudaStream_t s, int tile, const GemmParams& p)
+{
+    if (tile == 64)
+        return launch_dmma<Cfg64>(s, p);
+    return launch_dmma<Cfg128>(s, p);
+}
+
+GemmParams make_params(size_t m, size_t n, size_t k, double alpha, const double* A, size_t lda, const double* B,
+                       size_t ldb, double beta, double* C, size_t ldc)
+{
+    GemmParams p;
+    p.m = static_cast<int>(m);
+    p.n = static_cast<int>(n);
+    p.k = static_cast<int>(k);
+    p.alpha = alpha;
+    p.beta = beta;
+    p.a = A;
+    p.lda = static_cast<long long>(lda);
+    p.b = B;
+    p.ldb = static_cast<long long>(ldb);
+    p.c = C;
+    p.ldc = static_cast<long long>(ldc);
+    p.tiles_m = p.tiles_n = 0;
+    return p;
+}
+
+size_t round2(size_t v) { return (v + 1) & ~static_cast<size_t>(1); }
+
+// Host-resident operands (e2e path): B is staged once, then row panels of A and C stream
+// through a two-slot ring — H2D(A_p, C_p) + DGEMM on the queue stream, D2H(C_p) on the aux
+// stream — so panel p+1's upload overlaps panel p's download and compute. Each C element is
+// produced by the same kernel in the same k order, so panelling changes no bit.
+kw_status dgemm_staged(kw::Queue* q, int tile, size_t m, size_t n, size_t k, double alpha, const double* A,
+                       size_t lda, const double* B, size_t ldb, double beta, double* C, size_t ldc, bool a_dev,
+                       bool b_dev, bool c_dev)
+{
+    const size_t ldbs = round2(n), ldas = round2(k == 0 ? 1 : k), ldcs = round2(n);
+    const size_t row_bytes = (ldas + ldcs) * sizeof(double);
+    size_t R = (64u << 20) / row_bytes;
+    R = R < 128 ? 128 : R / 128 * 128;
+    if (R > m)
+        R = m;
+    const int ring = 2;
+    const size_t b_bytes = b_dev ? 0 : k * ldbs * sizeof(double);
+    const size_t slot_bytes = R * row_bytes;
+    kw_status st = kw::ensure_scratch(q, b_bytes + ring * slot_bytes + 256);
+    if (st != KW_OK)
+        return st;
+    char* base = static_cast<char*>(q->scratch);
+    const double* Bd = B;
+    size_t ldbd = ldb;
+    cudaError_t e = cudaSuccess;
+    if (!b_dev && k > 0) {
+        double* bs = reinterpret_cast<double*>(base);
+        e = cudaMemcpy2DAsync(bs, ldbs * 8, B, ldb * 8, n * 8, k, cudaMemcpyHostToDevice, q->stream);
+        Bd = bs;
+        ldbd = ldbs;
+    }
+    char* slots = base + ((b_bytes + 255) / 256) * 256;
+    const size_t npanels = kw::ceil_div(m, R);
+    for (size_t pi = 0; pi < npanels && e == cudaSuccess; ++pi) {
+        const int s = static_cast<int>(pi % ring);
+        const size_t r0 = pi * R, rows = m - r0 < R ? m - r0 : R;
+        double* as = reinterpret_cast<double*>(slots + s * slot_bytes);
+        double* cs = as + R * ldas;
+        if (pi >= static_cast<size_t>(ring))
+            e = cudaStreamWaitEvent(q->stream, q->ev_free[s], 0);
+        const double* Ad = A + r0 * lda;
+        size_t ldad = lda;
+        double* Cd = C + r0 * ldc;
+        size_t ldcd = ldc;
+        if (e == cudaSuccess && !a_dev && k > 0) {
+            e = cudaMemcpy2DAsync(as, ldas * 8, A + r0 * lda, lda * 8, k * 8, rows, cudaMemcpyHostToDevice, q->stream);
+            Ad = as;
+            ldad = ldas;
+        }
+        if (e == cudaSuccess && !c_dev) {
+            e = cudaMemcpy2DAsync(cs, ldcs * 8, C + r0 * ldc, ldc * 8, n * 8, rows, cudaMemcpyHostToDevice, q->stream);
+            Cd = cs;
+            ldcd = ldcs;
+        }
+        if (e != cudaSuccess)
+            break;
+        st = launch_tiled(q->stream, tile, make_params(rows, n, k, alpha, Ad, ldad, Bd, ldbd, beta, Cd, ldcd));
+        if (st != KW_OK)
+            return st;
+        e = cudaGetLastError();
+        if (e == cudaSuccess && !c_dev) {
+            e = cudaEventRecord(q->ev_ready[s], q->stream);
+            if (e == cudaSuccess)
+                e = cudaStreamWaitEvent(q->aux, q->ev_ready[s], 0);
+            if (e == cudaSuccess)
+                e = cudaMemcpy2DAsync(C + r0 * ldc, ldc * 8, cs, ldcs * 8, n * 8, rows, cudaMemcpyDeviceToHost, q->aux);
+            if (e == cudaSuccess)
+                e = cudaEventRecord(q->ev_free[s], q->aux);
+        }
+        else if (e == cudaSuccess) {
+            e = cudaEventRecord(q->ev_free[s], q->stream);
+        }
+    }
+    if (e == cudaSuccess) {
+        e = cudaEventRecord(q->ev_join, q->aux);
+        if (e == cudaSuccess)
+            e = cudaStreamWaitEvent(q->stream, q->ev_join, 0);
+    }
+    if (e != cudaSuccess)
+        return kw::task_fail(q, std::string("dgemm (host-staged): ") + cudaGetErrorString(e));
+    return kw::after_enqueue(q, "dgemm");
+}
+
+} // namespace
+
+namespace kw {
+// Used by the row-sharded driver (kw_comm.cu).
+kw_status dgemm_device(cudaStream_t s, int tile, size_t m, size_t n, size_t k, double alpha, const double* A,
+                       size_t lda, const double* B, size_t ldb, double beta, double* C, size_t ldc)
+{
+    if (m == 0 || n == 0)
+        return KW_OK;
+    return launch_tiled(s, tile, make_params(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc));
+}
+} // namespace kw
+
+extern "C" {
+
+kw_status kw_dgemm_default_workdiv(size_t m, size_t n, size_t tile, kw_workdiv* out)
+{
+    if (!out)
+        return kw::usage("kw_dgemm_default_workdiv: null output");
+    if (tile == 0)
+        tile = 128;
+    kw_workdiv wd = {};
+    wd.dim = 2;
+    for (int k = 0; k < 3; ++k)
+        wd.blocks[k] = wd.threads[k] = wd.elems[k] = 1;
+    if (tile == 128) {
+        wd.threads[0] = 16;
+        wd.threads[1] = 16;
+        wd.elems[0] = 8;
+        wd.elems[1] = 8;
+    }
+    else if (tile == 64) {
+        wd.threads[0] = 8;
+        wd.threads[1] = 16;
+        wd.elems[0] = 8;
+        wd.elems[1] = 4;
+    }
+    else {
+        return kw::usage("gemmTiledWorkDiv: GPU tile edge must be 64 or 128");
+    }
+    wd.blocks[0] = kw::ceil_div(m == 0 ? 1 : m, tile);
+    wd.blocks[1] = kw::ceil_div(n == 0 ? 1 : n, tile);
+    *out = wd;
+    return KW_OK;
+}
+
+kw_status kw_dgemm(kw_queue qh, const kw_workdiv* wd, size_t m, size_t n, size_t k, double alpha, const double* A,
+                   size_t lda, const double* B, size_t ldb, double beta, double* C, size_t ldc)
+{
+    KW_CHECK_QUEUE(qh);
+    auto* q = reinterpret_cast<kw::Queue*>(qh);
+    kw_status st = validate_gemm(m, n, k, A, lda, B, ldb, C, ldc);
+    if (st != KW_OK)
+        return st;
+    int tile = 128;
+    st = tile_from_wd(wd, m, n, &tile);
+    if (st != KW_OK)
+        return st;
+    if (m == 0 || n == 0)
+        return KW_OK;
+    kw::DeviceGuard g(q->device);
+    int da = -1, db = -1, dc = -1;
+    const bool a_dev = k == 0 || kw::pointer_kind(A, &da) == KW_MEM_DEVICE;
+    const bool b_dev = k == 0 || kw::pointer_kind(B, &db) == KW_MEM_DEVICE;
+    const bool c_dev = kw::pointer_kind(C, &dc) == KW_MEM_DEVICE;
+    if ((da >= 0 && a_dev && da != q->device) || (db >= 0 && b_dev && db != q->device) ||
+        (c_dev && dc != q->device))
+        return kw::usage("dgemm: buffer lives on a different device than the queue");
+    if (a_dev && b_dev && c_dev) {
+        st = launch_tiled(q->stream, tile, make_params(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc));
+        if (st != KW_OK)
+            return kw::task_fail(q, kw::last_error());
+        return kw::after_enqueue(q, "dgemm");
+    }
+    return dgemm_staged(q, tile, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, a_dev, b_dev, c_dev);
+}
+
+kw_status kw_dgemm_naive(kw_queue qh, const kw_workdiv* wd, size_t m, size_t n, size_t k, double alpha,
+                         const double* A, size_t lda, const double* B, size_t ldb, double beta, double* C, size_t ldc)
+{
+    KW_CHECK_QUEUE(qh);
+    auto* q = reinterpret_cast<kw::Queue*>(qh);
+    kw_status st = validate_gemm(m, n, k, A, lda, B, ldb, C, ldc);
+    if (st != KW_OK)
+        return st;
+    kw_workdiv def = {};
+    if (wd == nullptr) {
+        // GPU thread-level shape of gemmNaiveWorkDiv: (1, 1) elements, 8 x 32 threads.
+        def.dim = 2;
+        for (int i = 0; i < 3; ++i)
+            def.blocks[i] = def.threads[i] = def.elems[i] = 1;
+        def.threads[0] = 8;
+        def.threads[1] = 32;
+        def.blocks[0] = kw::ceil_div(m == 0 ? 1 : m, 8);
+        def.blocks[1] = kw::ceil_div(n == 0 ? 1 : n, 32);
+        wd = &def;
+    }
+    if (wd->dim != 2)
+        return kw::usage("dgemm_naive: the naive kernel runs on a 2-D (rows, cols) work division");
+    for (int i = 0; i < 2; ++i)
+        if (wd->blocks[i] == 0 || wd->threads[i] == 0 || wd->elems[i] == 0)
+            return kw::usage("WorkDiv: every level extent is at least 1");
+    if (wd->threads[0] * wd->threads[1] > 1024 || wd->threads[1] > 1024 || wd->threads[0] > 1024)
+        return kw::usage("dgemm_naive: threadsPerBlock exceeds the sm_100a block limit of 1024");
+    if (wd->blocks[0] > 65535 || wd->blocks[1] > static_cast<size_t>(INT_MAX))
+        return kw::usage("dgemm_naive: blocksPerGrid exceeds the grid limits");
+    if (wd->elems[0] > INT_MAX || wd->elems[1] > INT_MAX)
+        return kw::usage("dgemm_naive: elementsPerThread too large");
+    if (m == 0 || n == 0)
+        return KW_OK;
+    kw::DeviceGuard g(q->device);
+    int d = -1;
+    if (kw::pointer_kind(C, &d) != KW_MEM_DEVICE || (k > 0 && (kw::pointer_kind(A, &d) != KW_MEM_DEVICE ||
+                                                               kw::pointer_kind(B, &d) != KW_MEM_DEVICE)))
+        return kw::usage("dgemm_naive: operands must be device buffers");
+    dim3 grid(static_cast<unsigned>(wd->blocks[1]), static_cast<unsigned>(wd->blocks[0]));
+    dim3 block(static_cast<unsigned>(wd->threads[1]), static_cast<unsigned>(wd->threads[0]));
+    dgemm_naive_kernel<<<grid, block, 0, q->stream>>>(make_params(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc),
+                                                       static_cast<int>(wd->elems[0]), static_cast<int>(wd->elems[1]));
+    kw::g_launches.fetch_add(1, std::memory_order_relaxed);
+    return kw::after_enqueue(q, "dgemm_naive");
+}
+
+} // extern "C"

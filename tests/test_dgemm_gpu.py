@@ -1,0 +1,232 @@
+"""GPU parity: K2 tiled DGEMM (DMMA) and K3 naive DGEMM (bit-exact) through the C-ABI.
+
+Tolerance for K2 (stated in SURVEY.md §7 "Hard parts" 6 / DESIGN.md):
+    |C_gpu - C_ref| <= (K + 4) * 2^-53 * |C_ref|   elementwise,
+where C_ref is gemmReference (oracle). K3 must be bitwise equal. Mirrors test_kernels.cpp:114-306
+and acceptance criterion 1's GEMM half (acceptance.cpp:117-155)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from paper_1602_08477_b200 import _lib as L
+from paper_1602_08477_b200 import kernelweave as kw
+
+pytestmark = pytest.mark.gpu
+GPU = kw.BackendKind.GpuCudaRt
+U = 2.0 ** -53
+
+
+def h(v):
+    return f"{v:016x}"
+
+
+def mat(dev, a, rows=None, cols=None, align=64):
+    a = np.asarray(a, dtype=np.float64)
+    r, c = a.shape
+    b = kw.Buffer(dev, kw.IndexVec(rows or r, cols or c), 8, align)
+    if rows is None and cols is None:
+        b.upload(a)
+    else:
+        full = np.zeros((rows or r, cols or c))
+        full[:r, :c] = a
+        b.upload(full)
+    return b
+
+
+def within_tol(got, ref, k):
+    err = np.abs(got - ref)
+    bound = (k + 4) * U * np.abs(ref)
+    return bool(np.all(err <= bound)), float(np.max(err / np.maximum(np.abs(ref), 1e-300)) / ((k + 4) * U))
+
+
+def tiled(dev, alpha, beta, a, b, c, tile=128, align=64):
+    m, k = a.shape
+    n = b.shape[1]
+    A, B, Cb = mat(dev, a, align=align), mat(dev, b, align=align), mat(dev, c, align=align)
+    kw.executeTask(GPU, kw.gemmTiledWorkDiv(GPU, m, n, tile), kw.GemmTiledKernel(),
+                   kw.GemmArgs(m, n, k, alpha, beta, A, B, Cb, tile))
+    return Cb.download()
+
+
+def naive(dev, alpha, beta, a, b, c, tpb=4, ept=4):
+    m, k = a.shape
+    n = b.shape[1]
+    A, B, Cb = mat(dev, a), mat(dev, b), mat(dev, c)
+    kw.executeTask(GPU, kw.gemmNaiveWorkDiv(GPU, m, n, tpb, ept), kw.GemmNaiveKernel(),
+                   kw.GemmArgs(m, n, k, alpha, beta, A, B, Cb))
+    return Cb.download()
+
+
+def test_gemm_closed_forms(gpu, oracle):
+    rng = oracle.MT64(seed=7)
+    ident = np.eye(4)
+    b = rng.fill_uniform(16).reshape(4, 4)
+    c = rng.fill_uniform(16).reshape(4, 4)
+    for run in (tiled, naive):
+        assert np.array_equal(run(gpu, 1.0, 0.0, ident, b, c), b)
+        a2 = np.array([[1.0, 2.0], [3.0, 4.0]])
+        b2 = np.array([[5.0, 6.0], [7.0, 8.0]])
+        assert run(gpu, 1.0, 0.0, a2, b2, np.zeros((2, 2))).tolist() == [[19, 22], [43, 50]]
+        c3 = rng.fill_uniform(16).reshape(4, 4)
+        assert np.array_equal(run(gpu, 0.0, 1.0, ident, b, c3), c3)
+        assert run(gpu, 2.0, 10.0, np.array([[3.0]]), np.array([[5.0]]), np.array([[7.0]]))[0, 0] == 100.0
+
+
+@pytest.mark.parametrize("case", [4, 5])
+def test_golden_workloads(gpu, oracle, golden, case):
+    c = golden["workloads"][case]
+    alpha, beta, a, b, cin = oracle.workload_gemm(c["n"], c["seed"], "gemm-tiled")
+    ref = oracle.gemm(alpha, beta, a, b, cin)
+    assert h(oracle.fnv1a64(ref)) == c["c_out_digest"]
+    # K3 naive: bitwise equal to the reference digest
+    assert h(oracle.fnv1a64(naive(gpu, alpha, beta, a, b, cin))) == c["c_out_digest"]
+    for tile in (64, 128):
+        ok, worst = within_tol(tiled(gpu, alpha, beta, a, b, cin, tile), ref, c["n"])
+        assert ok, worst
+
+
+def test_naive_bitwise_random_cases(gpu, oracle):
+    """test_kernels.cpp:184-206: 50 random m, n, k <= 64 (seed 1234), bitwise."""
+    rng = oracle.MT64(seed=1234)
+    for _ in range(50):
+        m, n, k = 1 + rng() % 64, 1 + rng() % 64, 1 + rng() % 64
+        a = rng.fill_uniform(m * k).reshape(m, k)
+        b = rng.fill_uniform(k * n).reshape(k, n)
+        c = rng.fill_uniform(m * n).reshape(m, n)
+        alpha = 0.5 + float(rng() % 8)
+        beta = float(rng() % 3)
+        assert np.array_equal(naive(gpu, alpha, beta, a, b, c), oracle.gemm(alpha, beta, a, b, c))
+
+
+@pytest.mark.parametrize("tile", [64, 128])
+def test_tiled_every_size_1_to_64_and_large(gpu, oracle, tile):
+    """test_kernels.cpp:208-230 sizes 1..64 plus acceptance's {65, 100, 127, 128, 256}."""
+    rng = oracle.MT64(seed=5678)
+    worst = 0.0
+    for s in list(range(1, 65)) + [65, 100, 127, 128, 129, 256]:
+        a, b, c = (rng.fill_uniform(s * s).reshape(s, s) for _ in range(3))
+        got = tiled(gpu, 1.25, 0.75, a, b, c, tile)
+        ok, w = within_tol(got, oracle.gemm(1.25, 0.75, a, b, c), s)
+        worst = max(worst, w)
+        assert ok, (s, w)
+    assert worst < 1.0
+
+
+def test_ragged_and_rectangular(gpu, oracle, golden):
+    rng = oracle.MT64(seed=4321)
+    cases = golden["gemm_ragged_rng4321"]
+    shapes = [(16, 16, 16, 2.0, 1.0), (10, 10, 10, 1.0, 0.5)]
+    for (m, n, k, al, be), cs in zip(shapes, cases[:2]):
+        a, b, c = (rng.fill_uniform(m * m).reshape(m, m) for _ in range(3))
+        assert h(oracle.fnv1a64(naive(gpu, al, be, a, b, c))) == cs["c_out_digest"]
+        assert within_tol(tiled(gpu, al, be, a, b, c), oracle.gemm(al, be, a, b, c), k)[0]
+    m, n, k = 13, 29, 7
+    a = rng.fill_uniform(m * k).reshape(m, k)
+    b = rng.fill_uniform(k * n).reshape(k, n)
+    c = rng.fill_uniform(m * n).reshape(m, n)
+    assert h(oracle.fnv1a64(naive(gpu, 2.5, 0.0, a, b, c))) == cases[2]["c_out_digest"]
+    assert within_tol(tiled(gpu, 2.5, 0.0, a, b, c), oracle.gemm(2.5, 0.0, a, b, c), k)[0]
+    # odd leading dimensions (8-byte cp.async path) and rectangular extents
+    for (m, n, k) in ((1, 1, 1), (3, 5, 7), (130, 257, 33), (257, 130, 1), (64, 200, 513)):
+        a = rng.fill_uniform(m * k).reshape(m, k)
+        b = rng.fill_uniform(k * n).reshape(k, n)
+        c = rng.fill_uniform(m * n).reshape(m, n)
+        for tile in (64, 128):
+            for align in (8, 64):  # rowAlignment 8 -> odd leading dimensions (8-byte cp.async path)
+                got = tiled(gpu, 1.5, 0.5, a, b, c, tile, align)
+                assert within_tol(got, oracle.gemm(1.5, 0.5, a, b, c), k)[0], (m, n, k, tile, align)
+
+
+def test_never_writes_outside_logical_extents(gpu, oracle):
+    """test_kernels.cpp:281-306: C in a larger buffer, 0xEE canary everywhere else."""
+    rng = oracle.MT64(seed=86)
+    m, n, k = 9, 11, 5
+    a = rng.fill_uniform(m * k).reshape(m, k)
+    b = rng.fill_uniform(k * n).reshape(k, n)
+    for kern, wdf in ((kw.GemmTiledKernel(), lambda: kw.gemmTiledWorkDiv(GPU, m, n, 64)),
+                      (kw.GemmNaiveKernel(), lambda: kw.gemmNaiveWorkDiv(GPU, m, n, 2, 2))):
+        A, B = mat(gpu, a), mat(gpu, b)
+        Cb = kw.Buffer(gpu, kw.IndexVec(m + 3, n + 5), 8)
+        Cb.fill_raw(0xEE)
+        ones = np.ones((m, n))
+        q = kw._default_queue(gpu)
+        assert L.lib().kw_copy(q.handle(), Cb.data(), Cb.rowPitch(), L.sz3((m + 3, n + 5)), ones.ctypes.data, n * 8,
+                               L.sz3((m, n)), 2, L.sz3((m, n)), 8) == 0
+        q.wait()
+        kw.executeTask(GPU, wdf(), kern, kw.GemmArgs(m, n, k, 1.0, 0.0, A, B, Cb))
+        raw = np.frombuffer(Cb.download_raw(), dtype=np.uint8).reshape(m + 3, Cb.rowPitch())
+        assert (raw[:m, n * 8:] == 0xEE).all() and (raw[m:] == 0xEE).all()
+
+
+def test_beta_zero_still_reads_c(gpu):
+    """gemm.cpp:35 / 115: beta multiplies C even when 0, so NaN in C propagates."""
+    c = np.full((4, 4), np.nan)
+    for run in (tiled, naive):
+        out = run(gpu, 1.0, 0.0, np.eye(4), np.eye(4), c)
+        assert np.isnan(out).all()
+
+
+def test_row_panels_and_column_panels_are_bitwise_invariant(gpu, oracle):
+    """The property the row-sharded multi-GPU DGEMM relies on: computing C in row blocks or
+    column panels (different A/B/C base pointers and leading dimensions) gives the same bits
+    as one launch."""
+    rng = np.random.default_rng(3)
+    m, n, k = 384, 512, 300
+    a, b, c = rng.random((m, k)) * 10, rng.random((k, n)) * 10, rng.random((m, n)) * 10
+    full = tiled(gpu, 1.7, 0.3, a, b, c)
+    parts = np.vstack([tiled(gpu, 1.7, 0.3, a[r:r + 128], b, c[r:r + 128]) for r in range(0, m, 128)])
+    assert np.array_equal(full, parts)
+    cols = np.hstack([tiled(gpu, 1.7, 0.3, a, np.ascontiguousarray(b[:, j:j + 128]), c[:, j:j + 128])
+                      for j in range(0, n, 128)])
+    assert np.array_equal(full, cols)
+
+
+def test_rowsharded_single_rank_pipeline(gpu, oracle):
+    """kw_dgemm_rowsharded with world = 1 (NCCL single-rank communicator) exercises the
+    panel-broadcast pipeline on one GPU and must equal kw_dgemm bit for bit."""
+    rng = np.random.default_rng(5)
+    m, n, k = 256, 1000, 200
+    a, b, c = rng.random((m, k)) * 10, rng.random((k, n)) * 10, rng.random((m, n)) * 10
+    want = tiled(gpu, 1.1, 0.9, a, b, c)
+    uid = (C.c_char * 128)()
+    assert L.lib().kw_comm_unique_id(uid) == 0
+    comm = C.c_void_p()
+    assert L.lib().kw_comm_init(C.byref(comm), 0, 1, 0, uid) == 0, L.last_error()
+    A, B, Cb = mat(gpu, a), mat(gpu, b), mat(gpu, c)
+    panels = kw.Buffer(gpu, kw.IndexVec(k * n), 8)
+    q = kw.Queue(gpu, kw.QueueFlavor.Async)
+    st = L.lib().kw_dgemm_rowsharded(comm, q.handle(), m, n, k, 1.1, A.data(), A.leadingDim(), B.data(),
+                                     B.leadingDim(), 0.9, Cb.data(), Cb.leadingDim(), panels.data(), 3, 0)
+    assert st == 0, L.last_error()
+    q.wait()
+    assert np.array_equal(Cb.download(), want)
+    assert L.lib().kw_comm_destroy(comm) == 0
+
+
+def test_host_buffers_are_staged(gpu, oracle):
+    """DGEMM on host (pinned) buffers: B staged once, A/C row panels pipelined; equal bits to
+    the device-resident launch."""
+    rng = np.random.default_rng(9)
+    m, n, k = 1500, 700, 333
+    a, b, c = rng.random((m, k)) * 10, rng.random((k, n)) * 10, rng.random((m, n)) * 10
+    want = tiled(gpu, 0.7, 1.3, a, b, c)
+    host = kw.Device.host()
+    A, B, Cb = (kw.Buffer(host, kw.IndexVec(*x.shape), 8) for x in (a, b, c))
+    for buf, x in ((A, a), (B, b), (Cb, c)):
+        buf.host_view()[:, : x.shape[1]] = x
+    q = kw.Queue(gpu, kw.QueueFlavor.Async)
+    q.enqueue(kw.createExec(GPU, kw.gemmTiledWorkDiv(GPU, m, n, 128), kw.GemmTiledKernel(),
+                            kw.GemmArgs(m, n, k, 0.7, 1.3, A, B, Cb)))
+    q.wait()
+    assert np.array_equal(Cb.host_view()[:, :n], want)
+
+
+def test_4096_within_tolerance(gpu, oracle):
+    """The configured 1-GPU point: Workload("gemm-tiled", 4096, 42)."""
+    n = 4096
+    alpha, beta, a, b, c = oracle.workload_gemm(n, 42)
+    got = tiled(gpu, alpha, beta, a, b, c)
+    ref = oracle.gemm(alpha, beta, a, b, c)
+    ok, worst = within_tol(got, ref, n)
+    assert ok, worst
