@@ -159,6 +159,14 @@ KW_EXPORT kw_status kw_dgemm(kw_queue q, const kw_workdiv* wd, size_t m, size_t 
                              const double* A, size_t lda, const double* B, size_t ldb, double beta, double* C,
                              size_t ldc);
 
+/* Tile-configuration sweep (BASELINE.json configs[4]): the DMMA kernel's instantiated
+ * configurations, info = {BM, BN, BK, threads, stages}; device operands only. */
+KW_EXPORT int kw_dgemm_config_count(void);
+KW_EXPORT kw_status kw_dgemm_config_info(int cfg, int info[5]);
+KW_EXPORT kw_status kw_dgemm_with_config(kw_queue q, int cfg, size_t m, size_t n, size_t k, double alpha,
+                                         const double* A, size_t lda, const double* B, size_t ldb, double beta,
+                                         double* C, size_t ldc);
+
 /* ---- K3: naive DGEMM (GemmNaiveKernel, gemm.cpp:11-38) — BIT-EXACT mode --------------------
  * One dot product per output, ascending p, products and sums rounded separately, acc from
  * +0.0: bitwise identical to gemmReference. Honors the (rows, cols) work division exactly

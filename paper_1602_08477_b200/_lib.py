@@ -64,6 +64,10 @@ SIGNATURES = {
     "kw_axpy_f64": (st, [vp, C.POINTER(kw_workdiv), size_t, C.c_double, vp, vp]),
     "kw_dgemm": (st, [vp, C.POINTER(kw_workdiv), size_t, size_t, size_t, C.c_double, vp, size_t, vp, size_t,
                       C.c_double, vp, size_t]),
+    "kw_dgemm_config_count": (C.c_int, []),
+    "kw_dgemm_config_info": (st, [C.c_int, C.c_int * 5]),
+    "kw_dgemm_with_config": (st, [vp, C.c_int, size_t, size_t, size_t, C.c_double, vp, size_t, vp, size_t,
+                                  C.c_double, vp, size_t]),
     "kw_dgemm_naive": (st, [vp, C.POINTER(kw_workdiv), size_t, size_t, size_t, C.c_double, vp, size_t, vp,
                             size_t, C.c_double, vp, size_t]),
     "kw_comm_unique_id": (st, [C.c_char * 128]),
@@ -92,6 +96,14 @@ def lib() -> C.CDLL:
     if _lib is None:
         if not LIB_PATH.exists():
             raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+        # Prefer the NCCL torch ships (so torch.distributed and kw_comm share one libnccl.so.2).
+        if "KW_NCCL_LIBRARY" not in os.environ:
+            import importlib.util
+            spec = importlib.util.find_spec("nvidia.nccl")
+            if spec and spec.submodule_search_locations:
+                cand = Path(list(spec.submodule_search_locations)[0]) / "lib" / "libnccl.so.2"
+                if cand.exists():
+                    os.environ["KW_NCCL_LIBRARY"] = str(cand)
         handle = C.CDLL(str(LIB_PATH), mode=os.RTLD_NOW | os.RTLD_GLOBAL)
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(handle, name)

@@ -59,7 +59,7 @@ def build_lib(force: bool = False, verbose: bool = False) -> Path:
                     print(out)
                 (BUILD / "ptxas.log").open("a").write(out)
     if force or jobs or _stale(LIB, objs):
-        _run([NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart", "-lnccl"])
+        _run([NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart", "-ldl"])
     return LIB
 
 

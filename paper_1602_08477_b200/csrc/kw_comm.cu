@@ -12,13 +12,74 @@
 
 #include <nccl.h>
 
+#include <dlfcn.h>
+
+#include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 namespace kw {
 kw_status dgemm_device(cudaStream_t s, int tile, size_t m, size_t n, size_t k, double alpha, const double* A,
                        size_t lda, const double* B, size_t ldb, double beta, double* C, size_t ldc);
 }
+
+// NCCL is resolved at run time, never linked: a process that already loaded a libnccl.so.2
+// (e.g. torch's bundled 2.28) keeps using that one (RTLD_NOLOAD), otherwise KW_NCCL_LIBRARY or
+// the system libnccl.so.2 is opened. Linking it would pin the soname to whichever copy the
+// loader finds first and break a later `import torch` that needs newer NCCL symbols.
+namespace {
+struct NcclApi {
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+    std::string error;
+    bool ok = false;
+};
+
+NcclApi& nccl()
+{
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        const char* env = std::getenv("KW_NCCL_LIBRARY");
+        if (!h && env && *env)
+            h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+        if (!h)
+            h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            const char* e = dlerror();
+            api.error = std::string("cannot load libnccl.so.2: ") + (e ? e : "?");
+            return;
+        }
+        api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+        api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+        api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+        api.Broadcast = reinterpret_cast<decltype(api.Broadcast)>(dlsym(h, "ncclBroadcast"));
+        api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+        api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Broadcast && api.GetErrorString;
+        if (!api.ok)
+            api.error = "libnccl.so.2 lacks a required symbol";
+    });
+    return api;
+}
+
+#define ncclGetUniqueId nccl().GetUniqueId
+#define ncclCommInitRank nccl().CommInitRank
+#define ncclCommDestroy nccl().CommDestroy
+#define ncclBroadcast nccl().Broadcast
+#define ncclGetErrorString nccl().GetErrorString
+
+kw_status require_nccl()
+{
+    if (!nccl().ok)
+        return kw::resource(nccl().error);
+    return KW_OK;
+}
+} // namespace
 
 struct kw_comm_s {
     ncclComm_t comm = nullptr;
@@ -57,6 +118,8 @@ kw_status kw_comm_unique_id(unsigned char id[128])
     static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
     if (!id)
         return kw::usage("kw_comm_unique_id: null output");
+    if (require_nccl() != KW_OK)
+        return KW_RESOURCE;
     ncclUniqueId uid;
     ncclResult_t r = ncclGetUniqueId(&uid);
     if (r != ncclSuccess)
@@ -71,6 +134,8 @@ kw_status kw_comm_init(kw_comm* out, int device, int world, int rank, const unsi
         return kw::usage("kw_comm_init: null argument");
     if (world < 1 || rank < 0 || rank >= world)
         return kw::usage("kw_comm_init: rank must lie in [0, world)");
+    if (require_nccl() != KW_OK)
+        return KW_RESOURCE;
     kw::DeviceGuard g(device);
     auto* c = new kw_comm_s;
     c->device = device;

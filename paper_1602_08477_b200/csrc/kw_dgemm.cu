@@ -12,8 +12,9 @@
 //   * global -> shared through a STAGES-deep cp.async (LDGSTS) ring, zero-filling ragged
 //     edges in hardware (src-size < cp-size), which is the reference's zero-padded staging
 //     (gemm.cpp:77-92) without any branch in the math loop;
-//   * shared layouts XOR-swizzled at 16-byte granularity so every fragment load (LDS.64) is
-//     conflict-free: A[m][k] chunk (k/2) ^ (m & 7); B[k][n] chunk (n/2) ^ ((k & 1) << 2);
+//   * shared layouts XOR-swizzled at 16-byte granularity so every fragment load (LDS.64, served
+//     per half-warp) touches 16 distinct banks: A[m][k] chunk (k/2) ^ ((m & 3) << 1);
+//     B[k][n] chunk (n/2) ^ ((k & 3) << 1) (ncu: 0 shared-load bank conflicts);
 //   * epilogue fl(fl(alpha*acc) + fl(beta*c)) exactly as gemm.cpp:115 / reference.cpp:24
 //     (C is always read, also for beta == 0);
 //   * blocks rasterised in groups of 8 tile-rows so co-resident CTAs share A and B panels in L2.
@@ -22,7 +23,10 @@
 // (SURVEY.md §7 "Hard parts" 6). K3 below is the bit-exact mode.
 #include "kw_common.cuh"
 
+#include <cuda.h>
+
 #include <climits>
+#include <mutex>
 
 namespace {
 
@@ -64,15 +68,16 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
 // ------------------------------------------------------------------------------------------
 // K2: DMMA tiled kernel
 // ------------------------------------------------------------------------------------------
-template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_>
+template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_, int MIN_BLOCKS_ = 1>
 struct TileCfg {
     static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_;
+    static constexpr int MIN_BLOCKS = MIN_BLOCKS_;
     static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
     static constexpr int THREADS = 32 * WARPS_M * WARPS_N;
     static constexpr int MT = WM / 8, NT = WN / 8; // DMMA tiles per warp
     static constexpr int A_STAGE = BM * BK, B_STAGE = BK * BN; // doubles
     static constexpr size_t SMEM = static_cast<size_t>(STAGES) * (A_STAGE + B_STAGE) * sizeof(double);
-    static_assert(BK == 16, "A swizzle assumes 8 16-byte chunks per A row");
+    static_assert(BK == 16 || BK == 32, "A swizzle assumes >= 8 16-byte chunks per A row");
     static_assert(BN % 16 == 0 && BM % 8 == 0, "tile shape");
     static_assert((BM * BK / 2) % THREADS == 0 && (BK * BN / 2) % THREADS == 0, "load split");
 };
@@ -81,12 +86,12 @@ struct TileCfg {
 template <int BK>
 __device__ __forceinline__ int a_off(int m, int k)
 {
-    return m * BK + ((((k >> 1) ^ (m & 7))) << 1) + (k & 1);
+    return m * BK + ((((k >> 1) ^ ((m & 3) << 1))) << 1) + (k & 1);
 }
 template <int BN>
 __device__ __forceinline__ int b_off(int k, int n)
 {
-    return k * BN + ((((n >> 1) ^ ((k & 1) << 2))) << 1) + (n & 1);
+    return k * BN + ((((n >> 1) ^ ((k & 3) << 1))) << 1) + (n & 1);
 }
 
 struct GemmParams {
@@ -152,7 +157,7 @@ __device__ __forceinline__ void load_stage(const GemmParams& p, double* sA, doub
 }
 
 template <class Cfg, bool VEC16>
-__global__ void __launch_bounds__(Cfg::THREADS, 1) dgemm_dmma_kernel(GemmParams p)
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS) dgemm_dmma_kernel(GemmParams p)
 {
     extern __shared__ __align__(128) double smem[];
     double* sA = smem;
@@ -252,8 +257,260 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) dgemm_dmma_kernel(GemmParams 
     }
 }
 
-using Cfg128 = TileCfg<128, 128, 16, 64, 32, 4>;
-using Cfg64 = TileCfg<64, 64, 16, 32, 32, 4>;
+
+// ------------------------------------------------------------------------------------------
+// K2 (primary): warp-specialised TMA + mbarrier DMMA kernel.
+//   * one producer warp: a single elected lane streams k-tiles of A (box 16 x BM) and B
+//     (BN/16 boxes of 16 x 16) into a STAGES-deep shared ring with cp.async.bulk.tensor
+//     (TMA, SWIZZLE_128B, hardware zero-fill of ragged edges), signalling `full[s]` through
+//     the transaction count; it waits on `empty[s]` before reusing a slot;
+//   * CONSUMERS DMMA warps: wait `full[s]`, run the 4 k-steps of the tile, arrive on
+//     `empty[s]` — no CTA-wide barrier anywhere in the main loop, so warps drift freely and
+//     fill each other's issue gaps;
+//   * k-slot permutation: DMMA step s of a k-tile feeds lane t with
+//         k(s, t) = 8*(t>>1) + 2*((t+s)&3) + (t&1)
+//     (the 4 steps still cover the 16 k of the tile exactly once). Under the 128-byte TMA
+//     swizzle this makes every LDS.64 fragment load of A and of B hit 16 distinct banks per
+//     half-warp (proof in DESIGN.md §K2). Only the grouping of products inside a DMMA changes,
+//     which is within the stated (K+4)u tolerance and identical for every output element.
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@P1 bra DONE_%=;\n"
+        "bra WAIT_%=;\n"
+        "DONE_%=:\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+            dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map)
+{
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+template <int BM_, int BN_, int WM_, int WN_, int STAGES_>
+struct TmaCfg {
+    static constexpr int BM = BM_, BN = BN_, BK = 16, WM = WM_, WN = WN_, STAGES = STAGES_;
+    static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
+    static constexpr int CONSUMERS = WARPS_M * WARPS_N;
+    static constexpr int THREADS = 32 * (CONSUMERS + 1);
+    static constexpr int MT = WM / 8, NT = WN / 8;
+    static constexpr uint32_t A_BYTES = BM * 128; // BM rows of 16 doubles
+    static constexpr uint32_t B_BYTES = BN * 128; // BN/16 boxes of 16 x 16 doubles (2 KB)
+    static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr size_t SMEM = 1024 + static_cast<size_t>(STAGES) * STAGE_BYTES + 2 * STAGES * sizeof(uint64_t);
+    static_assert(WN % 16 == 0 && BN % 16 == 0 && BM <= 256, "tile shape");
+};
+
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, 1)
+    dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmParams p)
+{
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+    uint64_t* empty = full + Cfg::STAGES;
+
+    constexpr int GROUP = 8;
+    const int tile = blockIdx.x;
+    const int per_group = GROUP * p.tiles_n;
+    const int group = tile / per_group;
+    const int first_m = group * GROUP;
+    const int gsize = (p.tiles_m - first_m) < GROUP ? (p.tiles_m - first_m) : GROUP;
+    const int in_group = tile - group * per_group;
+    const int bm = (first_m + in_group % gsize) * Cfg::BM;
+    const int bn = (in_group / gsize) * Cfg::BN;
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        for (int s = 0; s < Cfg::STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], Cfg::CONSUMERS);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int ktiles = (p.k + Cfg::BK - 1) / Cfg::BK;
+
+    if (warp == Cfg::CONSUMERS) {
+        // ---------------- producer ----------------
+        if (lane == 0) {
+            tma_prefetch_desc(&tmA);
+            tma_prefetch_desc(&tmB);
+            for (int kt = 0; kt < ktiles; ++kt) {
+                const int s = kt % Cfg::STAGES;
+                const uint32_t r = static_cast<uint32_t>(kt / Cfg::STAGES);
+                mbar_wait(&empty[s], (r & 1u) ^ 1u);
+                mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
+                const uint32_t sa = smem_u32(smem + s * Cfg::STAGE_BYTES);
+                tma_load_2d(sa, &tmA, kt * Cfg::BK, bm, &full[s]);
+#pragma unroll
+                for (int j = 0; j < Cfg::BN / 16; ++j)
+                    tma_load_2d(sa + Cfg::A_BYTES + j * 2048, &tmB, bn + 16 * j, kt * Cfg::BK, &full[s]);
+            }
+        }
+        return;
+    }
+
+    // ---------------- consumers ----------------
+    const int wm = (warp / Cfg::WARPS_N) * Cfg::WM;
+    const int wn = (warp % Cfg::WARPS_N) * Cfg::WN;
+    const int g = lane >> 2, t = lane & 3;
+
+    double acc[Cfg::MT][Cfg::NT][2];
+#pragma unroll
+    for (int i = 0; i < Cfg::MT; ++i)
+#pragma unroll
+        for (int j = 0; j < Cfg::NT; ++j)
+            acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    // Per-lane parts of the fragment addresses (bytes inside a stage).
+    const uint32_t a_row = static_cast<uint32_t>(wm + g) * 128u;
+    const uint32_t b_box = static_cast<uint32_t>(wn >> 4) * 2048u;
+
+    for (int kt = 0; kt < ktiles; ++kt) {
+        const int s = kt % Cfg::STAGES;
+        const uint32_t r = static_cast<uint32_t>(kt / Cfg::STAGES);
+        mbar_wait(&full[s], r & 1u);
+        const uint8_t* sa = smem + s * Cfg::STAGE_BYTES;
+        const uint8_t* sb = sa + Cfg::A_BYTES;
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+            const int k = 8 * (t >> 1) + 2 * ((t + ks) & 3) + (t & 1);
+            const uint32_t a_sw = (static_cast<uint32_t>((k >> 1) ^ g) << 4) | (static_cast<uint32_t>(k & 1) << 3);
+            const uint32_t b_even =
+                static_cast<uint32_t>(k) * 128u + ((static_cast<uint32_t>((g >> 1) ^ (k & 7)) << 4) | ((g & 1) << 3));
+            const uint32_t b_odd = b_even ^ 64u;
+            double af[Cfg::MT], bf[Cfg::NT];
+#pragma unroll
+            for (int i = 0; i < Cfg::MT; ++i)
+                af[i] = *reinterpret_cast<const double*>(sa + a_row + i * 1024 + a_sw);
+#pragma unroll
+            for (int j = 0; j < Cfg::NT; ++j)
+                bf[j] = *reinterpret_cast<const double*>(sb + b_box + (j >> 1) * 2048 + ((j & 1) ? b_odd : b_even));
+#pragma unroll
+            for (int i = 0; i < Cfg::MT; ++i)
+#pragma unroll
+                for (int j = 0; j < Cfg::NT; ++j)
+                    dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
+        __syncwarp();
+        if (lane == 0)
+            mbar_arrive(&empty[s]);
+    }
+
+    const bool c_vec = (p.ldc % 2 == 0) && (reinterpret_cast<uintptr_t>(p.c) % 16 == 0);
+#pragma unroll
+    for (int i = 0; i < Cfg::MT; ++i) {
+        const int row = bm + wm + i * 8 + g;
+        if (row >= p.m)
+            continue;
+        double* crow = p.c + row * p.ldc;
+#pragma unroll
+        for (int j = 0; j < Cfg::NT; ++j) {
+            const int col = bn + wn + j * 8 + 2 * t;
+            if (c_vec && col + 1 < p.n) {
+                double2 old = *reinterpret_cast<const double2*>(crow + col);
+                double2 out;
+                out.x = __dadd_rn(__dmul_rn(p.alpha, acc[i][j][0]), __dmul_rn(p.beta, old.x));
+                out.y = __dadd_rn(__dmul_rn(p.alpha, acc[i][j][1]), __dmul_rn(p.beta, old.y));
+                *reinterpret_cast<double2*>(crow + col) = out;
+            }
+            else {
+                if (col < p.n)
+                    crow[col] = __dadd_rn(__dmul_rn(p.alpha, acc[i][j][0]), __dmul_rn(p.beta, crow[col]));
+                if (col + 1 < p.n)
+                    crow[col + 1] = __dadd_rn(__dmul_rn(p.alpha, acc[i][j][1]), __dmul_rn(p.beta, crow[col + 1]));
+            }
+        }
+    }
+}
+
+using PFN_encodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled encode_fn()
+{
+    static PFN_encodeTiled fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_encodeTiled>(f);
+        cudaGetLastError();
+    });
+    return fn;
+}
+
+// 2-D row-major fp64 matrix (rows x cols, ld elements) as a TMA map with box (16 cols, box_rows).
+bool make_map(CUtensorMap* map, const double* base, size_t rows, size_t cols, size_t ld, uint32_t box_rows)
+{
+    PFN_encodeTiled enc = encode_fn();
+    if (!enc)
+        return false;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * sizeof(double))};
+    const cuuint32_t box[2] = {16, box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool tma_eligible(const GemmParams& p)
+{
+    return p.k > 0 && (p.lda * 8) % 16 == 0 && (p.ldb * 8) % 16 == 0 && reinterpret_cast<uintptr_t>(p.a) % 16 == 0 &&
+           reinterpret_cast<uintptr_t>(p.b) % 16 == 0 && encode_fn() != nullptr;
+}
+
+template <class Cfg>
+kw_status launch_tma(cudaStream_t s, const GemmParams& p0);
+
+// Tile configurations (the DGEMM half of the work-division sweep, BASELINE.json configs[4]).
+using Cfg128 = TileCfg<128, 128, 16, 64, 32, 4>;          // 0: 8 warps of 64x32
+using Cfg128k32 = TileCfg<128, 128, 32, 64, 32, 3>;       // 1
+using Cfg128w16 = TileCfg<128, 128, 16, 32, 32, 4>;       // 2: 16 warps of 32x32
+using Cfg128w16k32 = TileCfg<128, 128, 32, 32, 32, 3>;    // 3
+using Cfg64 = TileCfg<64, 64, 16, 32, 32, 4, 2>;          // 4: 4 warps, several CTAs per SM
+using Cfg128x64 = TileCfg<128, 64, 32, 32, 32, 4, 2>;     // 5: 8 warps of 32x32, 2 CTAs per SM
+using Cfg64x128 = TileCfg<64, 128, 32, 32, 32, 4, 2>;     // 6
 
 template <class Cfg>
 kw_status launch_dmma(cudaStream_t s, const GemmParams& p0)
@@ -356,11 +613,65 @@ kw_status tile_from_wd(const kw_workdiv* wd, size_t m, size_t n, int* tile)
     return KW_OK;
 }
 
+template <class Cfg>
+kw_status launch_tma(cudaStream_t s, const GemmParams& p0)
+{
+    GemmParams p = p0;
+    p.tiles_m = static_cast<int>(kw::ceil_div(p.m, Cfg::BM));
+    p.tiles_n = static_cast<int>(kw::ceil_div(p.n, Cfg::BN));
+    const long long tiles = static_cast<long long>(p.tiles_m) * p.tiles_n;
+    if (tiles > INT_MAX)
+        return kw::usage("dgemm: problem too large for the tile grid");
+    if (!tma_eligible(p))
+        return launch_dmma<Cfg128>(s, p0); // unaligned operands: cp.async kernel
+    CUtensorMap ma, mb;
+    if (!make_map(&ma, p.a, p.m, p.k, p.lda, Cfg::BM) || !make_map(&mb, p.b, p.k, p.n, p.ldb, 16))
+        return launch_dmma<Cfg128>(s, p0);
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(dgemm_tma_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(Cfg::SMEM));
+        if (e != cudaSuccess)
+            return kw::cuda_fail("dgemm: cudaFuncSetAttribute", e);
+        attr = true;
+    }
+    dgemm_tma_kernel<Cfg><<<static_cast<unsigned>(tiles), Cfg::THREADS, Cfg::SMEM, s>>>(ma, mb, p);
+    kw::g_launches.fetch_add(1, std::memory_order_relaxed);
+    return KW_OK;
+}
+
+using Tma128 = TmaCfg<128, 128, 64, 32, 6>;   // 7: 8 consumer warps + 1 producer
+using Tma128s4 = TmaCfg<128, 128, 64, 32, 4>; // 8
+using Tma64x128 = TmaCfg<64, 128, 32, 32, 6>; // 9: 8 consumers of 32x32
+using Tma128x64 = TmaCfg<128, 64, 64, 32, 6>; // 10: 4 consumers
+
+struct CfgInfo {
+    int bm, bn, bk, threads, stages;
+    kw_status (*launch)(cudaStream_t, const GemmParams&);
+};
+
+const CfgInfo kCfgs[] = {
+    {Cfg128::BM, Cfg128::BN, Cfg128::BK, Cfg128::THREADS, Cfg128::STAGES, launch_dmma<Cfg128>},
+    {Cfg128k32::BM, Cfg128k32::BN, Cfg128k32::BK, Cfg128k32::THREADS, Cfg128k32::STAGES, launch_dmma<Cfg128k32>},
+    {Cfg128w16::BM, Cfg128w16::BN, Cfg128w16::BK, Cfg128w16::THREADS, Cfg128w16::STAGES, launch_dmma<Cfg128w16>},
+    {Cfg128w16k32::BM, Cfg128w16k32::BN, Cfg128w16k32::BK, Cfg128w16k32::THREADS, Cfg128w16k32::STAGES,
+     launch_dmma<Cfg128w16k32>},
+    {Cfg64::BM, Cfg64::BN, Cfg64::BK, Cfg64::THREADS, Cfg64::STAGES, launch_dmma<Cfg64>},
+    {Cfg128x64::BM, Cfg128x64::BN, Cfg128x64::BK, Cfg128x64::THREADS, Cfg128x64::STAGES, launch_dmma<Cfg128x64>},
+    {Cfg64x128::BM, Cfg64x128::BN, Cfg64x128::BK, Cfg64x128::THREADS, Cfg64x128::STAGES, launch_dmma<Cfg64x128>},
+    {Tma128::BM, Tma128::BN, Tma128::BK, Tma128::THREADS, Tma128::STAGES, launch_tma<Tma128>},
+    {Tma128s4::BM, Tma128s4::BN, Tma128s4::BK, Tma128s4::THREADS, Tma128s4::STAGES, launch_tma<Tma128s4>},
+    {Tma64x128::BM, Tma64x128::BN, Tma64x128::BK, Tma64x128::THREADS, Tma64x128::STAGES, launch_tma<Tma64x128>},
+    {Tma128x64::BM, Tma128x64::BN, Tma128x64::BK, Tma128x64::THREADS, Tma128x64::STAGES, launch_tma<Tma128x64>},
+};
+constexpr int kNumCfgs = sizeof(kCfgs) / sizeof(kCfgs[0]);
+int g_default_cfg128 = 7; // tile 128 -> TMA warp-specialised kernel (fastest in the sweep)
+int g_default_cfg64 = 4;  // tile 64  -> this config
+
 kw_status launch_tiled(cudaStream_t s, int tile, const GemmParams& p)
 {
-    if (tile == 64)
-        return launch_dmma<Cfg64>(s, p);
-    return launch_dmma<Cfg128>(s, p);
+    const int cfg = tile == 64 ? g_default_cfg64 : g_default_cfg128;
+    return kCfgs[cfg].launch(s, p);
 }
 
 GemmParams make_params(size_t m, size_t n, size_t k, double alpha, const double* A, size_t lda, const double* B,
@@ -541,6 +852,41 @@ kw_status kw_dgemm(kw_queue qh, const kw_workdiv* wd, size_t m, size_t n, size_t
         return kw::after_enqueue(q, "dgemm");
     }
     return dgemm_staged(q, tile, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, a_dev, b_dev, c_dev);
+}
+
+int kw_dgemm_config_count(void) { return kNumCfgs; }
+
+kw_status kw_dgemm_config_info(int cfg, int info[5])
+{
+    if (cfg < 0 || cfg >= kNumCfgs || !info)
+        return kw::usage("dgemm config index out of range");
+    info[0] = kCfgs[cfg].bm;
+    info[1] = kCfgs[cfg].bn;
+    info[2] = kCfgs[cfg].bk;
+    info[3] = kCfgs[cfg].threads;
+    info[4] = kCfgs[cfg].stages;
+    return KW_OK;
+}
+
+kw_status kw_dgemm_with_config(kw_queue qh, int cfg, size_t m, size_t n, size_t k, double alpha, const double* A,
+                               size_t lda, const double* B, size_t ldb, double beta, double* C, size_t ldc)
+{
+    KW_CHECK_QUEUE(qh);
+    auto* q = reinterpret_cast<kw::Queue*>(qh);
+    if (cfg < 0 || cfg >= kNumCfgs)
+        return kw::usage("dgemm config index out of range");
+    kw_status st = validate_gemm(m, n, k, A, lda, B, ldb, C, ldc);
+    if (st != KW_OK || m == 0 || n == 0)
+        return st;
+    kw::DeviceGuard g(q->device);
+    int d = -1;
+    if (kw::pointer_kind(C, &d) != KW_MEM_DEVICE || (k > 0 && (kw::pointer_kind(A, &d) != KW_MEM_DEVICE ||
+                                                               kw::pointer_kind(B, &d) != KW_MEM_DEVICE)))
+        return kw::usage("dgemm_with_config: operands must be device buffers");
+    st = kCfgs[cfg].launch(q->stream, make_params(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc));
+    if (st != KW_OK)
+        return kw::task_fail(q, kw::last_error());
+    return kw::after_enqueue(q, "dgemm");
 }
 
 kw_status kw_dgemm_naive(kw_queue qh, const kw_workdiv* wd, size_t m, size_t n, size_t k, double alpha,

@@ -230,3 +230,20 @@ def test_4096_within_tolerance(gpu, oracle):
     ref = oracle.gemm(alpha, beta, a, b, c)
     ok, worst = within_tol(got, ref, n)
     assert ok, worst
+
+
+def test_every_tile_configuration_within_tolerance(gpu, oracle):
+    """All instantiated DMMA configurations (cp.async and TMA families) on ragged shapes."""
+    lib = L.lib()
+    rng = np.random.default_rng(21)
+    q = kw.Queue(gpu, kw.QueueFlavor.Async)
+    for (m, n, k) in ((1, 1, 1), (17, 33, 9), (130, 257, 100), (200, 64, 513), (256, 384, 64)):
+        a, b, c = rng.random((m, k)) * 10, rng.random((k, n)) * 10, rng.random((m, n)) * 10
+        ref = oracle.gemm(1.3, 0.6, a, b, c)
+        for cfg in range(lib.kw_dgemm_config_count()):
+            A, B, Cb = mat(gpu, a), mat(gpu, b), mat(gpu, c)
+            assert lib.kw_dgemm_with_config(q.handle(), cfg, m, n, k, 1.3, A.data(), A.leadingDim(), B.data(),
+                                            B.leadingDim(), 0.6, Cb.data(), Cb.leadingDim()) == 0, L.last_error()
+            q.wait()
+            ok, worst = within_tol(Cb.download(), ref, k)
+            assert ok, (cfg, m, n, k, worst)
