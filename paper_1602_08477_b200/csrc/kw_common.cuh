@@ -25,7 +25,8 @@ struct Queue {
     int device = 0;
     int flavor = KW_QUEUE_SYNC;
     cudaStream_t stream = nullptr; // in-order FIFO of the queue
-    cudaStream_t aux = nullptr;    // second stream for overlapped copies (host-staged paths)
+    cudaStream_t aux = nullptr;    // D2H stream of the host-staged paths
+    cudaStream_t h2d = nullptr;    // H2D stream of the host-staged paths
     std::mutex mu;
     size_t failed = 0;
     std::string first_failure;
@@ -36,7 +37,10 @@ struct Queue {
     static constexpr int kRing = 4;
     cudaEvent_t ev_ready[kRing] = {};  // chunk computed -> D2H may start
     cudaEvent_t ev_free[kRing] = {};   // chunk drained  -> slot reusable
+    cudaEvent_t ev_h2d[kRing] = {};    // chunk uploaded -> compute may start
     cudaEvent_t ev_join = nullptr;
+    cudaEvent_t ev_start = nullptr;
+    cudaEvent_t ev_b = nullptr;
 };
 
 // RAII device selector: the reference's queues are bound to one device; every entry point

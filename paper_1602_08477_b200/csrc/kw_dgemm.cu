@@ -696,20 +696,21 @@ GemmParams make_params(size_t m, size_t n, size_t k, double alpha, const double*
 size_t round2(size_t v) { return (v + 1) & ~static_cast<size_t>(1); }
 
 // Host-resident operands (e2e path): B is staged once, then row panels of A and C stream
-// through a two-slot ring — H2D(A_p, C_p) + DGEMM on the queue stream, D2H(C_p) on the aux
-// stream — so panel p+1's upload overlaps panel p's download and compute. Each C element is
-// produced by the same kernel in the same k order, so panelling changes no bit.
+// through a three-slot ring on three streams — H2D(A_p, C_p) on the copy stream, DGEMM on the
+// queue stream, D2H(C_p) on the aux stream — so panel p+1's upload, panel p's compute and
+// panel p-1's download overlap (PCIe is full duplex). Each C element is produced by the same
+// kernel in the same k order, so panelling changes no bit.
 kw_status dgemm_staged(kw::Queue* q, int tile, size_t m, size_t n, size_t k, double alpha, const double* A,
                        size_t lda, const double* B, size_t ldb, double beta, double* C, size_t ldc, bool a_dev,
                        bool b_dev, bool c_dev)
 {
     const size_t ldbs = round2(n), ldas = round2(k == 0 ? 1 : k), ldcs = round2(n);
     const size_t row_bytes = (ldas + ldcs) * sizeof(double);
-    size_t R = (64u << 20) / row_bytes;
+    size_t R = (48u << 20) / row_bytes;
     R = R < 128 ? 128 : R / 128 * 128;
     if (R > m)
         R = m;
-    const int ring = 2;
+    const int ring = 3;
     const size_t b_bytes = b_dev ? 0 : k * ldbs * sizeof(double);
     const size_t slot_bytes = R * row_bytes;
     kw_status st = kw::ensure_scratch(q, b_bytes + ring * slot_bytes + 256);
@@ -718,10 +719,17 @@ kw_status dgemm_staged(kw::Queue* q, int tile, size_t m, size_t n, size_t k, dou
     char* base = static_cast<char*>(q->scratch);
     const double* Bd = B;
     size_t ldbd = ldb;
-    cudaError_t e = cudaSuccess;
-    if (!b_dev && k > 0) {
+    // Earlier work on the queue (which may produce A/B/C) precedes the uploads.
+    cudaError_t e = cudaEventRecord(q->ev_start, q->stream);
+    if (e == cudaSuccess)
+        e = cudaStreamWaitEvent(q->h2d, q->ev_start, 0);
+    if (e == cudaSuccess && !b_dev && k > 0) {
         double* bs = reinterpret_cast<double*>(base);
-        e = cudaMemcpy2DAsync(bs, ldbs * 8, B, ldb * 8, n * 8, k, cudaMemcpyHostToDevice, q->stream);
+        e = cudaMemcpy2DAsync(bs, ldbs * 8, B, ldb * 8, n * 8, k, cudaMemcpyHostToDevice, q->h2d);
+        if (e == cudaSuccess)
+            e = cudaEventRecord(q->ev_b, q->h2d);
+        if (e == cudaSuccess)
+            e = cudaStreamWaitEvent(q->stream, q->ev_b, 0);
         Bd = bs;
         ldbd = ldbs;
     }
@@ -733,20 +741,28 @@ kw_status dgemm_staged(kw::Queue* q, int tile, size_t m, size_t n, size_t k, dou
         double* as = reinterpret_cast<double*>(slots + s * slot_bytes);
         double* cs = as + R * ldas;
         if (pi >= static_cast<size_t>(ring))
-            e = cudaStreamWaitEvent(q->stream, q->ev_free[s], 0);
+            e = cudaStreamWaitEvent(q->h2d, q->ev_free[s], 0);
         const double* Ad = A + r0 * lda;
         size_t ldad = lda;
         double* Cd = C + r0 * ldc;
         size_t ldcd = ldc;
+        bool uploaded = false;
         if (e == cudaSuccess && !a_dev && k > 0) {
-            e = cudaMemcpy2DAsync(as, ldas * 8, A + r0 * lda, lda * 8, k * 8, rows, cudaMemcpyHostToDevice, q->stream);
+            e = cudaMemcpy2DAsync(as, ldas * 8, A + r0 * lda, lda * 8, k * 8, rows, cudaMemcpyHostToDevice, q->h2d);
             Ad = as;
             ldad = ldas;
+            uploaded = true;
         }
         if (e == cudaSuccess && !c_dev) {
-            e = cudaMemcpy2DAsync(cs, ldcs * 8, C + r0 * ldc, ldc * 8, n * 8, rows, cudaMemcpyHostToDevice, q->stream);
+            e = cudaMemcpy2DAsync(cs, ldcs * 8, C + r0 * ldc, ldc * 8, n * 8, rows, cudaMemcpyHostToDevice, q->h2d);
             Cd = cs;
             ldcd = ldcs;
+            uploaded = true;
+        }
+        if (e == cudaSuccess && uploaded) {
+            e = cudaEventRecord(q->ev_h2d[s], q->h2d);
+            if (e == cudaSuccess)
+                e = cudaStreamWaitEvent(q->stream, q->ev_h2d[s], 0);
         }
         if (e != cudaSuccess)
             break;

@@ -70,6 +70,7 @@ kw_status ensure_scratch(Queue* q, size_t bytes)
     if (q->scratch) {
         cudaStreamSynchronize(q->stream);
         cudaStreamSynchronize(q->aux);
+        cudaStreamSynchronize(q->h2d);
         cudaFree(q->scratch);
         q->scratch = nullptr;
         q->scratch_bytes = 0;
@@ -271,13 +272,21 @@ kw_status kw_queue_create(int device, int flavor, kw_queue* out)
     cudaError_t e = cudaStreamCreateWithFlags(&q->stream, cudaStreamNonBlocking);
     if (e == cudaSuccess)
         e = cudaStreamCreateWithFlags(&q->aux, cudaStreamNonBlocking);
+    if (e == cudaSuccess)
+        e = cudaStreamCreateWithFlags(&q->h2d, cudaStreamNonBlocking);
     for (int i = 0; e == cudaSuccess && i < Queue::kRing; ++i) {
         e = cudaEventCreateWithFlags(&q->ev_ready[i], cudaEventDisableTiming);
         if (e == cudaSuccess)
             e = cudaEventCreateWithFlags(&q->ev_free[i], cudaEventDisableTiming);
+        if (e == cudaSuccess)
+            e = cudaEventCreateWithFlags(&q->ev_h2d[i], cudaEventDisableTiming);
     }
     if (e == cudaSuccess)
         e = cudaEventCreateWithFlags(&q->ev_join, cudaEventDisableTiming);
+    if (e == cudaSuccess)
+        e = cudaEventCreateWithFlags(&q->ev_start, cudaEventDisableTiming);
+    if (e == cudaSuccess)
+        e = cudaEventCreateWithFlags(&q->ev_b, cudaEventDisableTiming);
     if (e != cudaSuccess) {
         cudaGetLastError();
         delete q;
@@ -295,16 +304,21 @@ kw_status kw_queue_destroy(kw_queue qh)
     kw::DeviceGuard g(q->device);
     cudaStreamSynchronize(q->stream);
     cudaStreamSynchronize(q->aux);
+    cudaStreamSynchronize(q->h2d);
     for (int i = 0; i < Queue::kRing; ++i) {
         if (q->ev_ready[i])
             cudaEventDestroy(q->ev_ready[i]);
         if (q->ev_free[i])
             cudaEventDestroy(q->ev_free[i]);
+        if (q->ev_h2d[i])
+            cudaEventDestroy(q->ev_h2d[i]);
     }
-    if (q->ev_join)
-        cudaEventDestroy(q->ev_join);
+    for (cudaEvent_t e : {q->ev_join, q->ev_start, q->ev_b})
+        if (e)
+            cudaEventDestroy(e);
     if (q->scratch)
         cudaFree(q->scratch);
+    cudaStreamDestroy(q->h2d);
     cudaStreamDestroy(q->aux);
     cudaStreamDestroy(q->stream);
     delete q;

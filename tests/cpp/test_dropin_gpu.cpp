@@ -1,0 +1,280 @@
+// GPU checks of the C++ drop-in, written like the reference's test_kernels.cpp (whose cases
+// are cited per test) but executing on BackendKind::GpuCudaRt through libkw_b200.so.
+// The expected values come from in-test sequential loops identical to axpyReference /
+// gemmReference (reference.cpp:8-26); built without FMA contraction (x86-64 baseline).
+#include <kernelweave/kernelweave.hpp>
+
+#include "check.hpp"
+
+#include <cmath>
+#include <cstring>
+#include <random>
+#include <vector>
+
+using namespace kernelweave;
+using namespace kernelweave::kernels;
+
+namespace {
+
+const Device kHost = Device::host();
+const Device kGpu = Device::gpu(0);
+constexpr BackendKind kBk = BackendKind::GpuCudaRt;
+
+template <class T>
+Buffer toGpu(const std::vector<T>& v)
+{
+    Buffer h(kHost, IndexVec(v.size()), sizeof(T));
+    std::memcpy(h.rowData<T>(0), v.data(), v.size() * sizeof(T));
+    Buffer d(kGpu, IndexVec(v.size()), sizeof(T));
+    Queue q(kGpu, QueueFlavor::Sync);
+    copyBuffer(q, d, h, h.extent());
+    return d;
+}
+
+template <class T>
+std::vector<T> toHost(const Buffer& d)
+{
+    Buffer h(kHost, d.extent(), d.elemSize());
+    Queue q(kGpu, QueueFlavor::Sync);
+    copyBuffer(q, h, d, d.extent());
+    return std::vector<T>(h.rowData<T>(0), h.rowData<T>(0) + d.extent()[0]);
+}
+
+Buffer matrix(std::size_t r, std::size_t c, std::mt19937_64& rng, std::vector<double>* dense)
+{
+    Buffer h(kHost, IndexVec(r, c), 8);
+    fillUniform<double>(h, rng, 0.0, 10.0);
+    dense->resize(r * c);
+    for (std::size_t i = 0; i < r; ++i)
+        std::memcpy(dense->data() + i * c, h.rowData<double>(i), c * 8);
+    Buffer d(kGpu, IndexVec(r, c), 8);
+    Queue q(kGpu, QueueFlavor::Sync);
+    copyBuffer(q, d, h, h.extent());
+    return d;
+}
+
+std::vector<double> download(const Buffer& d)
+{
+    Buffer h(kHost, d.extent(), 8);
+    Queue q(kGpu, QueueFlavor::Sync);
+    copyBuffer(q, h, d, d.extent());
+    const std::size_t r = d.extent()[0], c = d.extent()[1];
+    std::vector<double> out(r * c);
+    for (std::size_t i = 0; i < r; ++i)
+        std::memcpy(out.data() + i * c, h.rowData<double>(i), c * 8);
+    return out;
+}
+
+template <class T>
+void axpyRef(std::size_t n, T alpha, const T* x, T* y)
+{
+    for (std::size_t i = 0; i < n; ++i)
+        y[i] = alpha * x[i] + y[i];
+}
+
+void gemmRef(std::size_t m, std::size_t n, std::size_t k, double alpha, double beta, const double* a,
+             const double* b, double* c)
+{
+    for (std::size_t r = 0; r < m; ++r)
+        for (std::size_t col = 0; col < n; ++col) {
+            double acc = 0.0;
+            for (std::size_t p = 0; p < k; ++p)
+                acc += a[r * k + p] * b[p * n + col];
+            c[r * n + col] = alpha * acc + beta * c[r * n + col];
+        }
+}
+
+bool withinTol(const std::vector<double>& got, const std::vector<double>& ref, std::size_t k)
+{
+    for (std::size_t i = 0; i < got.size(); ++i)
+        if (std::fabs(got[i] - ref[i]) > (k + 4) * 0x1.0p-53 * std::fabs(ref[i]))
+            return false;
+    return true;
+}
+
+} // namespace
+
+TEST_CASE("axpy on tiny vectors (test_kernels.cpp:73-86)")
+{
+    Buffer x = toGpu<double>({1, 2, 3});
+    Buffer y = toGpu<double>({10, 20, 30});
+    executeTask(kBk, axpyWorkDiv(kBk, 3, 2, 1), AxpyKernel{}, AxpyArgs{3, 2.0, &x, &y});
+    CHECK((toHost<double>(y) == std::vector<double>{12, 24, 36}));
+    Buffer y2 = toGpu<double>({10, 20, 30});
+    executeTask(kBk, axpyWorkDiv(kBk, 3, 2, 1), AxpyKernel{}, AxpyArgs{3, 0.0, &x, &y2});
+    CHECK((toHost<double>(y2) == std::vector<double>{10, 20, 30}));
+}
+
+TEST_CASE("axpy guards the tail (test_kernels.cpp:88-112)")
+{
+    std::mt19937_64 rng(42);
+    std::vector<double> xs(128), ys(128);
+    for (auto* v : {&xs, &ys})
+        for (auto& e : *v)
+            e = static_cast<double>(rng() >> 11) * 0x1.0p-53 * 10.0;
+    for (std::size_t i = 100; i < 128; ++i)
+        ys[i] = -555.25;
+    std::vector<double> expected = ys;
+    axpyRef<double>(100, 1.5, xs.data(), expected.data());
+    Buffer x = toGpu(xs), y = toGpu(ys);
+    const WorkDiv wd(IndexVec(2), IndexVec(16), IndexVec(4));
+    CHECK(totalExtent(wd, Level::Grid, Unit::Elems) == IndexVec(128));
+    executeTask(kBk, wd, AxpyKernel{}, AxpyArgs{100, 1.5, &x, &y});
+    CHECK(toHost<double>(y) == expected);
+}
+
+TEST_CASE("native axpy loop and GPU kernel produce identical bits (test_kernels.cpp:331-349)")
+{
+    std::mt19937_64 rng(55);
+    const std::size_t n = 4099;
+    Buffer hx(kHost, IndexVec(n), 8), hy(kHost, IndexVec(n), 8);
+    fillUniform<double>(hx, rng, 0.0, 10.0);
+    fillUniform<double>(hy, rng, 0.0, 10.0);
+    std::vector<double> native(hy.rowData<double>(0), hy.rowData<double>(0) + n);
+    axpyRef<double>(n, 3.25, hx.rowData<double>(0), native.data());
+    for (auto [tpb, ept] : {std::pair<int, int>{16, 8}, {256, 16}, {1, 1}, {128, 3}}) {
+        Buffer x(kGpu, IndexVec(n), 8), y(kGpu, IndexVec(n), 8);
+        Queue q(kGpu, QueueFlavor::Async);
+        copyBuffer(q, x, hx, hx.extent());
+        copyBuffer(q, y, hy, hy.extent());
+        q.enqueue(createExec(kBk, axpyWorkDiv(kBk, n, tpb, ept), AxpyKernel{}, AxpyArgs{n, 3.25, &x, &y}));
+        q.wait();
+        CHECK(toHost<double>(y) == native);
+    }
+    // fp32 path, and host (pinned) operands streamed through the GPU
+    Buffer fx(kHost, IndexVec(n), 4), fy(kHost, IndexVec(n), 4);
+    fillUniform<float>(fx, rng, 0.0f, 10.0f);
+    fillUniform<float>(fy, rng, 0.0f, 10.0f);
+    std::vector<float> want(fy.rowData<float>(0), fy.rowData<float>(0) + n);
+    axpyRef<float>(n, 2.75f, fx.rowData<float>(0), want.data());
+    executeTask(kBk, axpyWorkDiv(kBk, n, 256, 16), AxpyKernel{}, AxpyArgsF32{n, 2.75f, &fx, &fy});
+    CHECK(std::memcmp(fy.rowData<float>(0), want.data(), n * 4) == 0);
+}
+
+TEST_CASE("gemm closed forms (test_kernels.cpp:114-170)")
+{
+    std::mt19937_64 rng(7);
+    std::vector<double> bd, cd;
+    Buffer hid(kHost, IndexVec(4, 4), 8);
+    for (std::size_t r = 0; r < 4; ++r)
+        for (std::size_t c = 0; c < 4; ++c)
+            hid.at<double>(IndexVec(r, c)) = r == c ? 1.0 : 0.0;
+    Buffer ident(kGpu, IndexVec(4, 4), 8);
+    Queue q(kGpu, QueueFlavor::Sync);
+    copyBuffer(q, ident, hid, hid.extent());
+    Buffer b = matrix(4, 4, rng, &bd);
+    for (int naive = 0; naive < 2; ++naive) {
+        Buffer c = matrix(4, 4, rng, &cd);
+        const GemmArgs args{4, 4, 4, 1.0, 0.0, &ident, &b, &c, 64};
+        if (naive)
+            executeTask(kBk, gemmNaiveWorkDiv(kBk, 4, 4, 2, 2), GemmNaiveKernel{}, args);
+        else
+            executeTask(kBk, gemmTiledWorkDiv(kBk, 4, 4, 64), GemmTiledKernel{}, args);
+        CHECK(download(c) == bd);
+        Buffer c3 = matrix(4, 4, rng, &cd);
+        const GemmArgs keep{4, 4, 4, 0.0, 1.0, &ident, &b, &c3, 128};
+        executeTask(kBk, gemmTiledWorkDiv(kBk, 4, 4, 128), GemmTiledKernel{}, keep);
+        CHECK(download(c3) == cd);
+    }
+}
+
+TEST_CASE("naive GPU kernel is bitwise equal to the sequential oracle (test_kernels.cpp:184-206)")
+{
+    std::mt19937_64 rng(1234);
+    for (int iter = 0; iter < 50; ++iter) {
+        const std::size_t m = 1 + rng() % 64, n = 1 + rng() % 64, k = 1 + rng() % 64;
+        std::vector<double> ad, bd, cd;
+        Buffer a = matrix(m, k, rng, &ad), b = matrix(k, n, rng, &bd), c = matrix(m, n, rng, &cd);
+        const double alpha = 0.5 + static_cast<double>(rng() % 8), beta = static_cast<double>(rng() % 3);
+        gemmRef(m, n, k, alpha, beta, ad.data(), bd.data(), cd.data());
+        executeTask(kBk, gemmNaiveWorkDiv(kBk, m, n, 4, 4), GemmNaiveKernel{}, GemmArgs{m, n, k, alpha, beta, &a, &b, &c});
+        CHECK(download(c) == cd);
+    }
+}
+
+TEST_CASE("tiled GPU kernel within (K+4)u at every size 1..64 and ragged shapes")
+{
+    std::mt19937_64 rng(5678);
+    for (std::size_t s = 1; s <= 64; ++s) {
+        std::vector<double> ad, bd, cd;
+        Buffer a = matrix(s, s, rng, &ad), b = matrix(s, s, rng, &bd), c = matrix(s, s, rng, &cd);
+        gemmRef(s, s, s, 1.25, 0.75, ad.data(), bd.data(), cd.data());
+        executeTask(kBk, gemmTiledWorkDiv(kBk, s, s, 128), GemmTiledKernel{},
+                    GemmArgs{s, s, s, 1.25, 0.75, &a, &b, &c, 128});
+        CHECK(withinTol(download(c), cd, s));
+    }
+    const std::size_t m = 13, n = 29, k = 7;
+    std::vector<double> ad, bd, cd;
+    Buffer a = matrix(m, k, rng, &ad), b = matrix(k, n, rng, &bd), c = matrix(m, n, rng, &cd);
+    gemmRef(m, n, k, 2.5, 0.0, ad.data(), bd.data(), cd.data());
+    executeTask(kBk, gemmTiledWorkDiv(kBk, m, n, 64), GemmTiledKernel{}, GemmArgs{m, n, k, 2.5, 0.0, &a, &b, &c, 64});
+    CHECK(withinTol(download(c), cd, k));
+}
+
+TEST_CASE("queue semantics: async FIFO, task handles, usage errors before enqueue")
+{
+    const std::size_t n = 1 << 20;
+    Buffer hx(kHost, IndexVec(n), 4), hy(kHost, IndexVec(n), 4);
+    std::mt19937_64 rng(9);
+    fillUniform<float>(hx, rng, 0.0f, 10.0f);
+    fillUniform<float>(hy, rng, 0.0f, 10.0f);
+    std::vector<float> want(hy.rowData<float>(0), hy.rowData<float>(0) + n);
+    for (int rep = 0; rep < 3; ++rep)
+        axpyRef<float>(n, 0.5f, hx.rowData<float>(0), want.data());
+    Buffer x(kGpu, IndexVec(n), 4), y(kGpu, IndexVec(n), 4);
+    Queue q(kGpu, QueueFlavor::Async);
+    copyBuffer(q, x, hx, hx.extent());
+    copyBuffer(q, y, hy, hy.extent());
+    TaskHandle last = q.enqueue(createExec(kBk, axpyWorkDiv(kBk, n, 256, 16), AxpyKernel{}, AxpyArgsF32{n, 0.5f, &x, &y}));
+    for (int rep = 1; rep < 3; ++rep)
+        last = q.enqueue(createExec(kBk, axpyWorkDiv(kBk, n, 256, 16), AxpyKernel{}, AxpyArgsF32{n, 0.5f, &x, &y}));
+    copyBuffer(q, hy, y, y.extent());
+    q.wait();
+    CHECK(last.state() == TaskState::Done);
+    CHECK(std::memcmp(hy.rowData<float>(0), want.data(), n * 4) == 0);
+    CHECK_THROWS_AS(q.enqueue(createExec(kBk, WorkDiv(IndexVec(1), IndexVec(4096), IndexVec(1)), AxpyKernel{},
+                                         AxpyArgsF32{n, 0.5f, &x, &y})),
+                    UsageError);
+    Buffer wrong(kGpu, IndexVec(8), 8);
+    CHECK_THROWS_AS(createExec(kBk, axpyWorkDiv(kBk, n, 256, 16), AxpyKernel{}, AxpyArgsF32{n, 0.5f, &x, &wrong}),
+                    UsageError);
+    q.wait(); // nothing failed
+}
+
+TEST_CASE("pitched copies never touch bytes outside the box (acceptance crit. 7 shape)")
+{
+    Buffer hsrc(kHost, IndexVec(5, 7), 8);
+    for (std::size_t r = 0; r < 5; ++r)
+        for (std::size_t c = 0; c < 7; ++c)
+            hsrc.at<double>(IndexVec(r, c)) = static_cast<double>(r * 7 + c);
+    Buffer dsrc(kGpu, IndexVec(5, 7), 8), ddst(kGpu, IndexVec(6, 9), 8);
+    Buffer hdst(kHost, IndexVec(6, 9), 8);
+    std::memset(hdst.data(), 0xEE, hdst.storageBytes());
+    Queue q(kGpu, QueueFlavor::Sync);
+    copyBuffer(q, ddst, hdst, hdst.extent());
+    copyBuffer(q, dsrc, hsrc, hsrc.extent());
+    copyBuffer(q, ddst, dsrc, IndexVec(4, 5));
+    copyBuffer(q, hdst, ddst, ddst.extent());
+    bool ok = true;
+    for (std::size_t r = 0; r < 6; ++r) {
+        const auto* raw = reinterpret_cast<const unsigned char*>(hdst.data()) + r * hdst.rowPitch();
+        for (std::size_t bi = 0; bi < hdst.rowPitch(); ++bi) {
+            const bool inside = r < 4 && bi < 5 * 8;
+            if (!inside && raw[bi] != 0xEE && bi < 9 * 8)
+                ok = false;
+        }
+        for (std::size_t c = 0; r < 4 && c < 5; ++c)
+            ok = ok && hdst.at<double>(IndexVec(r, c)) == static_cast<double>(r * 7 + c);
+    }
+    CHECK(ok);
+    CHECK_THROWS_AS(createCopy(ddst, dsrc, IndexVec(6, 9)), UsageError);
+}
+
+int main()
+{
+    if (deviceCount() == 0) {
+        std::printf("no CUDA device\n");
+        return 2;
+    }
+    return kwcheck::run();
+}
