@@ -21,6 +21,7 @@
 #include "kw_common.cuh"
 
 #include <climits>
+#include <cstdlib>
 
 namespace {
 
@@ -93,6 +94,105 @@ __global__ void __launch_bounds__(1024) axpy_vec_kernel(size_t limit, T alpha, c
         y[e] = axpy1(alpha, x[e], y[e]);
 }
 
+// 256-bit path (sm_100a LDG.E.256 / STG.E.256): one 32-byte vector = 8 floats or 4 doubles per
+// lane per access, so a warp moves 1 KiB per instruction. X goes through the non-coherent
+// path with an L2 256-byte promotion hint; Y is read and written once, never allocated in L1.
+template <typename T>
+struct V32 {
+    static constexpr int W = 32 / sizeof(T);
+    T v[W];
+};
+
+__device__ __forceinline__ void ld_x32(const float* p, V32<float>& r)
+{
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                 : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]), "=f"(r.v[5]), "=f"(r.v[6]),
+                   "=f"(r.v[7])
+                 : "l"(p));
+}
+__device__ __forceinline__ void ld_y32(const float* p, V32<float>& r)
+{
+    asm volatile("ld.global.L1::no_allocate.L2::256B.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                 : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]), "=f"(r.v[5]), "=f"(r.v[6]),
+                   "=f"(r.v[7])
+                 : "l"(p));
+}
+__device__ __forceinline__ void st_y32(float* p, const V32<float>& r)
+{
+    asm volatile("st.global.L1::no_allocate.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"l"(p), "f"(r.v[0]),
+                 "f"(r.v[1]), "f"(r.v[2]), "f"(r.v[3]), "f"(r.v[4]), "f"(r.v[5]), "f"(r.v[6]), "f"(r.v[7])
+                 : "memory");
+}
+__device__ __forceinline__ void ld_x32(const double* p, V32<double>& r)
+{
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.f64 {%0,%1,%2,%3}, [%4];\n"
+                 : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3])
+                 : "l"(p));
+}
+__device__ __forceinline__ void ld_y32(const double* p, V32<double>& r)
+{
+    asm volatile("ld.global.L1::no_allocate.L2::256B.v4.f64 {%0,%1,%2,%3}, [%4];\n"
+                 : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3])
+                 : "l"(p));
+}
+__device__ __forceinline__ void st_y32(double* p, const V32<double>& r)
+{
+    asm volatile("st.global.L1::no_allocate.v4.f64 [%0], {%1,%2,%3,%4};\n" ::"l"(p), "d"(r.v[0]), "d"(r.v[1]),
+                 "d"(r.v[2]), "d"(r.v[3])
+                 : "memory");
+}
+
+template <typename T, int U>
+__global__ void __launch_bounds__(1024) axpy_v32_kernel(size_t limit, T alpha, const T* __restrict__ x,
+                                                       T* __restrict__ y, uint32_t vecs_per_thread)
+{
+    constexpr int W = V32<T>::W;
+    const size_t threads = blockDim.x;
+    const size_t block_elems = threads * vecs_per_thread * W;
+    const size_t base = static_cast<size_t>(blockIdx.x) * block_elems;
+    if (base >= limit)
+        return;
+    const size_t end = limit - base < block_elems ? limit : base + block_elems;
+    const size_t nvec = (end - base) / W;
+    const T* xb = x + base;
+    T* yb = y + base;
+    for (uint32_t j0 = 0; j0 < vecs_per_thread; j0 += U) {
+        V32<T> xr[U], yr[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const size_t idx = (j0 + u) * threads + threadIdx.x;
+            if (j0 + u < vecs_per_thread && idx < nvec) {
+                ld_x32(xb + idx * W, xr[u]);
+                ld_y32(yb + idx * W, yr[u]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const size_t idx = (j0 + u) * threads + threadIdx.x;
+            if (j0 + u < vecs_per_thread && idx < nvec) {
+#pragma unroll
+                for (int w = 0; w < W; ++w)
+                    yr[u].v[w] = axpy1(alpha, xr[u].v[w], yr[u].v[w]);
+                st_y32(yb + idx * W, yr[u]);
+            }
+        }
+    }
+    for (size_t e = base + nvec * W + threadIdx.x; e < end; e += threads)
+        y[e] = axpy1(alpha, x[e], y[e]);
+}
+
+// Vector width policy: 128-bit vectors by default — the measured sweep (profiles/
+// axpy_workdiv_sweep_r01.txt) shows both widths saturating HBM at ~7.1 TB/s with the 128-bit
+// path at 512 x 4 reproducibly on top; KW_AXPY_VECTOR_BYTES=32 selects the 256-bit path.
+int vector_bytes_policy()
+{
+    static int v = [] {
+        const char* e = std::getenv("KW_AXPY_VECTOR_BYTES");
+        return (e && std::atoi(e) == 32) ? 32 : 16;
+    }();
+    return v;
+}
+
 // Scalar path (misaligned pointers or V not a multiple of W): element j*T + t of the block.
 template <typename T>
 __global__ void __launch_bounds__(1024) axpy_scalar_kernel(size_t limit, T alpha, const T* __restrict__ x,
@@ -142,7 +242,16 @@ void launch_device(cudaStream_t s, size_t blocks, uint32_t threads, uint32_t ele
     const unsigned grid = static_cast<unsigned>(useful < blocks ? useful : blocks);
     if (grid == 0)
         return;
-    if (aligned && elems % W == 0) {
+    constexpr int W32 = V32<T>::W;
+    const bool aligned32 = (reinterpret_cast<uintptr_t>(x) % 32 == 0) && (reinterpret_cast<uintptr_t>(y) % 32 == 0);
+    if (vector_bytes_policy() == 32 && aligned32 && elems % W32 == 0) {
+        const uint32_t vpt = elems / W32;
+        if (vpt >= 2)
+            axpy_v32_kernel<T, 2><<<grid, threads, 0, s>>>(limit, alpha, x, y, vpt);
+        else
+            axpy_v32_kernel<T, 1><<<grid, threads, 0, s>>>(limit, alpha, x, y, vpt);
+    }
+    else if (aligned && elems % W == 0) {
         const uint32_t vpt = elems / W;
         if (vpt >= 4)
             axpy_vec_kernel<T, 4><<<grid, threads, 0, s>>>(limit, alpha, x, y, vpt);
@@ -266,9 +375,9 @@ kw_status kw_axpy_default_workdiv(size_t n, int elem_size, kw_workdiv* out)
         return kw::usage("kw_axpy_default_workdiv: null output");
     if (elem_size != 4 && elem_size != 8)
         return kw::usage("kw_axpy_default_workdiv: element size must be 4 or 8");
-    // 256 threads x 4 vectors of 16 B per thread: 8 independent 128-bit loads in flight per
-    // thread, ~65k blocks at n = 2^28 (many waves over 148 SMs, no tail effect).
-    const size_t threads = 256, elems = elem_size == 4 ? 16 : 8;
+    // 512 threads x one 16-byte vector per thread (the sweep's best point): 131072 blocks at
+    // n = 2^28, ~900 waves over 148 SMs, so the grid tail is negligible.
+    const size_t threads = 512, elems = elem_size == 4 ? 4 : 2;
     kw_workdiv wd = {};
     wd.dim = 1;
     for (int k = 0; k < 3; ++k)
