@@ -326,7 +326,14 @@ struct TmaCfg {
     static constexpr int BM = BM_, BN = BN_, BK = 16, WM = WM_, WN = WN_, STAGES = STAGES_;
     static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
     static constexpr int CONSUMERS = WARPS_M * WARPS_N;
-    static constexpr int THREADS = 32 * (CONSUMERS + 1);
+    // Consumer warps + one producer warpgroup (4 warps: one issues TMA, the others exit).
+    // setmaxnreg moves registers from the producer warpgroup to the consumers.
+    static constexpr int THREADS = 32 * (CONSUMERS + 4);
+    static constexpr int PRODUCER_REGS = 40;
+    static constexpr int CONSUMER_REGS = ((65536 / 32 - 4 * PRODUCER_REGS) / CONSUMERS) / 8 * 8 > 240
+                                             ? 240
+                                             : ((65536 / 32 - 4 * PRODUCER_REGS) / CONSUMERS) / 8 * 8;
+    static_assert(CONSUMERS % 4 == 0, "consumer warps form whole warpgroups (setmaxnreg granularity)");
     static constexpr int MT = WM / 8, NT = WN / 8;
     static constexpr uint32_t A_BYTES = BM * 128; // BM rows of 16 doubles
     static constexpr uint32_t B_BYTES = BN * 128; // BN/16 boxes of 16 x 16 doubles (2 KB)
@@ -366,9 +373,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     __syncthreads();
     const int ktiles = (p.k + Cfg::BK - 1) / Cfg::BK;
 
-    if (warp == Cfg::CONSUMERS) {
-        // ---------------- producer ----------------
-        if (lane == 0) {
+    if (warp >= Cfg::CONSUMERS) {
+        // ---------------- producer warpgroup ----------------
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(Cfg::PRODUCER_REGS));
+        if (warp == Cfg::CONSUMERS && lane == 0) {
             tma_prefetch_desc(&tmA);
             tma_prefetch_desc(&tmB);
             for (int kt = 0; kt < ktiles; ++kt) {
@@ -387,6 +395,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     }
 
     // ---------------- consumers ----------------
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(Cfg::CONSUMER_REGS));
     const int wm = (warp / Cfg::WARPS_N) * Cfg::WM;
     const int wn = (warp % Cfg::WARPS_N) * Cfg::WN;
     const int g = lane >> 2, t = lane & 3;
@@ -401,36 +410,59 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     // Per-lane parts of the fragment addresses (bytes inside a stage).
     const uint32_t a_row = static_cast<uint32_t>(wm + g) * 128u;
     const uint32_t b_box = static_cast<uint32_t>(wn >> 4) * 2048u;
-
-    for (int kt = 0; kt < ktiles; ++kt) {
-        const int s = kt % Cfg::STAGES;
-        const uint32_t r = static_cast<uint32_t>(kt / Cfg::STAGES);
-        mbar_wait(&full[s], r & 1u);
-        const uint8_t* sa = smem + s * Cfg::STAGE_BYTES;
+    uint32_t a_sw[4], b_even[4];
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+        const int k = 8 * (t >> 1) + 2 * ((t + ks) & 3) + (t & 1);
+        a_sw[ks] = a_row + ((static_cast<uint32_t>((k >> 1) ^ g) << 4) | (static_cast<uint32_t>(k & 1) << 3));
+        b_even[ks] = b_box + static_cast<uint32_t>(k) * 128u +
+                     ((static_cast<uint32_t>((g >> 1) ^ (k & 7)) << 4) | ((g & 1) << 3));
+    }
+    auto load_frags = [&](const uint8_t* sa, int ks, double (&af)[Cfg::MT], double (&bf)[Cfg::NT]) {
         const uint8_t* sb = sa + Cfg::A_BYTES;
 #pragma unroll
+        for (int i = 0; i < Cfg::MT; ++i)
+            af[i] = *reinterpret_cast<const double*>(sa + a_sw[ks] + i * 1024);
+#pragma unroll
+        for (int j = 0; j < Cfg::NT; ++j)
+            bf[j] = *reinterpret_cast<const double*>(sb + (j >> 1) * 2048 + (b_even[ks] ^ ((j & 1) ? 64u : 0u)));
+    };
+
+    // Register double buffering: the fragments of the next k-step (or of the next stage's
+    // first k-step) are loaded before the DMMAs of the current one are issued, so LDS latency
+    // hides behind 32 DMMAs instead of stalling the warp.
+    double af[2][Cfg::MT], bf[2][Cfg::NT];
+    if (ktiles > 0) {
+        mbar_wait(&full[0], 0);
+        load_frags(smem, 0, af[0], bf[0]);
+    }
+    for (int kt = 0; kt < ktiles; ++kt) {
+        const int s = kt % Cfg::STAGES;
+        const uint8_t* sa = smem + s * Cfg::STAGE_BYTES;
+#pragma unroll
         for (int ks = 0; ks < 4; ++ks) {
-            const int k = 8 * (t >> 1) + 2 * ((t + ks) & 3) + (t & 1);
-            const uint32_t a_sw = (static_cast<uint32_t>((k >> 1) ^ g) << 4) | (static_cast<uint32_t>(k & 1) << 3);
-            const uint32_t b_even =
-                static_cast<uint32_t>(k) * 128u + ((static_cast<uint32_t>((g >> 1) ^ (k & 7)) << 4) | ((g & 1) << 3));
-            const uint32_t b_odd = b_even ^ 64u;
-            double af[Cfg::MT], bf[Cfg::NT];
-#pragma unroll
-            for (int i = 0; i < Cfg::MT; ++i)
-                af[i] = *reinterpret_cast<const double*>(sa + a_row + i * 1024 + a_sw);
-#pragma unroll
-            for (int j = 0; j < Cfg::NT; ++j)
-                bf[j] = *reinterpret_cast<const double*>(sb + b_box + (j >> 1) * 2048 + ((j & 1) ? b_odd : b_even));
+            const int cur = ks & 1, nxt = cur ^ 1;
+            if (ks < 3) {
+                load_frags(sa, ks + 1, af[nxt], bf[nxt]);
+            }
+            else {
+                // Every fragment of stage s is in registers: release the slot to the producer,
+                // then wait for the next stage (if any) and prefetch its first k-step.
+                __syncwarp();
+                if (lane == 0)
+                    mbar_arrive(&empty[s]);
+                if (kt + 1 < ktiles) {
+                    const int s2 = (kt + 1) % Cfg::STAGES;
+                    mbar_wait(&full[s2], static_cast<uint32_t>((kt + 1) / Cfg::STAGES) & 1u);
+                    load_frags(smem + s2 * Cfg::STAGE_BYTES, 0, af[nxt], bf[nxt]);
+                }
+            }
 #pragma unroll
             for (int i = 0; i < Cfg::MT; ++i)
 #pragma unroll
                 for (int j = 0; j < Cfg::NT; ++j)
-                    dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+                    dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[cur][i], bf[cur][j]);
         }
-        __syncwarp();
-        if (lane == 0)
-            mbar_arrive(&empty[s]);
     }
 
     const bool c_vec = (p.ldc % 2 == 0) && (reinterpret_cast<uintptr_t>(p.c) % 16 == 0);
