@@ -170,14 +170,6 @@ class Dist:
             self.dist.destroy_process_group()
 
 
-def shard(n: int, world: int, rank: int, align: int = 4):
-    """Contiguous index range of `rank`, boundaries multiples of `align` elements (16 B)."""
-    per = -(-n // world)
-    per = -(-per // align) * align
-    lo = min(n, rank * per)
-    return lo, min(n, lo + per)
-
-
 # --------------------------------------------------------------------------------------------
 # product arm
 # --------------------------------------------------------------------------------------------
@@ -191,7 +183,8 @@ def run_ours(args, dist: Dist) -> dict:
     GPU = kw.BackendKind.GpuCudaRt
     q = kw.Queue(dev, kw.QueueFlavor.Async)
 
-    lo, hi = shard(N_AXPY, dist.world, dist.rank)
+    from paper_1602_08477_b200 import sharding as S
+    lo, hi = S.axpy_range(N_AXPY, dist.world, dist.rank)
     n = hi - lo
     rng = np.random.default_rng(1234)
     # synthetic data of the configured shape (same bytes on every rank count: one global draw)
@@ -395,7 +388,8 @@ def run_dgemm(args, dist, kw, L, lib, dev, q, sampler) -> dict:
 
     # N > 1: 16384^3, A/C row blocks per rank, B broadcast from rank 0 in column panels.
     size = 16384
-    r0, r1 = shard(size, dist.world, dist.rank, align=128)
+    from paper_1602_08477_b200 import sharding as S
+    r0, r1 = S.dgemm_rows(size, dist.world, dist.rank)
     ml = r1 - r0
     A = kw.Buffer(dev, kw.IndexVec(max(ml, 1), size), 8)
     Cb = kw.Buffer(dev, kw.IndexVec(max(ml, 1), size), 8)

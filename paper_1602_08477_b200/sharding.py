@@ -1,0 +1,54 @@
+"""Multi-GPU decomposition of the hot path (one process per GPU).
+
+AXPY: contiguous index ranges, boundaries on 16-byte multiples; no collective — every element
+is independent, so the sharded result is bit-identical to one GPU by construction.
+
+DGEMM: rank r owns row block r of A and C (boundaries on the 128-row tile); B lives on the root
+and is broadcast (ncclBroadcast over NVLink) in column panels, panel j packed dense (k x w_j) in
+the panel-major scratch, each panel's broadcast overlapped with the previous panel's DGEMM.
+`dgemm_panels` is the exact layout kw_dgemm_rowsharded uses (kw_comm.cu), so host code and
+tests can reproduce it.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+
+def ceil_div(a: int, b: int) -> int:
+    return -(-a // b)
+
+
+def axpy_range(n: int, world: int, rank: int, align: int = 4) -> tuple[int, int]:
+    """[lo, hi) of `rank`; shard sizes are multiples of `align` elements except the last."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("rank must lie in [0, world)")
+    per = ceil_div(ceil_div(n, world), align) * align
+    lo = min(n, rank * per)
+    return lo, min(n, lo + per)
+
+
+def dgemm_rows(m: int, world: int, rank: int, tile: int = 128) -> tuple[int, int]:
+    """Row block [r0, r1) of A and C owned by `rank` (tile-aligned boundaries)."""
+    return axpy_range(m, world, rank, align=tile)
+
+
+@dataclass(frozen=True)
+class Panel:
+    index: int
+    n0: int          # first column of B / C
+    width: int       # columns in this panel
+    offset: int      # element offset of the dense k x width panel in the panel-major scratch
+
+
+def dgemm_panels(n: int, k: int, panels: int, tile: int = 128) -> list[Panel]:
+    """Column panels of B exactly as kw_dgemm_rowsharded lays them out."""
+    if panels < 1:
+        raise ValueError("panels must be >= 1")
+    w = ceil_div(ceil_div(n, panels), tile) * tile
+    out, off = [], 0
+    for j in range(ceil_div(n, w)):
+        n0 = j * w
+        wj = min(w, n - n0)
+        out.append(Panel(j, n0, wj, off))
+        off += k * wj
+    return out
