@@ -23,19 +23,31 @@ public:
         if (gridBlockIdx.dim() != wd.dim())
             throw UsageError("AccContext: index and work-division dimensionalities differ");
     }
-    KW_HD AccContext(const kw_workdiv& wd, const IndexVec& gridBlockIdx, const IndexVec& blockThreadIdx) noexcept
-        : m_wd(wd), m_block(gridBlockIdx), m_thread(blockThreadIdx)
+    KW_HD AccContext(const kw_workdiv& wd, const IndexVec& gridBlockIdx, const IndexVec& blockThreadIdx,
+                     std::byte* shared = nullptr, std::size_t sharedBytes = 0) noexcept
+        : m_wd(wd), m_block(gridBlockIdx), m_thread(blockThreadIdx), m_shared(shared), m_sharedBytes(sharedBytes)
     {
     }
+    AccContext(const AccContext&) = default;
 
     KW_HD const kw_workdiv& workDiv() const noexcept { return m_wd; }
     KW_HD const IndexVec& gridBlockIdx() const noexcept { return m_block; }
     KW_HD const IndexVec& blockThreadIdx() const noexcept { return m_thread; }
 
+    // Block shared-memory arena (device launches, kernelweave/cuda_exec.cuh): allocation calls
+    // are matched across a block's threads by sequence, exactly like SharedArena
+    // (accel.cpp:24-61) — every thread issues the same sequence and so computes the same offsets.
+    KW_HD std::byte* sharedBase() const noexcept { return m_shared; }
+    KW_HD std::size_t sharedBytes() const noexcept { return m_sharedBytes; }
+    KW_HD std::size_t& sharedCursor() const noexcept { return m_cursor; }
+
 private:
     kw_workdiv m_wd;
     IndexVec m_block;
     IndexVec m_thread;
+    std::byte* m_shared = nullptr;
+    std::size_t m_sharedBytes = 0;
+    mutable std::size_t m_cursor = 0;
 };
 
 namespace detail {
@@ -53,8 +65,8 @@ KW_HD inline IndexVec mulAdd(const IndexVec& a, const std::size_t* b, const Inde
 } // namespace detail
 
 /// accel.cpp:269-279: (Grid, Blocks), (Grid, Threads) = block * threadsPerBlock + thread,
-/// (Block, Threads); any other pair is a usage error.
-inline IndexVec getIdx(const AccContext& acc, Level origin, Unit unit)
+/// (Block, Threads); any other pair is a usage error (device code: a trap).
+KW_HD inline IndexVec getIdx(const AccContext& acc, Level origin, Unit unit)
 {
     if (origin == Level::Grid && unit == Unit::Blocks)
         return acc.gridBlockIdx();
@@ -62,14 +74,41 @@ inline IndexVec getIdx(const AccContext& acc, Level origin, Unit unit)
         return detail::mulAdd(acc.gridBlockIdx(), acc.workDiv().threads, acc.blockThreadIdx());
     if (origin == Level::Block && unit == Unit::Threads)
         return acc.blockThreadIdx();
+#if defined(__CUDA_ARCH__)
+    __trap();
+    return acc.gridBlockIdx();
+#else
     throw UsageError("getIdx: unsupported (origin, unit) pair (" + std::string(name(origin)) + ", " +
                      std::string(name(unit)) + ")");
+#endif
 }
 
-/// accel.cpp:281-284 → totalExtent.
-inline IndexVec getWorkDiv(const AccContext& acc, Level origin, Unit unit)
+/// accel.cpp:281-284 → totalExtent (work_div.cpp:65-94).
+KW_HD inline IndexVec getWorkDiv(const AccContext& acc, Level origin, Unit unit)
 {
-    return totalExtent(WorkDiv::fromC(acc.workDiv()), origin, unit);
+    const kw_workdiv& w = acc.workDiv();
+    std::size_t r[3] = {1, 1, 1};
+    const bool ok = (origin == Level::Grid) || (origin == Level::Block && unit != Unit::Blocks) ||
+                    (origin == Level::Thread && unit == Unit::Elems);
+    if (!ok) {
+#if defined(__CUDA_ARCH__)
+        __trap();
+#else
+        throw UsageError("totalExtent: unsupported (origin, unit) pair (" + std::string(name(origin)) + ", " +
+                         std::string(name(unit)) + ")");
+#endif
+    }
+    for (uint32_t k = 0; k < w.dim; ++k) {
+        std::size_t v = 1;
+        if (origin == Level::Grid)
+            v *= w.blocks[k];
+        if (origin != Level::Thread && unit != Unit::Blocks)
+            v *= w.threads[k];
+        if (unit == Unit::Elems)
+            v *= w.elems[k];
+        r[k] = v;
+    }
+    return detail::make(w.dim, r);
 }
 
 // ---- the paper's template-tag spelling --------------------------------

@@ -1,0 +1,221 @@
+/* kernelweave B200 drop-in — generic device functor launch.
+ *
+ * Runs ANY kernelweave functor `operator()(const AccContext&, Args...)` on the GPU, the role
+ * detail::runGrid plays for the reference's CPU engines (accel.cpp:120-265): one CUDA thread per
+ * (block, thread) pair of the work division, the last (fastest) work-division component on
+ * CUDA x. Inside the functor the reference's kernel-side API works unchanged:
+ *   getIdx / getWorkDiv (both spellings)        -> acc.hpp (host/device)
+ *   allocSharedMem<T>(acc, n)                   -> dynamic shared memory, matched by call
+ *                                                  sequence, zero-initialised (accel.cpp:286-292)
+ *   syncBlockThreads(acc)                       -> __syncthreads (accel.cpp:294-302)
+ *   atomicAdd(acc, cell, v) f64 / i64 / u64     -> native global atomics (accel.cpp:304-321)
+ * Buffers cross into device code as BufferView (pointer, pitch, extent): a host Buffer object
+ * cannot be dereferenced on the GPU.
+ *
+ * Usage (translation unit compiled by nvcc -gencode arch=compute_100a,code=sm_100a):
+ *   struct MyKernel { template <class Acc> __device__ void operator()(const Acc&, Args) const; };
+ *   KW_DEVICE_FUNCTOR(MyKernel)          // at global scope
+ *   executeTask(BackendKind::GpuCudaRt, wd, MyKernel{}, args...);
+ * A functor may declare `static constexpr std::size_t sharedMemBytes = …;` (default 48 KiB).
+ */
+#pragma once
+
+#if !defined(__CUDACC__)
+#error "kernelweave/cuda_exec.cuh must be compiled by nvcc"
+#endif
+
+#include "kernelweave/kernelweave.hpp"
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace kernelweave {
+
+/// Device view of a Buffer (buffer.hpp:29-128 accessors that make sense on the GPU).
+struct BufferView {
+    std::byte* ptr = nullptr;
+    std::size_t pitch = 0;
+    std::size_t elemSize = 0;
+    std::uint32_t dim = 1;
+    std::size_t extent[3] = {1, 1, 1};
+    int device = 0;
+
+    template <class T>
+    __host__ __device__ T* rowData(std::size_t row) const noexcept
+    {
+        return reinterpret_cast<T*>(ptr + row * pitch);
+    }
+    template <class T>
+    __host__ __device__ std::size_t leadingDim() const noexcept
+    {
+        return pitch / sizeof(T);
+    }
+    __host__ __device__ std::size_t rowCount() const noexcept
+    {
+        std::size_t r = 1;
+        for (std::uint32_t k = 0; k + 1 < dim; ++k)
+            r *= extent[k];
+        return r;
+    }
+};
+
+inline BufferView view(const Buffer& b)
+{
+    if (b.device().isHost())
+        throw UsageError("BufferView: device functors take GPU buffers (copy host data first)");
+    BufferView v;
+    v.ptr = const_cast<std::byte*>(b.data());
+    v.pitch = b.rowPitch();
+    v.elemSize = b.elemSize();
+    v.dim = static_cast<std::uint32_t>(b.dim());
+    for (std::size_t k = 0; k < b.dim(); ++k)
+        v.extent[k] = b.extent()[k];
+    v.device = b.device().cudaIndex();
+    return v;
+}
+
+/// Block-shared region of count*elemSize bytes; every thread of the block must issue the same
+/// allocation sequence (acc.hpp:75-84 contract), which makes this a collective: the region is
+/// zeroed cooperatively and published with a block barrier.
+__device__ inline void* allocSharedMem(const AccContext& acc, std::size_t elemCount, std::size_t elemSize)
+{
+    const std::size_t bytes = elemCount * elemSize;
+    const std::size_t off = (acc.sharedCursor() + 15) & ~static_cast<std::size_t>(15);
+    if (bytes == 0 || off + bytes > acc.sharedBytes())
+        __trap(); // UsageError / ResourceError in the reference
+    acc.sharedCursor() = off + bytes;
+    std::byte* p = acc.sharedBase() + off;
+    const unsigned nthreads = blockDim.x * blockDim.y * blockDim.z;
+    const unsigned tid = (threadIdx.z * blockDim.y + threadIdx.y) * blockDim.x + threadIdx.x;
+    for (std::size_t i = tid; i < bytes; i += nthreads)
+        p[i] = std::byte{0};
+    __syncthreads();
+    return p;
+}
+
+template <class T>
+__device__ inline T* allocSharedMem(const AccContext& acc, std::size_t count)
+{
+    return static_cast<T*>(allocSharedMem(acc, count, sizeof(T)));
+}
+
+__device__ inline void syncBlockThreads(const AccContext&) { __syncthreads(); }
+
+__device__ inline double atomicAdd(const AccContext&, double& cell, double operand)
+{
+    return ::atomicAdd(&cell, operand);
+}
+__device__ inline std::int64_t atomicAdd(const AccContext&, std::int64_t& cell, std::int64_t operand)
+{
+    return static_cast<std::int64_t>(::atomicAdd(reinterpret_cast<unsigned long long*>(&cell),
+                                                 static_cast<unsigned long long>(operand)));
+}
+__device__ inline std::uint64_t atomicAdd(const AccContext&, std::uint64_t& cell, std::uint64_t operand)
+{
+    return static_cast<std::uint64_t>(::atomicAdd(reinterpret_cast<unsigned long long*>(&cell),
+                                                 static_cast<unsigned long long>(operand)));
+}
+
+namespace detail {
+
+template <class Kernel, class = void>
+struct SharedBytesOf {
+    static constexpr std::size_t value = 48 * 1024;
+};
+template <class Kernel>
+struct SharedBytesOf<Kernel, std::void_t<decltype(Kernel::sharedMemBytes)>> {
+    static constexpr std::size_t value = Kernel::sharedMemBytes;
+};
+
+template <class Kernel, class... Args>
+__global__ void functorKernel(kw_workdiv wd, std::size_t sharedBytes, Kernel kernel, Args... args)
+{
+    extern __shared__ __align__(16) std::byte kwSharedArena[];
+    const unsigned d = wd.dim;
+    std::size_t b[3] = {0, 0, 0}, t[3] = {0, 0, 0};
+    b[d - 1] = blockIdx.x;
+    t[d - 1] = threadIdx.x;
+    if (d >= 2) {
+        b[d - 2] = blockIdx.y;
+        t[d - 2] = threadIdx.y;
+    }
+    if (d == 3) {
+        b[0] = blockIdx.z;
+        t[0] = threadIdx.z;
+    }
+    const AccContext acc(wd, make(d, b), make(d, t), kwSharedArena, sharedBytes);
+    kernel(acc, args...);
+}
+
+template <class T>
+int viewDevice(const T&)
+{
+    return -1;
+}
+inline int viewDevice(const BufferView& v) { return v.device; }
+
+template <class Kernel, class... Args>
+struct DeviceLauncher {
+    static dim3 toDim3(const std::size_t* v, std::uint32_t d)
+    {
+        return dim3(static_cast<unsigned>(v[d - 1]), d >= 2 ? static_cast<unsigned>(v[d - 2]) : 1u,
+                    d == 3 ? static_cast<unsigned>(v[0]) : 1u);
+    }
+    static void validate(const WorkDiv& wd, const Args&...)
+    {
+        const kw_workdiv w = wd.toC();
+        std::size_t threads = 1;
+        for (std::uint32_t k = 0; k < w.dim; ++k)
+            threads *= w.threads[k];
+        if (threads > 1024)
+            throw UsageError("device functor: threadsPerBlock exceeds the sm_100a block limit of 1024");
+        const std::size_t maxGrid[3] = {65535, 65535, 2147483647};
+        for (std::uint32_t k = 0; k < w.dim; ++k)
+            if (w.blocks[k] > maxGrid[3 - w.dim + k])
+                throw UsageError("device functor: blocksPerGrid exceeds the grid limits");
+        if (w.elems[0] * w.elems[1] * w.elems[2] == 0)
+            throw UsageError("WorkDiv: every level extent is at least 1");
+    }
+    static kw_status launch(kw_queue q, const WorkDiv& wd, const Kernel& kernel, const Args&... args)
+    {
+        void* stream = nullptr;
+        int dev = 0;
+        kw_status st = kw_queue_stream(q, &stream);
+        if (st == KW_OK)
+            st = kw_queue_device(q, &dev);
+        if (st != KW_OK)
+            return st;
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(dev);
+        const kw_workdiv w = wd.toC();
+        constexpr std::size_t smem = SharedBytesOf<Kernel>::value;
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(functorKernel<Kernel, Args...>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem));
+        functorKernel<Kernel, Args...><<<toDim3(w.blocks, w.dim), toDim3(w.threads, w.dim), smem,
+                                         static_cast<cudaStream_t>(stream)>>>(w, smem, kernel, args...);
+        const int err = static_cast<int>(cudaGetLastError());
+        st = kw_queue_complete_launch(q, err, "device functor");
+        cudaSetDevice(prev);
+        return st;
+    }
+    static Device device(const Args&... args)
+    {
+        int d = -1;
+        ((d = d >= 0 ? d : viewDevice(args)), ...);
+        return Device::gpu(d >= 0 ? d : 0);
+    }
+};
+
+} // namespace detail
+} // namespace kernelweave
+
+/// Registers a user functor for GPU execution through createExec / executeTask.
+#define KW_DEVICE_FUNCTOR(K)                                                                                   \
+    namespace kernelweave::detail {                                                                            \
+    template <class... Args>                                                                                   \
+    struct Launcher<K, Args...> : DeviceLauncher<K, Args...> {                                                 \
+    };                                                                                                         \
+    }

@@ -50,7 +50,7 @@ struct Launcher<kernels::AxpyKernel, kernels::AxpyArgsT<T>> {
         if (wd.dim() != 1)
             throw UsageError("axpy: the AXPY kernel runs on a 1-D work division");
     }
-    static kw_status launch(kw_queue q, const WorkDiv& wd, const kernels::AxpyArgsT<T>& a)
+    static kw_status launch(kw_queue q, const WorkDiv& wd, const kernels::AxpyKernel&, const kernels::AxpyArgsT<T>& a)
     {
         const kw_workdiv w = wd.toC();
         if constexpr (std::is_same_v<T, float>)

@@ -76,7 +76,8 @@ struct GemmLauncherBase {
 
 template <>
 struct Launcher<kernels::GemmTiledKernel, kernels::GemmArgs> : GemmLauncherBase {
-    static kw_status launch(kw_queue q, const WorkDiv& wd, const kernels::GemmArgs& a)
+    static kw_status launch(kw_queue q, const WorkDiv& wd, const kernels::GemmTiledKernel&,
+                            const kernels::GemmArgs& a)
     {
         const kw_workdiv w = wd.toC();
         return kw_dgemm(q, &w, a.m, a.n, a.k, a.alpha, a.a->rowData<double>(0), a.a->leadingDim<double>(),
@@ -87,7 +88,8 @@ struct Launcher<kernels::GemmTiledKernel, kernels::GemmArgs> : GemmLauncherBase 
 
 template <>
 struct Launcher<kernels::GemmNaiveKernel, kernels::GemmArgs> : GemmLauncherBase {
-    static kw_status launch(kw_queue q, const WorkDiv& wd, const kernels::GemmArgs& a)
+    static kw_status launch(kw_queue q, const WorkDiv& wd, const kernels::GemmNaiveKernel&,
+                            const kernels::GemmArgs& a)
     {
         const kw_workdiv w = wd.toC();
         return kw_dgemm_naive(q, &w, a.m, a.n, a.k, a.alpha, a.a->rowData<double>(0), a.a->leadingDim<double>(),

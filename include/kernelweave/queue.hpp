@@ -67,12 +67,17 @@ struct CopyTask {
 };
 
 namespace detail {
-/// Maps a kernel functor type onto its sm_100a entry point in libkw_b200.so. Specialised by the
-/// shipped kernels (kernels/axpy.hpp, kernels/gemm.hpp).
+/// Maps a kernel functor type onto its sm_100a launch. Specialised by the shipped kernels
+/// (kernels/axpy.hpp, kernels/gemm.hpp → libkw_b200.so entry points) and, for user functors
+/// compiled by nvcc, by KW_DEVICE_FUNCTOR (kernelweave/cuda_exec.cuh). Contract:
+///   static void validate(const WorkDiv&, const Args&...);          // throws UsageError
+///   static kw_status launch(kw_queue, const WorkDiv&, const Kernel&, const Args&...);
+///   static Device device(const Args&...);                            // for executeTask
 template <class Kernel, class... Args>
 struct Launcher {
     static_assert(sizeof(Kernel) == 0,
-                  "no sm_100a launcher is registered for this kernel functor in the B200 build");
+                  "no sm_100a launcher is registered for this kernel functor: compile the translation unit "
+                  "with nvcc, include kernelweave/cuda_exec.cuh and declare KW_DEVICE_FUNCTOR(YourKernel)");
 };
 } // namespace detail
 
@@ -84,9 +89,10 @@ ExecTask createExec(BackendKind backend, const WorkDiv& wd, Kernel kernel, Args.
     detail::requireGpu(backend);
     detail::Launcher<Kernel, Args...>::validate(wd, args...);
     return ExecTask{backend, wd, [wd, kernel, bound = std::make_tuple(std::move(args)...)](kw_queue q) {
-                        (void)kernel;
                         return std::apply(
-                            [&](const auto&... a) { return detail::Launcher<Kernel, Args...>::launch(q, wd, a...); },
+                            [&](const auto&... a) {
+                                return detail::Launcher<Kernel, Args...>::launch(q, wd, kernel, a...);
+                            },
                             bound);
                     }};
 }

@@ -113,6 +113,12 @@ KW_EXPORT kw_status kw_queue_flavor(kw_queue q, int* flavor);
 KW_EXPORT kw_status kw_queue_stream(kw_queue q, void** cuda_stream);
 KW_EXPORT kw_status kw_queue_shutdown(kw_queue q);
 
+/* Completes a kernel launch made OUTSIDE this library on q's stream (the header-only generic
+ * functor launcher, include/kernelweave/cuda_exec.cuh): `cuda_error` is the launch's
+ * cudaGetLastError() value. Records a failure for kw_queue_wait, counts the launch, and for a
+ * Sync queue completes the task before returning. */
+KW_EXPORT kw_status kw_queue_complete_launch(kw_queue q, int cuda_error, const char* what);
+
 /* TaskHandle (queue.hpp:36-52) as a CUDA event recorded after the last enqueued task. */
 KW_EXPORT kw_status kw_event_record(kw_queue q, kw_event* ev);
 KW_EXPORT kw_status kw_event_state(kw_event ev, int* state);

@@ -51,6 +51,7 @@ SIGNATURES = {
     "kw_queue_flavor": (st, [vp, C.POINTER(C.c_int)]),
     "kw_queue_stream": (st, [vp, C.POINTER(vp)]),
     "kw_queue_shutdown": (st, [vp]),
+    "kw_queue_complete_launch": (st, [vp, C.c_int, C.c_char_p]),
     "kw_event_record": (st, [vp, C.POINTER(vp)]),
     "kw_event_state": (st, [vp, C.POINTER(C.c_int)]),
     "kw_event_destroy": (st, [vp]),

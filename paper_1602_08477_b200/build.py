@@ -67,12 +67,18 @@ def build_cpp_tests(force: bool = False) -> list[Path]:
     """Builds the C++ drop-in programs under tests/cpp against include/ and libkw_b200.so."""
     out = []
     cpp_dir = ROOT / "tests" / "cpp"
-    hdrs = list((INCLUDE / "kernelweave").rglob("*.hpp")) + [INCLUDE / "kw_b200.h"]
+    hdrs = list((INCLUDE / "kernelweave").rglob("*.hpp")) + [INCLUDE / "kw_b200.h", INCLUDE / "kernelweave" / "cuda_exec.cuh"]
     for src in sorted(cpp_dir.glob("*.cpp")):
         exe = BUILD / src.stem
         if force or _stale(exe, [src, LIB] + hdrs):
             _run(["g++", "-O2", "-std=c++20", "-Wall", "-Wextra", f"-I{INCLUDE}", str(src), "-o", str(exe),
                   f"-L{PKG}", "-lkw_b200", f"-Wl,-rpath,{PKG}", "-Wl,-rpath,$ORIGIN/..", "-lpthread"])
+        out.append(exe)
+    for src in sorted(cpp_dir.glob("*.cu")):
+        exe = BUILD / src.stem
+        if force or _stale(exe, [src, LIB] + hdrs + [INCLUDE / "kernelweave" / "cuda_exec.cuh"]):
+            _run([NVCC, *ARCH, "-O2", "-std=c++20", "-lineinfo", f"-I{INCLUDE}", str(src), "-o", str(exe),
+                  f"-L{PKG}", "-lkw_b200", f"-Xlinker=-rpath,{PKG}", "-lcudart"])
         out.append(exe)
     return out
 

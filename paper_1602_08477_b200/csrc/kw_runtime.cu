@@ -381,6 +381,21 @@ kw_status kw_queue_shutdown(kw_queue qh)
     return KW_OK;
 }
 
+kw_status kw_queue_complete_launch(kw_queue qh, int cuda_error, const char* what)
+{
+    if (!qh)
+        return kw::usage("null queue");
+    auto* q = reinterpret_cast<Queue*>(qh);
+    const std::string w = what ? what : "kernel";
+    if (cuda_error != 0) {
+        cudaGetLastError();
+        return kw::task_fail(q, w + ": " + cudaGetErrorString(static_cast<cudaError_t>(cuda_error)));
+    }
+    kw::g_launches.fetch_add(1, std::memory_order_relaxed);
+    kw::DeviceGuard g(q->device);
+    return kw::after_enqueue(q, w.c_str());
+}
+
 // ---- task events --------------------------------------------------------------------------
 
 kw_status kw_event_record(kw_queue qh, kw_event* out)

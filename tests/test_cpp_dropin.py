@@ -29,3 +29,12 @@ def test_dropin_gpu_kernels(programs):
     p = run(programs["test_dropin_gpu"])
     assert p.returncode == 0, p.stdout + p.stderr
     assert "0 failures" in p.stdout
+
+
+@pytest.mark.gpu
+def test_generic_device_functors(programs):
+    """kernelweave/cuda_exec.cuh: user functors (coverage, shared memory, atomics, the README
+    functor) through createExec/executeTask on the GPU."""
+    p = run(programs["test_functor_gpu"])
+    assert p.returncode == 0, p.stdout + p.stderr
+    assert "0 failures" in p.stdout
