@@ -55,12 +55,29 @@ KW_HD inline IndexVec make(std::size_t dim, const std::size_t* v) noexcept
 {
     return dim == 1 ? IndexVec(v[0]) : dim == 2 ? IndexVec(v[0], v[1]) : IndexVec(v[0], v[1], v[2]);
 }
+/// a * b + c component-wise (b a size_t[3] of the work division); array-free for device code.
 KW_HD inline IndexVec mulAdd(const IndexVec& a, const std::size_t* b, const IndexVec& c) noexcept
 {
-    std::size_t r[3] = {0, 0, 0};
-    for (std::size_t k = 0; k < a.dim(); ++k)
-        r[k] = a.get(k) * b[k] + c.get(k);
-    return make(a.dim(), r);
+    const std::size_t d = a.dim();
+    const std::size_t x0 = a.get(0) * b[0] + c.get(0);
+    if (d == 1)
+        return IndexVec(x0);
+    const std::size_t x1 = a.get(1) * b[1] + c.get(1);
+    if (d == 2)
+        return IndexVec(x0, x1);
+    return IndexVec(x0, x1, a.get(2) * b[2] + c.get(2));
+}
+/// One (origin, unit) extent component of a work division (totalExtent, work_div.cpp:65-94).
+KW_HD inline std::size_t extentComponent(const kw_workdiv& w, std::size_t k, Level origin, Unit unit) noexcept
+{
+    std::size_t v = 1;
+    if (origin == Level::Grid)
+        v *= w.blocks[k];
+    if (origin != Level::Thread && unit != Unit::Blocks)
+        v *= w.threads[k];
+    if (unit == Unit::Elems)
+        v *= w.elems[k];
+    return v;
 }
 } // namespace detail
 
@@ -87,7 +104,6 @@ KW_HD inline IndexVec getIdx(const AccContext& acc, Level origin, Unit unit)
 KW_HD inline IndexVec getWorkDiv(const AccContext& acc, Level origin, Unit unit)
 {
     const kw_workdiv& w = acc.workDiv();
-    std::size_t r[3] = {1, 1, 1};
     const bool ok = (origin == Level::Grid) || (origin == Level::Block && unit != Unit::Blocks) ||
                     (origin == Level::Thread && unit == Unit::Elems);
     if (!ok) {
@@ -98,17 +114,13 @@ KW_HD inline IndexVec getWorkDiv(const AccContext& acc, Level origin, Unit unit)
                          std::string(name(unit)) + ")");
 #endif
     }
-    for (uint32_t k = 0; k < w.dim; ++k) {
-        std::size_t v = 1;
-        if (origin == Level::Grid)
-            v *= w.blocks[k];
-        if (origin != Level::Thread && unit != Unit::Blocks)
-            v *= w.threads[k];
-        if (unit == Unit::Elems)
-            v *= w.elems[k];
-        r[k] = v;
-    }
-    return detail::make(w.dim, r);
+    const std::size_t e0 = detail::extentComponent(w, 0, origin, unit);
+    if (w.dim == 1)
+        return IndexVec(e0);
+    const std::size_t e1 = detail::extentComponent(w, 1, origin, unit);
+    if (w.dim == 2)
+        return IndexVec(e0, e1);
+    return IndexVec(e0, e1, detail::extentComponent(w, 2, origin, unit));
 }
 
 // ---- the paper's template-tag spelling --------------------------------
@@ -138,25 +150,24 @@ namespace workdiv {
 template <class Origin, class UnitT>
 KW_HD inline IndexVec getWorkDiv(const AccContext& acc) noexcept
 {
+    constexpr bool valid =
+        std::is_same_v<Origin, Grid> || (std::is_same_v<Origin, Block> && !std::is_same_v<UnitT, Blocks>) ||
+        (std::is_same_v<Origin, Thread> && std::is_same_v<UnitT, Elems>);
+    static_assert(valid, "getWorkDiv: unsupported (origin, unit) pair");
+    constexpr Level o = std::is_same_v<Origin, Grid> ? Level::Grid
+                        : std::is_same_v<Origin, Block> ? Level::Block
+                                                        : Level::Thread;
+    constexpr Unit u = std::is_same_v<UnitT, Blocks> ? Unit::Blocks
+                       : std::is_same_v<UnitT, Threads> ? Unit::Threads
+                                                        : Unit::Elems;
     const kw_workdiv& w = acc.workDiv();
-    std::size_t r[3];
-    for (uint32_t k = 0; k < 3; ++k) {
-        if constexpr (std::is_same_v<Origin, Grid> && std::is_same_v<UnitT, Blocks>)
-            r[k] = w.blocks[k];
-        else if constexpr (std::is_same_v<Origin, Grid> && std::is_same_v<UnitT, Threads>)
-            r[k] = w.blocks[k] * w.threads[k];
-        else if constexpr (std::is_same_v<Origin, Grid> && std::is_same_v<UnitT, Elems>)
-            r[k] = w.blocks[k] * w.threads[k] * w.elems[k];
-        else if constexpr (std::is_same_v<Origin, Block> && std::is_same_v<UnitT, Threads>)
-            r[k] = w.threads[k];
-        else if constexpr (std::is_same_v<Origin, Block> && std::is_same_v<UnitT, Elems>)
-            r[k] = w.threads[k] * w.elems[k];
-        else if constexpr (std::is_same_v<Origin, Thread> && std::is_same_v<UnitT, Elems>)
-            r[k] = w.elems[k];
-        else
-            static_assert(sizeof(Origin) == 0, "getWorkDiv: unsupported (origin, unit) pair");
-    }
-    return detail::make(w.dim, r);
+    const std::size_t e0 = detail::extentComponent(w, 0, o, u);
+    if (w.dim == 1)
+        return IndexVec(e0);
+    const std::size_t e1 = detail::extentComponent(w, 1, o, u);
+    if (w.dim == 2)
+        return IndexVec(e0, e1);
+    return IndexVec(e0, e1, detail::extentComponent(w, 2, o, u));
 }
 } // namespace workdiv
 

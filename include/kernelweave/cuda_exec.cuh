@@ -132,19 +132,17 @@ template <class Kernel, class... Args>
 __global__ void functorKernel(kw_workdiv wd, std::size_t sharedBytes, Kernel kernel, Args... args)
 {
     extern __shared__ __align__(16) std::byte kwSharedArena[];
+    // Last work-division component = CUDA x (index_vec.hpp:15-24 axis rule). Built from
+    // scalars: local index arrays here were once assigned one stack slot by nvcc 12.9 (the block
+    // index read back as the thread index) — keep this path array-free.
     const unsigned d = wd.dim;
-    std::size_t b[3] = {0, 0, 0}, t[3] = {0, 0, 0};
-    b[d - 1] = blockIdx.x;
-    t[d - 1] = threadIdx.x;
-    if (d >= 2) {
-        b[d - 2] = blockIdx.y;
-        t[d - 2] = threadIdx.y;
-    }
-    if (d == 3) {
-        b[0] = blockIdx.z;
-        t[0] = threadIdx.z;
-    }
-    const AccContext acc(wd, make(d, b), make(d, t), kwSharedArena, sharedBytes);
+    const IndexVec bIdx = d == 1 ? IndexVec(blockIdx.x)
+                          : d == 2 ? IndexVec(blockIdx.y, blockIdx.x)
+                                   : IndexVec(blockIdx.z, blockIdx.y, blockIdx.x);
+    const IndexVec tIdx = d == 1 ? IndexVec(threadIdx.x)
+                          : d == 2 ? IndexVec(threadIdx.y, threadIdx.x)
+                                   : IndexVec(threadIdx.z, threadIdx.y, threadIdx.x);
+    const AccContext acc(wd, bIdx, tIdx, kwSharedArena, sharedBytes);
     kernel(acc, args...);
 }
 

@@ -153,7 +153,18 @@ TEST_CASE("README functor runs unchanged on the GPU, bitwise equal to axpyRefere
     Buffer dx = upload(x), dy = upload(y);
     executeTask(kBk, divideForBackend(IndexVec(n), kBk, IndexVec(256), IndexVec(4)), ScaleKernel{}, n, 2.5, view(dx),
                 view(dy));
-    CHECK(download<double>(dy, n) == want);
+    const auto got = download<double>(dy, n);
+    std::size_t bad = 0, first = n;
+    for (std::size_t i = 0; i < n; ++i)
+        if (got[i] != want[i]) {
+            if (first == n)
+                first = i;
+            ++bad;
+        }
+    if (bad)
+        std::printf("  %zu mismatches, first at %zu: got %.17g want %.17g (x %.17g y %.17g)\n", bad, first,
+                    got[first], want[first], x[first], y[first]);
+    CHECK(bad == 0);
 }
 
 TEST_CASE("index spellings agree on the device (test_accel.cpp:61-86)")
