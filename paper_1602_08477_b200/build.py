@@ -74,6 +74,12 @@ def build_cpp_tests(force: bool = False) -> list[Path]:
             _run(["g++", "-O2", "-std=c++20", "-Wall", "-Wextra", f"-I{INCLUDE}", str(src), "-o", str(exe),
                   f"-L{PKG}", "-lkw_b200", f"-Wl,-rpath,{PKG}", "-Wl,-rpath,$ORIGIN/..", "-lpthread"])
         out.append(exe)
+    kwb = ROOT / "tools" / "kwbench" / "kwbench.cpp"
+    exe = BUILD / "kwbench"
+    if force or _stale(exe, [kwb, LIB] + hdrs):
+        _run(["g++", "-O2", "-std=c++20", "-Wall", "-Wextra", f"-I{INCLUDE}", str(kwb), "-o", str(exe), f"-L{PKG}",
+              "-lkw_b200", f"-Wl,-rpath,{PKG}", "-lpthread"])
+    out.append(exe)
     for src in sorted(cpp_dir.glob("*.cu")):
         exe = BUILD / src.stem
         if force or _stale(exe, [src, LIB] + hdrs + [INCLUDE / "kernelweave" / "cuda_exec.cuh"]):

@@ -676,6 +676,8 @@ using Tma128 = TmaCfg<128, 128, 64, 32, 6>;   // 7: 8 consumer warps + 1 produce
 using Tma128s4 = TmaCfg<128, 128, 64, 32, 4>; // 8
 using Tma64x128 = TmaCfg<64, 128, 32, 32, 6>; // 9: 8 consumers of 32x32
 using Tma128x64 = TmaCfg<128, 64, 64, 32, 6>; // 10: 4 consumers
+using Tma128w16 = TmaCfg<128, 128, 32, 32, 6>; // 11: 16 consumers of 32x32 (4 per scheduler)
+using Tma128s7 = TmaCfg<128, 128, 64, 32, 7>;  // 12: 7-stage ring (224 KiB)
 
 struct CfgInfo {
     int bm, bn, bk, threads, stages;
@@ -695,6 +697,8 @@ const CfgInfo kCfgs[] = {
     {Tma128s4::BM, Tma128s4::BN, Tma128s4::BK, Tma128s4::THREADS, Tma128s4::STAGES, launch_tma<Tma128s4>},
     {Tma64x128::BM, Tma64x128::BN, Tma64x128::BK, Tma64x128::THREADS, Tma64x128::STAGES, launch_tma<Tma64x128>},
     {Tma128x64::BM, Tma128x64::BN, Tma128x64::BK, Tma128x64::THREADS, Tma128x64::STAGES, launch_tma<Tma128x64>},
+    {Tma128w16::BM, Tma128w16::BN, Tma128w16::BK, Tma128w16::THREADS, Tma128w16::STAGES, launch_tma<Tma128w16>},
+    {Tma128s7::BM, Tma128s7::BN, Tma128s7::BK, Tma128s7::THREADS, Tma128s7::STAGES, launch_tma<Tma128s7>},
 };
 constexpr int kNumCfgs = sizeof(kCfgs) / sizeof(kCfgs[0]);
 int g_default_cfg128 = 7; // tile 128 -> TMA warp-specialised kernel (fastest in the sweep)

@@ -38,3 +38,36 @@ def test_generic_device_functors(programs):
     p = run(programs["test_functor_gpu"])
     assert p.returncode == 0, p.stdout + p.stderr
     assert "0 failures" in p.stdout
+
+
+def test_kwbench_usage_errors_exit_2(programs):
+    """tools/bench/main.cpp exit-code contract: 2 for usage errors (acceptance crit. 11)."""
+    for argv in (["--kernel", "foo"], ["--reps", "2"], ["--sizes", "0"], ["--backend", "blocks"],
+                 ["--kernel", "axpy", "--pessimize"], ["--bogus"]):
+        p = subprocess.run([str(programs["kwbench"]), *argv], capture_output=True, text=True, timeout=60)
+        assert p.returncode == 2, (argv, p.stdout, p.stderr)
+
+
+@pytest.mark.gpu
+def test_kwbench_gpu_csv_and_verification(programs, tmp_path):
+    """kwbench on the GPU: verified runs exit 0 with the reference's CSV schema; fault
+    injection (KWBENCH_INJECT_FAULT) makes verification fail with exit code 1."""
+    import csv
+    import os
+    exe = str(programs["kwbench"])
+    for argv, rows in ((["--kernel", "axpy", "--dtype", "f32", "--sizes", "1000003,4096"], 6),
+                       (["--kernel", "axpy", "--sizes", "4099"], 3),
+                       (["--kernel", "gemm-naive", "--sizes", "64,100", "--tpb", "4", "--ept", "4"], 6),
+                       (["--kernel", "gemm-tiled", "--sizes", "256,300", "--tile", "128", "--pessimize"], 12)):
+        out = tmp_path / "r.csv"
+        p = subprocess.run([exe, *argv, "--reps", "3", "--verify", "--csv", str(out)], capture_output=True,
+                           text=True, timeout=600)
+        assert p.returncode == 0, (argv, p.stdout, p.stderr)
+        recs = list(csv.DictReader(out.open()))
+        assert list(recs[0].keys()) == ["kernel", "backend", "n", "b", "v", "tile", "rep", "seconds", "gflops",
+                                        "verified"]
+        assert len(recs) == rows and all(r["verified"] == "1" and r["backend"] == "gpu" for r in recs)
+    env = dict(os.environ, KWBENCH_INJECT_FAULT="1")
+    p = subprocess.run([exe, "--kernel", "axpy", "--sizes", "1000", "--reps", "3", "--verify"], capture_output=True,
+                       text=True, timeout=120, env=env)
+    assert p.returncode == 1, p.stdout
