@@ -23,6 +23,9 @@ struct GemmArgs {
     const Buffer* b = nullptr;
     Buffer* c = nullptr;
     std::size_t tile = 128;
+    /// GemmTiledKernel only: bit-exact mode — separately rounded products and sums in
+    /// ascending k, bitwise equal to gemmReference (FP64-pipe bound, about half the DMMA rate).
+    bool bitwise = false;
 };
 
 struct GemmNaiveKernel {};
@@ -80,6 +83,10 @@ struct Launcher<kernels::GemmTiledKernel, kernels::GemmArgs> : GemmLauncherBase 
                             const kernels::GemmArgs& a)
     {
         const kw_workdiv w = wd.toC();
+        if (a.bitwise)
+            return kw_dgemm_bitwise(q, &w, a.m, a.n, a.k, a.alpha, a.a->rowData<double>(0), a.a->leadingDim<double>(),
+                                    a.b->rowData<double>(0), a.b->leadingDim<double>(), a.beta,
+                                    a.c->rowData<double>(0), a.c->leadingDim<double>());
         return kw_dgemm(q, &w, a.m, a.n, a.k, a.alpha, a.a->rowData<double>(0), a.a->leadingDim<double>(),
                         a.b->rowData<double>(0), a.b->leadingDim<double>(), a.beta, a.c->rowData<double>(0),
                         a.c->leadingDim<double>());

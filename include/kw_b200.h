@@ -165,6 +165,14 @@ KW_EXPORT kw_status kw_dgemm(kw_queue q, const kw_workdiv* wd, size_t m, size_t 
                              const double* A, size_t lda, const double* B, size_t ldb, double beta, double* C,
                              size_t ldc);
 
+/* K2 bitwise mode: the tiled DGEMM with separately rounded products and sums in ascending k —
+ * BITWISE equal to gemmReference and to the reference's GemmTiledKernel (test_kernels.cpp:208-230
+ * pins tiled == naive bitwise). FP64 pipe bound (two operations per term). 128x128 tiles of 256
+ * threads; device operands. */
+KW_EXPORT kw_status kw_dgemm_bitwise(kw_queue q, const kw_workdiv* wd, size_t m, size_t n, size_t k, double alpha,
+                                     const double* A, size_t lda, const double* B, size_t ldb, double beta, double* C,
+                                     size_t ldc);
+
 /* Tile-configuration sweep (BASELINE.json configs[4]): the DMMA kernel's instantiated
  * configurations, info = {BM, BN, BK, threads, stages}; device operands only. */
 KW_EXPORT int kw_dgemm_config_count(void);

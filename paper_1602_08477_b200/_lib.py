@@ -65,6 +65,8 @@ SIGNATURES = {
     "kw_axpy_f64": (st, [vp, C.POINTER(kw_workdiv), size_t, C.c_double, vp, vp]),
     "kw_dgemm": (st, [vp, C.POINTER(kw_workdiv), size_t, size_t, size_t, C.c_double, vp, size_t, vp, size_t,
                       C.c_double, vp, size_t]),
+    "kw_dgemm_bitwise": (st, [vp, C.POINTER(kw_workdiv), size_t, size_t, size_t, C.c_double, vp, size_t, vp,
+                              size_t, C.c_double, vp, size_t]),
     "kw_dgemm_config_count": (C.c_int, []),
     "kw_dgemm_config_info": (st, [C.c_int, C.c_int * 5]),
     "kw_dgemm_with_config": (st, [vp, C.c_int, size_t, size_t, size_t, C.c_double, vp, size_t, vp, size_t,

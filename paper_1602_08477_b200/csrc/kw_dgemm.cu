@@ -330,9 +330,18 @@ struct TmaCfg {
     // setmaxnreg moves registers from the producer warpgroup to the consumers.
     static constexpr int THREADS = 32 * (CONSUMERS + 4);
     static constexpr int PRODUCER_REGS = 40;
-    static constexpr int CONSUMER_REGS = ((65536 / 32 - 4 * PRODUCER_REGS) / CONSUMERS) / 8 * 8 > 240
-                                             ? 240
-                                             : ((65536 / 32 - 4 * PRODUCER_REGS) / CONSUMERS) / 8 * 8;
+    // The CTA's register pool is fixed at launch: ptxas pins a setmaxnreg kernel to the
+    // launch-bounds cap, floor(65536 / roundup(THREADS, 128) / 8) * 8 per thread. setmaxnreg.inc
+    // blocks until registers are free, so the consumers may only take what the producer
+    // warpgroup releases — asking for more deadlocks the CTA.
+    static constexpr int LAUNCH_REGS_RAW = (65536 / (((THREADS + 127) / 128) * 128)) / 8 * 8;
+    static constexpr int LAUNCH_REGS = LAUNCH_REGS_RAW > 255 ? 255 : LAUNCH_REGS_RAW;
+    static constexpr int POOL_PER_LANE = LAUNCH_REGS * (CONSUMERS + 4);
+    static constexpr int CONSUMER_REGS_RAW = ((POOL_PER_LANE - 4 * PRODUCER_REGS) / CONSUMERS) / 8 * 8;
+    static constexpr int CONSUMER_REGS = CONSUMER_REGS_RAW > 240 ? 240 : CONSUMER_REGS_RAW;
+    // Small CTAs already get (nearly) 255 registers per thread: no redistribution needed.
+    static constexpr bool REBALANCE = CONSUMER_REGS > LAUNCH_REGS;
+    static_assert(4 * PRODUCER_REGS + CONSUMERS * CONSUMER_REGS <= POOL_PER_LANE, "register pool overcommitted");
     static_assert(CONSUMERS % 4 == 0, "consumer warps form whole warpgroups (setmaxnreg granularity)");
     static constexpr int MT = WM / 8, NT = WN / 8;
     static constexpr uint32_t A_BYTES = BM * 128; // BM rows of 16 doubles
@@ -375,7 +384,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
 
     if (warp >= Cfg::CONSUMERS) {
         // ---------------- producer warpgroup ----------------
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(Cfg::PRODUCER_REGS));
+        if constexpr (Cfg::REBALANCE)
+            asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(Cfg::PRODUCER_REGS));
         if (warp == Cfg::CONSUMERS && lane == 0) {
             tma_prefetch_desc(&tmA);
             tma_prefetch_desc(&tmB);
@@ -395,7 +405,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     }
 
     // ---------------- consumers ----------------
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(Cfg::CONSUMER_REGS));
+    if constexpr (Cfg::REBALANCE)
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(Cfg::CONSUMER_REGS));
     const int wm = (warp / Cfg::WARPS_N) * Cfg::WM;
     const int wn = (warp % Cfg::WARPS_N) * Cfg::WN;
     const int g = lane >> 2, t = lane & 3;
@@ -597,6 +608,190 @@ __global__ void dgemm_naive_kernel(GemmParams p, int er, int ec)
     }
 }
 
+
+// ------------------------------------------------------------------------------------------
+// K2-bitwise: tiled DGEMM that is BITWISE equal to gemmReference (reference.cpp:14-26) and to
+// the reference's own GemmTiledKernel (gemm.cpp:40-118, which test_kernels.cpp:208-230 pins
+// bitwise to the naive kernel). Every output element is accumulated from +0.0 over k = 0..K-1
+// in ascending order with separately rounded products and sums (DMUL then DADD, never DFMA),
+// then fl(fl(alpha*acc) + fl(beta*c)). Padded k never enters a sum. FP64 pipe bound: two
+// pipe operations per term, so at most half the DFMA rate.
+//   block tile 128 x 128, k-tile 16, 256 threads; thread (ty, tx) owns C[ty + 16i][tx + 16j],
+//   i, j < 8 (64 independent accumulation chains); A staged row-major with a 144-byte row
+//   pitch (two rows read by one warp land in different banks), B row-major; 3-stage cp.async.
+// ------------------------------------------------------------------------------------------
+namespace bw {
+constexpr int BM = 128, BN = 128, BK = 16, THREADS = 256, STAGES = 3;
+constexpr int A_LD = BK + 2; // doubles; 144-byte rows
+constexpr int A_STAGE = BM * A_LD, B_STAGE = BK * BN;
+constexpr size_t SMEM = static_cast<size_t>(STAGES) * (A_STAGE + B_STAGE) * sizeof(double);
+} // namespace bw
+
+template <bool VEC16>
+__device__ __forceinline__ void bw_load_stage(const GemmParams& p, double* sA, double* sB, int bm, int bn, int k0,
+                                              int tid)
+{
+#pragma unroll
+    for (int it = 0; it < (bw::BM * bw::BK / 2) / bw::THREADS; ++it) {
+        const int c = tid + it * bw::THREADS;
+        const int row = c / (bw::BK / 2), kc = c % (bw::BK / 2);
+        const int gm = bm + row, gk = k0 + kc * 2;
+        int valid = 0;
+        if (gm < p.m) {
+            valid = p.k - gk;
+            valid = valid < 0 ? 0 : (valid > 2 ? 2 : valid);
+        }
+        const double* src = valid > 0 ? p.a + gm * p.lda + gk : p.a;
+        const uint32_t dst = smem_u32(sA + row * bw::A_LD + kc * 2);
+        if (VEC16) {
+            cp_async16(dst, src, valid * 8);
+        }
+        else {
+            cp_async8(dst, src, valid >= 1 ? 8 : 0);
+            cp_async8(dst + 8, valid >= 2 ? src + 1 : p.a, valid >= 2 ? 8 : 0);
+        }
+    }
+#pragma unroll
+    for (int it = 0; it < (bw::BK * bw::BN / 2) / bw::THREADS; ++it) {
+        const int c = tid + it * bw::THREADS;
+        const int row = c / (bw::BN / 2), nc = c % (bw::BN / 2);
+        const int gk = k0 + row, gn = bn + nc * 2;
+        int valid = 0;
+        if (gk < p.k) {
+            valid = p.n - gn;
+            valid = valid < 0 ? 0 : (valid > 2 ? 2 : valid);
+        }
+        const double* src = valid > 0 ? p.b + gk * p.ldb + gn : p.b;
+        const uint32_t dst = smem_u32(sB + row * bw::BN + nc * 2);
+        if (VEC16) {
+            cp_async16(dst, src, valid * 8);
+        }
+        else {
+            cp_async8(dst, src, valid >= 1 ? 8 : 0);
+            cp_async8(dst + 8, valid >= 2 ? src + 1 : p.b, valid >= 2 ? 8 : 0);
+        }
+    }
+}
+
+template <bool VEC16>
+__global__ void __launch_bounds__(bw::THREADS, 1) dgemm_bitwise_kernel(GemmParams p)
+{
+    extern __shared__ __align__(128) double smem[];
+    double* sA = smem;
+    double* sB = smem + bw::STAGES * bw::A_STAGE;
+    constexpr int GROUP = 8;
+    const int tile = blockIdx.x;
+    const int per_group = GROUP * p.tiles_n;
+    const int group = tile / per_group;
+    const int first_m = group * GROUP;
+    const int gsize = (p.tiles_m - first_m) < GROUP ? (p.tiles_m - first_m) : GROUP;
+    const int in_group = tile - group * per_group;
+    const int bm = (first_m + in_group % gsize) * bw::BM;
+    const int bn = (in_group / gsize) * bw::BN;
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+
+    double acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            acc[i][j] = 0.0;
+
+    const int ktiles = (p.k + bw::BK - 1) / bw::BK;
+#pragma unroll
+    for (int s = 0; s < bw::STAGES - 1; ++s) {
+        if (s < ktiles)
+            bw_load_stage<VEC16>(p, sA + s * bw::A_STAGE, sB + s * bw::B_STAGE, bm, bn, s * bw::BK, tid);
+        cp_async_commit();
+    }
+    for (int kt = 0; kt < ktiles; ++kt) {
+        cp_async_wait<bw::STAGES - 2>();
+        __syncthreads();
+        {
+            const int nk = kt + bw::STAGES - 1;
+            if (nk < ktiles) {
+                const int s = nk % bw::STAGES;
+                bw_load_stage<VEC16>(p, sA + s * bw::A_STAGE, sB + s * bw::B_STAGE, bm, bn, nk * bw::BK, tid);
+            }
+            cp_async_commit();
+        }
+        const int s = kt % bw::STAGES;
+        const double* a_s = sA + s * bw::A_STAGE + ty * bw::A_LD;
+        const double* b_s = sB + s * bw::B_STAGE + tx;
+        const int kend = (p.k - kt * bw::BK) < bw::BK ? (p.k - kt * bw::BK) : bw::BK; // no padded terms
+        if (kend == bw::BK) {
+#pragma unroll
+            for (int kk = 0; kk < bw::BK; ++kk) {
+                double a[8], b[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    a[i] = a_s[i * 16 * bw::A_LD + kk];
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    b[j] = b_s[kk * bw::BN + j * 16];
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        acc[i][j] = __dadd_rn(acc[i][j], __dmul_rn(a[i], b[j]));
+            }
+        }
+        else {
+            for (int kk = 0; kk < kend; ++kk) {
+                double a[8], b[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    a[i] = a_s[i * 16 * bw::A_LD + kk];
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    b[j] = b_s[kk * bw::BN + j * 16];
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        acc[i][j] = __dadd_rn(acc[i][j], __dmul_rn(a[i], b[j]));
+            }
+        }
+    }
+    cp_async_wait<0>();
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int row = bm + ty + 16 * i;
+        if (row >= p.m)
+            continue;
+        double* crow = p.c + row * p.ldc;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int col = bn + tx + 16 * j;
+            if (col < p.n)
+                crow[col] = __dadd_rn(__dmul_rn(p.alpha, acc[i][j]), __dmul_rn(p.beta, crow[col]));
+        }
+    }
+}
+
+kw_status launch_bitwise(cudaStream_t s, const GemmParams& p0)
+{
+    GemmParams p = p0;
+    p.tiles_m = static_cast<int>(kw::ceil_div(p.m, bw::BM));
+    p.tiles_n = static_cast<int>(kw::ceil_div(p.n, bw::BN));
+    const long long tiles = static_cast<long long>(p.tiles_m) * p.tiles_n;
+    if (tiles > INT_MAX)
+        return kw::usage("dgemm: problem too large for the tile grid");
+    const bool vec16 = (p.lda % 2 == 0) && (p.ldb % 2 == 0) && (reinterpret_cast<uintptr_t>(p.a) % 16 == 0) &&
+                       (reinterpret_cast<uintptr_t>(p.b) % 16 == 0);
+    auto kern = vec16 ? dgemm_bitwise_kernel<true> : dgemm_bitwise_kernel<false>;
+    static bool attr[2] = {false, false};
+    if (!attr[vec16]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bw::SMEM));
+        if (e != cudaSuccess)
+            return kw::cuda_fail("dgemm_bitwise: cudaFuncSetAttribute", e);
+        attr[vec16] = true;
+    }
+    kern<<<static_cast<unsigned>(tiles), bw::THREADS, bw::SMEM, s>>>(p);
+    kw::g_launches.fetch_add(1, std::memory_order_relaxed);
+    return KW_OK;
+}
+
 kw_status validate_gemm(size_t m, size_t n, size_t k, const double* A, size_t lda, const double* B, size_t ldb,
                         const double* C, size_t ldc)
 {
@@ -676,8 +871,8 @@ using Tma128 = TmaCfg<128, 128, 64, 32, 6>;   // 7: 8 consumer warps + 1 produce
 using Tma128s4 = TmaCfg<128, 128, 64, 32, 4>; // 8
 using Tma64x128 = TmaCfg<64, 128, 32, 32, 6>; // 9: 8 consumers of 32x32
 using Tma128x64 = TmaCfg<128, 64, 64, 32, 6>; // 10: 4 consumers
-using Tma128w16 = TmaCfg<128, 128, 32, 32, 6>; // 11: 16 consumers of 32x32 (4 per scheduler)
-using Tma128s7 = TmaCfg<128, 128, 64, 32, 7>;  // 12: 7-stage ring (224 KiB)
+using Tma128s7 = TmaCfg<128, 128, 64, 32, 7>; // 11: 7-stage ring (224 KiB)
+// (16 consumer warps of 32x32 were measured out: 104 registers per consumer spill.)
 
 struct CfgInfo {
     int bm, bn, bk, threads, stages;
@@ -697,7 +892,6 @@ const CfgInfo kCfgs[] = {
     {Tma128s4::BM, Tma128s4::BN, Tma128s4::BK, Tma128s4::THREADS, Tma128s4::STAGES, launch_tma<Tma128s4>},
     {Tma64x128::BM, Tma64x128::BN, Tma64x128::BK, Tma64x128::THREADS, Tma64x128::STAGES, launch_tma<Tma64x128>},
     {Tma128x64::BM, Tma128x64::BN, Tma128x64::BK, Tma128x64::THREADS, Tma128x64::STAGES, launch_tma<Tma128x64>},
-    {Tma128w16::BM, Tma128w16::BN, Tma128w16::BK, Tma128w16::THREADS, Tma128w16::STAGES, launch_tma<Tma128w16>},
     {Tma128s7::BM, Tma128s7::BN, Tma128s7::BK, Tma128s7::THREADS, Tma128s7::STAGES, launch_tma<Tma128s7>},
 };
 constexpr int kNumCfgs = sizeof(kCfgs) / sizeof(kCfgs[0]);
@@ -926,6 +1120,38 @@ kw_status kw_dgemm(kw_queue qh, const kw_workdiv* wd, size_t m, size_t n, size_t
         return kw::after_enqueue(q, "dgemm");
     }
     return dgemm_staged(q, tile, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, a_dev, b_dev, c_dev);
+}
+
+
+kw_status kw_dgemm_bitwise(kw_queue qh, const kw_workdiv* wd, size_t m, size_t n, size_t k, double alpha,
+                           const double* A, size_t lda, const double* B, size_t ldb, double beta, double* C, size_t ldc)
+{
+    KW_CHECK_QUEUE(qh);
+    auto* q = reinterpret_cast<kw::Queue*>(qh);
+    kw_status st = validate_gemm(m, n, k, A, lda, B, ldb, C, ldc);
+    if (st != KW_OK)
+        return st;
+    if (wd != nullptr) {
+        if (wd->dim != 2)
+            return kw::usage("dgemm_bitwise: the tiled kernel runs on a 2-D (rows, cols) work division");
+        if (wd->threads[0] * wd->elems[0] != 128 || wd->threads[1] * wd->elems[1] != 128 ||
+            wd->threads[0] * wd->threads[1] != 256)
+            return kw::usage("dgemm_bitwise: the bitwise tiled kernel runs 128x128 tiles of 256 threads "
+                             "(gemmTiledWorkDiv(GpuCudaRt, m, n, 128))");
+        if (wd->blocks[0] * 128 < m || wd->blocks[1] * 128 < n)
+            return kw::usage("dgemm: work division does not cover the m x n output");
+    }
+    if (m == 0 || n == 0)
+        return KW_OK;
+    kw::DeviceGuard g(q->device);
+    int d = -1;
+    if (kw::pointer_kind(C, &d) != KW_MEM_DEVICE || (k > 0 && (kw::pointer_kind(A, &d) != KW_MEM_DEVICE ||
+                                                               kw::pointer_kind(B, &d) != KW_MEM_DEVICE)))
+        return kw::usage("dgemm_bitwise: operands must be device buffers");
+    st = launch_bitwise(q->stream, make_params(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc));
+    if (st != KW_OK)
+        return kw::task_fail(q, kw::last_error());
+    return kw::after_enqueue(q, "dgemm_bitwise");
 }
 
 int kw_dgemm_config_count(void) { return kNumCfgs; }

@@ -616,6 +616,7 @@ class GemmArgs:
     b: Optional[Buffer] = None
     c: Optional[Buffer] = None
     tile: int = 128
+    bitwise: bool = False  # tiled kernel in bit-exact mode (separately rounded, ascending k)
 
 
 class AxpyKernel:
@@ -654,7 +655,10 @@ class GemmTiledKernel:
         if c.extent()[0] < args.m or c.extent()[1] < args.n:
             raise UsageError("gemm: extents exceed a buffer extent")
         cwd = wd.to_c()
-        f = L.lib().kw_dgemm_naive if self.naive else L.lib().kw_dgemm
+        if self.naive:
+            f = L.lib().kw_dgemm_naive
+        else:
+            f = L.lib().kw_dgemm_bitwise if args.bitwise else L.lib().kw_dgemm
         vals = (int(args.m), int(args.n), int(args.k), float(args.alpha), a.data(), a.leadingDim(), b.data(),
                 b.leadingDim(), float(args.beta), c.data(), c.leadingDim())
         keep = (a, b, c)

@@ -247,3 +247,37 @@ def test_every_tile_configuration_within_tolerance(gpu, oracle):
             q.wait()
             ok, worst = within_tol(Cb.download(), ref, k)
             assert ok, (cfg, m, n, k, worst)
+
+
+def tiled_bitwise(dev, alpha, beta, a, b, c, align=64):
+    m, k = a.shape
+    n = b.shape[1]
+    A, B, Cb = mat(dev, a, align=align), mat(dev, b, align=align), mat(dev, c, align=align)
+    kw.executeTask(GPU, kw.gemmTiledWorkDiv(GPU, m, n, 128), kw.GemmTiledKernel(),
+                   kw.GemmArgs(m, n, k, alpha, beta, A, B, Cb, 128, bitwise=True))
+    return Cb.download()
+
+
+def test_tiled_bitwise_mode_is_bit_exact(gpu, oracle, golden):
+    """GemmTiledKernel in bitwise mode reproduces the reference bit for bit — the reference's
+    own contract tiled == naive == gemmReference (test_kernels.cpp:184-279)."""
+    for case in (4, 5):
+        c = golden["workloads"][case]
+        alpha, beta, a, b, cin = oracle.workload_gemm(c["n"], c["seed"], "gemm-tiled")
+        assert h(oracle.fnv1a64(tiled_bitwise(gpu, alpha, beta, a, b, cin))) == c["c_out_digest"]
+    rng = oracle.MT64(seed=5678)
+    for s in list(range(1, 65)) + [65, 127, 129, 200]:
+        a, b, c = (rng.fill_uniform(s * s).reshape(s, s) for _ in range(3))
+        assert np.array_equal(tiled_bitwise(gpu, 1.25, 0.75, a, b, c), oracle.gemm(1.25, 0.75, a, b, c)), s
+    rng2 = np.random.default_rng(17)
+    for (m, n, k) in ((13, 29, 7), (130, 257, 33), (257, 130, 1), (64, 200, 513), (1, 1, 1)):
+        a, b, c = rng2.standard_normal((m, k)), rng2.standard_normal((k, n)), rng2.standard_normal((m, n))
+        for align in (8, 64):
+            got = tiled_bitwise(gpu, 1.5, -0.5, a, b, c, align)
+            assert np.array_equal(got, oracle.gemm(1.5, -0.5, a, b, c)), (m, n, k, align)
+
+
+def test_tiled_bitwise_4096(gpu, oracle):
+    n = 4096
+    alpha, beta, a, b, c = oracle.workload_gemm(n, 42)
+    assert np.array_equal(tiled_bitwise(gpu, alpha, beta, a, b, c), oracle.gemm(alpha, beta, a, b, c))

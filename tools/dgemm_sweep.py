@@ -46,6 +46,22 @@ def main():
             tf = 2 * n ** 3 * reps / (ms.value / 1e3) / 1e12
             print(json.dumps({"n": n, "cfg": cfg, "BM": info[0], "BN": info[1], "BK": info[2], "threads": info[3],
                               "stages": info[4], "tflops": round(tf, 3)}), flush=True)
+        # bit-exact tiled mode (kw_dgemm_bitwise)
+        def gob():
+            L.check(lib.kw_dgemm_bitwise(q.handle(), None, n, n, n, 1.0, A.data(), A.leadingDim(), B.data(),
+                                         B.leadingDim(), 1.0, Cb.data(), Cb.leadingDim()))
+        gob()
+        q.wait()
+        e0, e1 = C.c_void_p(), C.c_void_p()
+        lib.kw_event_record(q.handle(), C.byref(e0))
+        rb = max(2, reps // 2)
+        for _ in range(rb):
+            gob()
+        lib.kw_event_record(q.handle(), C.byref(e1))
+        ms = C.c_float()
+        L.check(lib.kw_event_elapsed_ms(e0, e1, C.byref(ms)))
+        print(json.dumps({"n": n, "cfg": "bitwise", "tflops": round(2 * n ** 3 * rb / (ms.value / 1e3) / 1e12, 3)}),
+              flush=True)
         try:
             import torch
             a = torch.rand(n, n, dtype=torch.float64, device="cuda")
