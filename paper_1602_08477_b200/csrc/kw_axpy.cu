@@ -275,9 +275,11 @@ template <typename T>
 kw_status run_staged(kw::Queue* q, uint32_t threads, uint32_t elems, size_t limit, T alpha, const T* x, T* y,
                      bool x_dev, bool y_dev)
 {
-    constexpr size_t kChunkBytes = 32u << 20; // per operand per slot
+    // 8 MiB per operand per slot, 4 slots: short pipeline fill/drain (the first D2H can start
+    // after 16 MiB of H2D) while each copy stays large enough to run at full PCIe rate.
+    constexpr size_t kChunkBytes = 8u << 20;
     const size_t chunk = kChunkBytes / sizeof(T);
-    const int ring = 3;
+    const int ring = kw::Queue::kRing;
     const size_t slot_elems = chunk * 2;
     kw_status st = kw::ensure_scratch(q, ring * slot_elems * sizeof(T));
     if (st != KW_OK)

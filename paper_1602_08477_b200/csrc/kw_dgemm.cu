@@ -321,9 +321,10 @@ __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map)
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
 
-template <int BM_, int BN_, int WM_, int WN_, int STAGES_>
+template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int MIN_BLOCKS_ = 1>
 struct TmaCfg {
     static constexpr int BM = BM_, BN = BN_, BK = 16, WM = WM_, WN = WN_, STAGES = STAGES_;
+    static constexpr int MIN_BLOCKS = MIN_BLOCKS_; // co-resident CTAs per SM
     static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
     static constexpr int CONSUMERS = WARPS_M * WARPS_N;
     // Consumer warps + one producer warpgroup (4 warps: one issues TMA, the others exit).
@@ -334,7 +335,7 @@ struct TmaCfg {
     // launch-bounds cap, floor(65536 / roundup(THREADS, 128) / 8) * 8 per thread. setmaxnreg.inc
     // blocks until registers are free, so the consumers may only take what the producer
     // warpgroup releases — asking for more deadlocks the CTA.
-    static constexpr int LAUNCH_REGS_RAW = (65536 / (((THREADS + 127) / 128) * 128)) / 8 * 8;
+    static constexpr int LAUNCH_REGS_RAW = (65536 / MIN_BLOCKS / (((THREADS + 127) / 128) * 128)) / 8 * 8;
     static constexpr int LAUNCH_REGS = LAUNCH_REGS_RAW > 255 ? 255 : LAUNCH_REGS_RAW;
     static constexpr int POOL_PER_LANE = LAUNCH_REGS * (CONSUMERS + 4);
     static constexpr int CONSUMER_REGS_RAW = ((POOL_PER_LANE - 4 * PRODUCER_REGS) / CONSUMERS) / 8 * 8;
@@ -352,7 +353,7 @@ struct TmaCfg {
 };
 
 template <class Cfg>
-__global__ void __launch_bounds__(Cfg::THREADS, 1)
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmParams p)
 {
     extern __shared__ uint8_t smem_raw[];
@@ -872,6 +873,8 @@ using Tma128s4 = TmaCfg<128, 128, 64, 32, 4>; // 8
 using Tma64x128 = TmaCfg<64, 128, 32, 32, 6>; // 9: 8 consumers of 32x32
 using Tma128x64 = TmaCfg<128, 64, 64, 32, 6>; // 10: 4 consumers
 using Tma128s7 = TmaCfg<128, 128, 64, 32, 7>; // 11: 7-stage ring (224 KiB)
+using Tma128x64x2 = TmaCfg<128, 64, 64, 32, 4, 2>; // 12: two CTAs per SM, 4 consumers each
+using Tma64x128x2 = TmaCfg<64, 128, 64, 32, 4, 2>; // 13
 // (16 consumer warps of 32x32 were measured out: 104 registers per consumer spill.)
 
 struct CfgInfo {
@@ -893,6 +896,10 @@ const CfgInfo kCfgs[] = {
     {Tma64x128::BM, Tma64x128::BN, Tma64x128::BK, Tma64x128::THREADS, Tma64x128::STAGES, launch_tma<Tma64x128>},
     {Tma128x64::BM, Tma128x64::BN, Tma128x64::BK, Tma128x64::THREADS, Tma128x64::STAGES, launch_tma<Tma128x64>},
     {Tma128s7::BM, Tma128s7::BN, Tma128s7::BK, Tma128s7::THREADS, Tma128s7::STAGES, launch_tma<Tma128s7>},
+    {Tma128x64x2::BM, Tma128x64x2::BN, Tma128x64x2::BK, Tma128x64x2::THREADS, Tma128x64x2::STAGES,
+     launch_tma<Tma128x64x2>},
+    {Tma64x128x2::BM, Tma64x128x2::BN, Tma64x128x2::BK, Tma64x128x2::THREADS, Tma64x128x2::STAGES,
+     launch_tma<Tma64x128x2>},
 };
 constexpr int kNumCfgs = sizeof(kCfgs) / sizeof(kCfgs[0]);
 int g_default_cfg128 = 7; // tile 128 -> TMA warp-specialised kernel (fastest in the sweep)
