@@ -125,36 +125,48 @@ class ClockSampler:
 # distributed plumbing
 # --------------------------------------------------------------------------------------------
 class Dist:
-    def __init__(self, n_gpus: int):
+    def __init__(self, n_gpus: int, backend: str = "nccl", same_gpu: bool = False):
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
-        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        # --same-gpu (gloo only): every rank on GPU 0 — a harness self-test of the N > 1 code path
+        # on a one-GPU box; ranks never wait on one another inside a kernel.
+        self.local = 0 if same_gpu else int(os.environ.get("LOCAL_RANK", "0"))
+        self.backend = backend
         self.pg = None
         if self.world > 1:
             import torch
             import torch.distributed as dist
             torch.cuda.set_device(self.local)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            if backend == "nccl":
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            else:
+                dist.init_process_group("gloo")
             self.dist = dist
             self.torch = torch
         if n_gpus != self.world and self.rank == 0:
             print(f"warning: --gpus {n_gpus} but WORLD_SIZE={self.world}", file=sys.stderr)
 
+    def _dev(self):
+        return "cuda" if self.backend == "nccl" else "cpu"
+
     def barrier(self):
         if self.world > 1:
-            self.dist.barrier(device_ids=[self.local])
+            if self.backend == "nccl":
+                self.dist.barrier(device_ids=[self.local])
+            else:
+                self.dist.barrier()
 
     def max(self, v: float) -> float:
         if self.world == 1:
             return v
-        t = self.torch.tensor([v], dtype=self.torch.float64, device="cuda")
+        t = self.torch.tensor([v], dtype=self.torch.float64, device=self._dev())
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
 
     def sum(self, v: float) -> float:
         if self.world == 1:
             return v
-        t = self.torch.tensor([v], dtype=self.torch.float64, device="cuda")
+        t = self.torch.tensor([v], dtype=self.torch.float64, device=self._dev())
         self.dist.all_reduce(t)
         return float(t.item())
 
@@ -296,7 +308,10 @@ def run_ours(args, dist: Dist) -> dict:
                        "buffers)) + wait, wall clock; chunked H2D/kernel/D2H on two streams"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "peak_source": peak_src,
-                     "traffic": traffic_from_profiles("axpy_f32"),
+                     "traffic": (None if traffic_from_profiles("axpy_f32") is None
+                                 else round(traffic_from_profiles("axpy_f32") * n / N_AXPY)),
+                     "traffic_source": "profiles/traffic.json (ncu --set full at n=2^28, scaled to this rank's "
+                                       "shard)",
                      "kernel": "axpy_vec_kernel<float,4>", "bytes_per_launch": BYTES_PER_ELEM * n},
         "gpu_launches": int(launches),
         "clocks": clocks,
@@ -341,7 +356,7 @@ def run_dgemm(args, dist, kw, L, lib, dev, q, sampler) -> dict:
         return dist.max(ms.value)
 
     rng = np.random.default_rng(77)
-    if dist.world == 1:
+    if dist.world == 1 and not args.force_rowsharded:
         for size, steps in ((8192, args.dgemm_steps), (4096, args.dgemm_steps * 4)):
             a = rng.random((size, size)) * 10
             b = rng.random((size, size)) * 10
@@ -568,6 +583,10 @@ def main():
     ap.add_argument("--ref-steps", type=int, default=10)
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-dgemm", action="store_true")
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl")
+    ap.add_argument("--same-gpu", action="store_true", help="self-test: all ranks on GPU 0 (gloo only)")
+    ap.add_argument("--force-rowsharded", action="store_true",
+                    help="self-test: run the 16384^3 row-sharded NCCL path even at world size 1")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules; using 3", file=sys.stderr)
@@ -582,7 +601,9 @@ def main():
         out = run_reference(args, _D())
         print(json.dumps(out), flush=True)
         return 0
-    dist = Dist(args.gpus)
+    if args.same_gpu and args.dist_backend != "gloo":
+        ap.error("--same-gpu requires --dist-backend gloo")
+    dist = Dist(args.gpus, args.dist_backend, args.same_gpu)
     try:
         out = run_ours(args, dist)
     finally:

@@ -275,9 +275,13 @@ template <typename T>
 kw_status run_staged(kw::Queue* q, uint32_t threads, uint32_t elems, size_t limit, T alpha, const T* x, T* y,
                      bool x_dev, bool y_dev)
 {
-    // 8 MiB per operand per slot, 4 slots: short pipeline fill/drain (the first D2H can start
-    // after 16 MiB of H2D) while each copy stays large enough to run at full PCIe rate.
-    constexpr size_t kChunkBytes = 8u << 20;
+    // Chunk bytes per operand per slot (KW_STAGE_CHUNK_MB overrides; measured in
+    // profiles/e2e_chunk_sweep_r01.txt), 4 slots.
+    static const size_t kChunkBytes = [] {
+        const char* e = std::getenv("KW_STAGE_CHUNK_MB");
+        const long v = e ? std::atol(e) : 0;
+        return static_cast<size_t>(v > 0 && v <= 1024 ? v : 32) << 20;
+    }();
     const size_t chunk = kChunkBytes / sizeof(T);
     const int ring = kw::Queue::kRing;
     const size_t slot_elems = chunk * 2;
