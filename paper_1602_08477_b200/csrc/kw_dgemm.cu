@@ -321,9 +321,12 @@ __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map)
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
 
-template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int MIN_BLOCKS_ = 1>
+template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int MIN_BLOCKS_ = 1, bool PAIRED_ = false>
 struct TmaCfg {
     static constexpr int BM = BM_, BN = BN_, BK = 16, WM = WM_, WN = WN_, STAGES = STAGES_;
+    // PAIRED: k-slot map k = 8(t>>1) + 4(t&1) + 2((t>>1)^(s>>1)) + (s&1) puts the A fragments
+    // of k-steps 2q and 2q+1 in one 16-byte chunk -> A via LDS.128 (still conflict-free).
+    static constexpr bool PAIRED = PAIRED_;
     static constexpr int MIN_BLOCKS = MIN_BLOCKS_; // co-resident CTAs per SM
     static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
     static constexpr int CONSUMERS = WARPS_M * WARPS_N;
@@ -440,6 +443,75 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
             bf[j] = *reinterpret_cast<const double*>(sb + (j >> 1) * 2048 + (b_even[ks] ^ ((j & 1) ? 64u : 0u)));
     };
 
+    if constexpr (Cfg::PAIRED) {
+        // A pair fragments: one double2 per (i, q) = k-steps 2q and 2q+1; B per k-step.
+        const int a_bit = t >> 1, b_bit = t & 1;
+        uint32_t a_sw2[2], b_ev[4];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int k_half = 4 * a_bit + 2 * b_bit + (a_bit ^ q); // k >> 1 for both k-steps of the pair
+            a_sw2[q] = a_row + (static_cast<uint32_t>(k_half ^ g) << 4);
+        }
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+            const int k = 8 * a_bit + 4 * b_bit + 2 * (a_bit ^ (ks >> 1)) + (ks & 1);
+            b_ev[ks] = b_box + static_cast<uint32_t>(k) * 128u +
+                       ((static_cast<uint32_t>((g >> 1) ^ (k & 7)) << 4) | ((g & 1) << 3));
+        }
+        auto load_a2 = [&](const uint8_t* sa, int q, double2 (&a2)[Cfg::MT]) {
+#pragma unroll
+            for (int i = 0; i < Cfg::MT; ++i)
+                a2[i] = *reinterpret_cast<const double2*>(sa + a_sw2[q] + i * 1024);
+        };
+        auto load_b = [&](const uint8_t* sa, int ks, double (&bf)[Cfg::NT]) {
+            const uint8_t* sb = sa + Cfg::A_BYTES;
+#pragma unroll
+            for (int j = 0; j < Cfg::NT; ++j)
+                bf[j] = *reinterpret_cast<const double*>(sb + (j >> 1) * 2048 + (b_ev[ks] ^ ((j & 1) ? 64u : 0u)));
+        };
+        // A pairs double-buffered (one LDS.128 per row block covers two k-steps); B fragments
+        // one k-step ahead.
+        double2 a2[2][Cfg::MT];
+        double bf[2][Cfg::NT];
+        if (ktiles > 0) {
+            mbar_wait(&full[0], 0);
+            load_a2(smem, 0, a2[0]);
+            load_b(smem, 0, bf[0]);
+        }
+        for (int kt = 0; kt < ktiles; ++kt) {
+            const int s = kt % Cfg::STAGES;
+            const uint8_t* sa = smem + s * Cfg::STAGE_BYTES;
+            const uint8_t* sa2 = sa;
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {
+                const int q = ks >> 1, h = ks & 1;
+                const int bc = ks & 1, bn2 = bc ^ 1;
+                if (ks == 0)
+                    load_a2(sa, 1, a2[1]);
+                if (ks < 3) {
+                    load_b(sa, ks + 1, bf[bn2]);
+                }
+                else {
+                    __syncwarp();
+                    if (lane == 0)
+                        mbar_arrive(&empty[s]);
+                    if (kt + 1 < ktiles) {
+                        const int s2 = (kt + 1) % Cfg::STAGES;
+                        mbar_wait(&full[s2], static_cast<uint32_t>((kt + 1) / Cfg::STAGES) & 1u);
+                        sa2 = smem + s2 * Cfg::STAGE_BYTES;
+                        load_b(sa2, 0, bf[bn2]);
+                        load_a2(sa2, 0, a2[0]); // a2[0] is idle during k-steps 2 and 3
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < Cfg::MT; ++i)
+#pragma unroll
+                    for (int j = 0; j < Cfg::NT; ++j)
+                        dmma_8x8x4(acc[i][j][0], acc[i][j][1], h ? a2[q][i].y : a2[q][i].x, bf[bc][j]);
+            }
+        }
+    }
+    else {
     // Register double buffering: the fragments of the next k-step (or of the next stage's
     // first k-step) are loaded before the DMMAs of the current one are issued, so LDS latency
     // hides behind 32 DMMAs instead of stalling the warp.
@@ -475,6 +547,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
                 for (int j = 0; j < Cfg::NT; ++j)
                     dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[cur][i], bf[cur][j]);
         }
+    }
+
     }
 
     const bool c_vec = (p.ldc % 2 == 0) && (reinterpret_cast<uintptr_t>(p.c) % 16 == 0);
@@ -875,6 +949,8 @@ using Tma128x64 = TmaCfg<128, 64, 64, 32, 6>; // 10: 4 consumers
 using Tma128s7 = TmaCfg<128, 128, 64, 32, 7>; // 11: 7-stage ring (224 KiB)
 using Tma128x64x2 = TmaCfg<128, 64, 64, 32, 4, 2>; // 12: two CTAs per SM, 4 consumers each
 using Tma64x128x2 = TmaCfg<64, 128, 64, 32, 4, 2>; // 13
+using Tma128p = TmaCfg<128, 128, 64, 32, 6, 1, true>;       // 14: LDS.128 paired A fragments
+using Tma64x128x2p = TmaCfg<64, 128, 64, 32, 4, 2, true>;   // 15
 // (16 consumer warps of 32x32 were measured out: 104 registers per consumer spill.)
 
 struct CfgInfo {
@@ -900,9 +976,12 @@ const CfgInfo kCfgs[] = {
      launch_tma<Tma128x64x2>},
     {Tma64x128x2::BM, Tma64x128x2::BN, Tma64x128x2::BK, Tma64x128x2::THREADS, Tma64x128x2::STAGES,
      launch_tma<Tma64x128x2>},
+    {Tma128p::BM, Tma128p::BN, Tma128p::BK, Tma128p::THREADS, Tma128p::STAGES, launch_tma<Tma128p>},
+    {Tma64x128x2p::BM, Tma64x128x2p::BN, Tma64x128x2p::BK, Tma64x128x2p::THREADS, Tma64x128x2p::STAGES,
+     launch_tma<Tma64x128x2p>},
 };
 constexpr int kNumCfgs = sizeof(kCfgs) / sizeof(kCfgs[0]);
-int g_default_cfg128 = 7; // tile 128 -> TMA warp-specialised kernel (fastest in the sweep)
+int g_default_cfg128 = 14; // tile 128 -> TMA warp-specialised kernel, paired LDS.128 A fragments (tools/dgemm_ab.py)
 int g_default_cfg64 = 4;  // tile 64  -> this config
 
 kw_status launch_tiled(cudaStream_t s, int tile, const GemmParams& p)
