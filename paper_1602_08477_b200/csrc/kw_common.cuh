@@ -41,6 +41,8 @@ struct Queue {
     cudaEvent_t ev_join = nullptr;
     cudaEvent_t ev_start = nullptr;
     cudaEvent_t ev_b = nullptr;
+    static constexpr int kBPanels = 8;
+    cudaEvent_t ev_bp[kBPanels] = {}; // B column panel j uploaded (DGEMM e2e streaming)
 };
 
 // RAII device selector: the reference's queues are bound to one device; every entry point

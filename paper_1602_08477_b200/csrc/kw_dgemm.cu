@@ -1061,14 +1061,21 @@ kw_status dgemm_staged(kw::Queue* q, int tile, size_t m, size_t n, size_t k, dou
     cudaError_t e = cudaEventRecord(q->ev_start, q->stream);
     if (e == cudaSuccess)
         e = cudaStreamWaitEvent(q->h2d, q->ev_start, 0);
-    if (e == cudaSuccess && !b_dev && k > 0) {
-        double* bs = reinterpret_cast<double*>(base);
-        e = cudaMemcpy2DAsync(bs, ldbs * 8, B, ldb * 8, n * 8, k, cudaMemcpyHostToDevice, q->h2d);
-        if (e == cudaSuccess)
-            e = cudaEventRecord(q->ev_b, q->h2d);
-        if (e == cudaSuccess)
-            e = cudaStreamWaitEvent(q->stream, q->ev_b, 0);
-        Bd = bs;
+    // B streaming: B is uploaded in column panels into its dense device copy; the first row
+    // panel is computed block by block as the B panels land, the remaining row panels (full
+    // width) after the last one. Start latency = A_0 + C_0 + one B panel instead of all of B.
+    const bool stream_b = !b_dev && k > 0;
+    int nbp = 0;
+    size_t bw = n;
+    if (stream_b) {
+        bw = kw::ceil_div(kw::ceil_div(n, static_cast<size_t>(4)), 128) * 128;
+        nbp = static_cast<int>(kw::ceil_div(n, bw));
+        if (nbp > kw::Queue::kBPanels) {
+            bw = kw::ceil_div(n, static_cast<size_t>(kw::Queue::kBPanels));
+            bw = kw::ceil_div(bw, 128) * 128;
+            nbp = static_cast<int>(kw::ceil_div(n, bw));
+        }
+        Bd = reinterpret_cast<double*>(base);
         ldbd = ldbs;
     }
     char* slots = base + ((b_bytes + 255) / 256) * 256;
@@ -1104,9 +1111,30 @@ kw_status dgemm_staged(kw::Queue* q, int tile, size_t m, size_t n, size_t k, dou
         }
         if (e != cudaSuccess)
             break;
-        st = launch_tiled(q->stream, tile, make_params(rows, n, k, alpha, Ad, ldad, Bd, ldbd, beta, Cd, ldcd));
-        if (st != KW_OK)
-            return st;
+        if (pi == 0 && stream_b) {
+            // B column panels behind the first A/C panel on the copy stream; compute block (0, j)
+            // as soon as panel j is resident.
+            for (int j = 0; j < nbp && e == cudaSuccess; ++j) {
+                const size_t n0 = static_cast<size_t>(j) * bw, wj = n - n0 < bw ? n - n0 : bw;
+                e = cudaMemcpy2DAsync(const_cast<double*>(Bd) + n0, ldbs * 8, B + n0, ldb * 8, wj * 8, k,
+                                      cudaMemcpyHostToDevice, q->h2d);
+                if (e == cudaSuccess)
+                    e = cudaEventRecord(q->ev_bp[j], q->h2d);
+                if (e == cudaSuccess)
+                    e = cudaStreamWaitEvent(q->stream, q->ev_bp[j], 0);
+                if (e != cudaSuccess)
+                    break;
+                st = launch_tiled(q->stream, tile,
+                                  make_params(rows, wj, k, alpha, Ad, ldad, Bd + n0, ldbd, beta, Cd + n0, ldcd));
+                if (st != KW_OK)
+                    return st;
+            }
+        }
+        else {
+            st = launch_tiled(q->stream, tile, make_params(rows, n, k, alpha, Ad, ldad, Bd, ldbd, beta, Cd, ldcd));
+            if (st != KW_OK)
+                return st;
+        }
         e = cudaGetLastError();
         if (e == cudaSuccess && !c_dev) {
             e = cudaEventRecord(q->ev_ready[s], q->stream);

@@ -287,6 +287,8 @@ kw_status kw_queue_create(int device, int flavor, kw_queue* out)
         e = cudaEventCreateWithFlags(&q->ev_start, cudaEventDisableTiming);
     if (e == cudaSuccess)
         e = cudaEventCreateWithFlags(&q->ev_b, cudaEventDisableTiming);
+    for (int i = 0; e == cudaSuccess && i < Queue::kBPanels; ++i)
+        e = cudaEventCreateWithFlags(&q->ev_bp[i], cudaEventDisableTiming);
     if (e != cudaSuccess) {
         cudaGetLastError();
         delete q;
@@ -314,6 +316,9 @@ kw_status kw_queue_destroy(kw_queue qh)
             cudaEventDestroy(q->ev_h2d[i]);
     }
     for (cudaEvent_t e : {q->ev_join, q->ev_start, q->ev_b})
+        if (e)
+            cudaEventDestroy(e);
+    for (cudaEvent_t e : q->ev_bp)
         if (e)
             cudaEventDestroy(e);
     if (q->scratch)

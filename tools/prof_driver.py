@@ -32,8 +32,9 @@ def main():
             b = kw.Buffer(dev, kw.IndexVec(n, n), 8)
             b.upload(rng.random((n, n)))
             bufs.append(b)
+        bitwise = len(sys.argv) > 4 and sys.argv[4] == "bitwise"
         task = kw.createExec(GPU, kw.gemmTiledWorkDiv(GPU, n, n, tile), kw.GemmTiledKernel(),
-                             kw.GemmArgs(n, n, n, 1.0, 1.0, *bufs))
+                             kw.GemmArgs(n, n, n, 1.0, 1.0, *bufs, bitwise=bitwise))
     for _ in range(4):
         q.enqueue(task)
     q.wait()
