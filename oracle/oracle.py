@@ -98,6 +98,8 @@ def ref() -> C.CDLL:
         r.kwref_run_bench.argtypes = [C.c_char_p, C.c_char_p, sz, C.c_int, C.c_uint64, sz, sz, sz, C.c_int, dp,
                                       C.POINTER(C.c_int)]
         r.kwref_run_bench.restype = C.c_int
+        r.kwref_csv_roundtrip.argtypes = [C.c_char_p]
+        r.kwref_csv_roundtrip.restype = C.c_long
         _r = r
     return _r
 

@@ -30,8 +30,11 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <fstream>
 #include <random>
+#include <sstream>
 #include <string>
+#include <vector>
 
 using namespace kernelweave;
 
@@ -318,6 +321,29 @@ int kwref_run_bench(const char* kernel, const char* backend, std::size_t n, int 
         *median_seconds = bench::median(secs);
         *verified = ok ? 1 : 0;
     });
+}
+
+/// Parses a CSV file with the reference's readRecordsCsv (records.cpp:58-105) and re-emits it
+/// with writeRecordsCsv (records.cpp:17-42); returns the record count when the re-emitted bytes
+/// equal the file's (acceptance criterion 11's byte round-trip), -1 on a parse error, -2 when
+/// the bytes differ.
+long kwref_csv_roundtrip(const char* path)
+{
+    std::ifstream in(path, std::ios::binary);
+    std::stringstream original;
+    original << in.rdbuf();
+    std::vector<bench::BenchRecord> recs;
+    try {
+        std::istringstream is(original.str());
+        recs = bench::readRecordsCsv(is);
+    }
+    catch (const std::exception& e) {
+        g_error = e.what();
+        return -1;
+    }
+    std::ostringstream os;
+    bench::writeRecordsCsv(recs, os);
+    return os.str() == original.str() ? static_cast<long>(recs.size()) : -2;
 }
 
 } // extern "C"

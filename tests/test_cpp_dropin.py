@@ -67,6 +67,9 @@ def test_kwbench_gpu_csv_and_verification(programs, tmp_path):
         assert list(recs[0].keys()) == ["kernel", "backend", "n", "b", "v", "tile", "rep", "seconds", "gflops",
                                         "verified"]
         assert len(recs) == rows and all(r["verified"] == "1" and r["backend"] == "gpu" for r in recs)
+        from oracle import oracle as O
+        if O.ref_available():  # the reference's own readRecordsCsv/writeRecordsCsv: byte round-trip
+            assert O.ref().kwref_csv_roundtrip(str(out).encode()) == rows
     env = dict(os.environ, KWBENCH_INJECT_FAULT="1")
     p = subprocess.run([exe, "--kernel", "axpy", "--sizes", "1000", "--reps", "3", "--verify"], capture_output=True,
                        text=True, timeout=120, env=env)
