@@ -1,0 +1,43 @@
+"""e2e DGEMM (host pinned A, B, C through the public API) at n: streamed full-copy schedule vs
+the panel ring (KW_DGEMM_FORCE_RING=1), median of 3 wall-clock steps."""
+import os
+import statistics
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+from paper_1602_08477_b200 import kernelweave as kw  # noqa: E402
+
+
+def run(n, ring):
+    if ring:
+        os.environ["KW_DGEMM_FORCE_RING"] = "1"
+    else:
+        os.environ.pop("KW_DGEMM_FORCE_RING", None)
+    GPU = kw.BackendKind.GpuCudaRt
+    q = kw.Queue(kw.Device.gpu(0), kw.QueueFlavor.Async)
+    host = kw.Device.host()
+    bufs = [kw.Buffer(host, kw.IndexVec(n, n), 8) for _ in range(3)]
+    for b in bufs:
+        b.host_view()[:, :n] = 1.0
+    task = kw.createExec(GPU, kw.gemmTiledWorkDiv(GPU, n, n, 128), kw.GemmTiledKernel(),
+                         kw.GemmArgs(n, n, n, 1.0, 0.5, *bufs))
+    q.enqueue(task)
+    q.wait()
+    ts = []
+    for _ in range(3):
+        t = time.perf_counter()
+        q.enqueue(task)
+        q.wait()
+        ts.append(time.perf_counter() - t)
+    med = statistics.median(ts)
+    print(f"n={n} ring={ring} {med*1e3:.1f} ms {2*n**3/med/1e12:.2f} TFLOP/s")
+
+
+if __name__ == "__main__":
+    for n in (4096, 8192):
+        run(n, False)
+        run(n, True)
