@@ -39,11 +39,6 @@ BYTES_PER_ELEM = 12  # read X, read Y, write Y (fp32)
 FP64_NOMINAL_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # 37.2: 148 SMs x 64 FP64 FMA/clk x 1.965 GHz
 
 
-def env_int(name, default):
-    v = os.environ.get(name)
-    return int(v) if v else default
-
-
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():

@@ -575,9 +575,11 @@ kw_status kw_l2_flush(kw_queue qh)
 {
     KW_CHECK_QUEUE(qh);
     auto* q = reinterpret_cast<Queue*>(qh);
-    static void* flush_buf[64] = {};
+    static void* flush_buf[64] = {}; // per device: 2 x L2 bytes, written once per call
     static size_t flush_bytes[64] = {};
     static std::mutex mu;
+    if (q->device >= 64)
+        return kw::usage("l2 flush: device index beyond 63");
     kw::DeviceGuard g(q->device);
     std::lock_guard<std::mutex> lock(mu);
     if (!flush_buf[q->device]) {
@@ -590,7 +592,7 @@ kw_status kw_l2_flush(kw_queue qh)
         }
         flush_bytes[q->device] = bytes;
     }
-    cudaError_t e = cudaMemsetAsync(flush_buf[q->device], q->failed & 0xff, flush_bytes[q->device], q->stream);
+    cudaError_t e = cudaMemsetAsync(flush_buf[q->device], 0, flush_bytes[q->device], q->stream);
     if (e != cudaSuccess)
         return kw::task_fail(q, std::string("l2 flush: ") + cudaGetErrorString(e));
     return kw::after_enqueue(q, "l2 flush");

@@ -21,8 +21,8 @@ from __future__ import annotations
 import ctypes as C
 import enum
 import threading
-from dataclasses import dataclass, field
-from typing import Any, Callable, Optional
+from dataclasses import dataclass
+from typing import Callable, Optional
 
 import numpy as np
 

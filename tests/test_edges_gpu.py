@@ -1,7 +1,5 @@
 """GPU edge cases: empty and degenerate extents, and index ranges beyond 2^31 elements (64-bit
 addressing in the AXPY grid and the DGEMM TMA coordinates / epilogue)."""
-import ctypes as C
-
 import numpy as np
 import pytest
 

@@ -6,8 +6,6 @@ import sys
 import time
 from pathlib import Path
 
-import numpy as np
-
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_1602_08477_b200 import kernelweave as kw  # noqa: E402
 
