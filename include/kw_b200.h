@@ -119,7 +119,9 @@ KW_EXPORT kw_status kw_queue_shutdown(kw_queue q);
  * Sync queue completes the task before returning. */
 KW_EXPORT kw_status kw_queue_complete_launch(kw_queue q, int cuda_error, const char* what);
 
-/* TaskHandle (queue.hpp:36-52) as a CUDA event recorded after the last enqueued task. */
+/* TaskHandle (queue.hpp:36-52) as a CUDA event recorded after the last enqueued task. State is
+ * PENDING until the event completes, then DONE (FAILED on a device fault). A task's own launch
+ * failure is the KW_TASK returned by its kw_* call (the C++/Python handles carry it). */
 KW_EXPORT kw_status kw_event_record(kw_queue q, kw_event* ev);
 KW_EXPORT kw_status kw_event_state(kw_event ev, int* state);
 KW_EXPORT kw_status kw_event_destroy(kw_event ev);

@@ -114,7 +114,6 @@ struct kw_event_s {
     int device;
     cudaEvent_t ev;
     Queue* q;
-    size_t failed_at_record;
 };
 
 extern "C" {
@@ -410,17 +409,13 @@ kw_status kw_event_record(kw_queue qh, kw_event* out)
         return kw::usage("kw_event_record: null output");
     auto* q = reinterpret_cast<Queue*>(qh);
     kw::DeviceGuard g(q->device);
-    auto* ev = new kw_event_s{q->device, nullptr, q, 0};
+    auto* ev = new kw_event_s{q->device, nullptr, q};
     cudaError_t e = cudaEventCreate(&ev->ev);
     if (e == cudaSuccess)
         e = cudaEventRecord(ev->ev, q->stream);
     if (e != cudaSuccess) {
         delete ev;
         return kw::cuda_fail("event record", e);
-    }
-    {
-        std::lock_guard<std::mutex> lock(q->mu);
-        ev->failed_at_record = q->failed;
     }
     *out = ev;
     return KW_OK;
@@ -437,11 +432,9 @@ kw_status kw_event_state(kw_event ev, int* state)
         *state = KW_TASK_PENDING;
         return KW_OK;
     }
-    if (e != cudaSuccess) {
-        *state = KW_TASK_FAILED;
-        return KW_OK;
-    }
-    *state = ev->failed_at_record > 0 ? KW_TASK_FAILED : KW_TASK_DONE;
+    // A task's own launch failure is returned synchronously by its kw_* call (and collected for
+    // kw_queue_wait); the event reports completion, or a device fault (sticky, context-wide).
+    *state = e == cudaSuccess ? KW_TASK_DONE : KW_TASK_FAILED;
     return KW_OK;
 }
 

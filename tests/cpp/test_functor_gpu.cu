@@ -108,6 +108,43 @@ struct IndexKernel {
 };
 KW_DEVICE_FUNCTOR(IndexKernel)
 
+// A functor asking for more shared memory than an SM has: its launch fails on the device side.
+struct TooMuchSharedKernel {
+    static constexpr std::size_t sharedMemBytes = 512 * 1024;
+    __device__ void operator()(const AccContext&, BufferView) const {}
+};
+KW_DEVICE_FUNCTOR(TooMuchSharedKernel)
+
+TEST_CASE("failed tasks are collected, later tasks still run, wait() reports TaskError (queue.hpp:86-93)")
+{
+    Buffer counts = upload(std::vector<std::uint64_t>(64, 0));
+    Queue q(kGpu, QueueFlavor::Async);
+    const WorkDiv wd(IndexVec(1), IndexVec(64), IndexVec(1));
+    TaskHandle bad1 = q.enqueue(createExec(kBk, wd, TooMuchSharedKernel{}, view(counts)));
+    TaskHandle good = q.enqueue(createExec(kBk, wd, MarkKernel{}, view(counts)));
+    TaskHandle bad2 = q.enqueue(createExec(kBk, wd, TooMuchSharedKernel{}, view(counts)));
+    bool threw = false;
+    std::size_t failed = 0;
+    try {
+        q.wait();
+    }
+    catch (const TaskError& e) {
+        threw = true;
+        failed = e.failedCount();
+    }
+    CHECK(threw);
+    CHECK(failed == 2);
+    CHECK(bad1.state() == TaskState::Failed);
+    CHECK(bad2.state() == TaskState::Failed);
+    CHECK(good.state() == TaskState::Done);
+    const auto got = download<std::uint64_t>(counts, 64);
+    bool ok = true;
+    for (auto v : got)
+        ok = ok && v == 1; // the task between the failures ran
+    CHECK(ok);
+    q.wait(); // failures were reported once; the queue is clean again
+}
+
 TEST_CASE("invocation coverage: every (block, thread) exactly once (acceptance crit. 2)")
 {
     std::mt19937_64 rng(202);
