@@ -207,3 +207,25 @@ def test_copy_respects_pitches_and_extents(gpu):
     assert np.array_equal(d3.download()[:2, :3, :4], v[:2, :3, :4])
     with pytest.raises(kw.UsageError, match="extent"):
         kw.createCopy(src, dst, kw.IndexVec(6, 9))
+
+
+def test_aliased_x_and_y(gpu, oracle):
+    """AxpyArgs with x == y (y = alpha*y + y) is legal in the reference: each element is read
+    before it is written by the same thread."""
+    n = 100003
+    _, xs, _ = oracle.workload_axpy(n, 13, True)
+    y = vec(gpu, xs, np.float32)
+    run_axpy(n, 1.75, y, y)
+    assert np.array_equal(y.download(), oracle.axpy(np.float32(1.75), xs, xs))
+
+
+def test_queue_shutdown_rejects_enqueue(gpu):
+    """Queue::shutdown (queue.hpp:111-112): outstanding work completes, further enqueues are
+    usage errors."""
+    q = kw.Queue(gpu, kw.QueueFlavor.Async)
+    x = vec(gpu, [1.0, 2.0])
+    q.enqueue(kw.createExec(GPU, kw.axpyWorkDiv(GPU, 2, 32, 1), kw.AxpyKernel(), kw.AxpyArgs(2, 1.0, x, x)))
+    q.shutdown()
+    assert x.download().tolist() == [2.0, 4.0]
+    with pytest.raises(kw.UsageError, match="shutdown"):
+        q.enqueue(kw.createExec(GPU, kw.axpyWorkDiv(GPU, 2, 32, 1), kw.AxpyKernel(), kw.AxpyArgs(2, 1.0, x, x)))
