@@ -364,15 +364,22 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
     uint64_t* empty = full + Cfg::STAGES;
 
+    // Grouped rasterisation: runs of 8 tile-rows sweep the tile-columns together. A CTA walks
+    // tiles blockIdx.x, +gridDim.x, ... (one tile when the grid covers every tile; a persistent
+    // grid keeps the smem ring running across tiles, so the producer fills the next tile's
+    // stages while the consumers run the epilogue). All CTAs at step j work on consecutive tile
+    // ids, which keeps the L2 locality of the rasterisation.
     constexpr int GROUP = 8;
-    const int tile = blockIdx.x;
-    const int per_group = GROUP * p.tiles_n;
-    const int group = tile / per_group;
-    const int first_m = group * GROUP;
-    const int gsize = (p.tiles_m - first_m) < GROUP ? (p.tiles_m - first_m) : GROUP;
-    const int in_group = tile - group * per_group;
-    const int bm = (first_m + in_group % gsize) * Cfg::BM;
-    const int bn = (in_group / gsize) * Cfg::BN;
+    const int ntiles = p.tiles_m * p.tiles_n;
+    auto origin = [&](int tile, int& bm, int& bn) {
+        const int per_group = GROUP * p.tiles_n;
+        const int group = tile / per_group;
+        const int first_m = group * GROUP;
+        const int gsize = (p.tiles_m - first_m) < GROUP ? (p.tiles_m - first_m) : GROUP;
+        const int in_group = tile - group * per_group;
+        bm = (first_m + in_group % gsize) * Cfg::BM;
+        bn = (in_group / gsize) * Cfg::BN;
+    };
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
@@ -393,16 +400,21 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
         if (warp == Cfg::CONSUMERS && lane == 0) {
             tma_prefetch_desc(&tmA);
             tma_prefetch_desc(&tmB);
-            for (int kt = 0; kt < ktiles; ++kt) {
-                const int s = kt % Cfg::STAGES;
-                const uint32_t r = static_cast<uint32_t>(kt / Cfg::STAGES);
-                mbar_wait(&empty[s], (r & 1u) ^ 1u);
-                mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
-                const uint32_t sa = smem_u32(smem + s * Cfg::STAGE_BYTES);
-                tma_load_2d(sa, &tmA, kt * Cfg::BK, bm, &full[s]);
+            int it = 0; // k-tile iteration counter across this CTA's tiles (ring position)
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                int bm, bn;
+                origin(tile, bm, bn);
+                for (int kt = 0; kt < ktiles; ++kt, ++it) {
+                    const int s = it % Cfg::STAGES;
+                    const uint32_t r = static_cast<uint32_t>(it / Cfg::STAGES);
+                    mbar_wait(&empty[s], (r & 1u) ^ 1u);
+                    mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
+                    const uint32_t sa = smem_u32(smem + s * Cfg::STAGE_BYTES);
+                    tma_load_2d(sa, &tmA, kt * Cfg::BK, bm, &full[s]);
 #pragma unroll
-                for (int j = 0; j < Cfg::BN / 16; ++j)
-                    tma_load_2d(sa + Cfg::A_BYTES + j * 2048, &tmB, bn + 16 * j, kt * Cfg::BK, &full[s]);
+                    for (int j = 0; j < Cfg::BN / 16; ++j)
+                        tma_load_2d(sa + Cfg::A_BYTES + j * 2048, &tmB, bn + 16 * j, kt * Cfg::BK, &full[s]);
+                }
             }
         }
         return;
@@ -415,12 +427,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     const int wn = (warp % Cfg::WARPS_N) * Cfg::WN;
     const int g = lane >> 2, t = lane & 3;
 
-    double acc[Cfg::MT][Cfg::NT][2];
-#pragma unroll
-    for (int i = 0; i < Cfg::MT; ++i)
-#pragma unroll
-        for (int j = 0; j < Cfg::NT; ++j)
-            acc[i][j][0] = acc[i][j][1] = 0.0;
 
     // Per-lane parts of the fragment addresses (bytes inside a stage).
     const uint32_t a_row = static_cast<uint32_t>(wm + g) * 128u;
@@ -442,6 +448,18 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
         for (int j = 0; j < Cfg::NT; ++j)
             bf[j] = *reinterpret_cast<const double*>(sb + (j >> 1) * 2048 + (b_even[ks] ^ ((j & 1) ? 64u : 0u)));
     };
+
+    const bool c_vec = (p.ldc % 2 == 0) && (reinterpret_cast<uintptr_t>(p.c) % 16 == 0);
+    int it0 = 0; // ring position of this tile's first k-tile
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it0 += ktiles) {
+    int bm, bn;
+    origin(tile, bm, bn);
+    double acc[Cfg::MT][Cfg::NT][2];
+#pragma unroll
+    for (int i = 0; i < Cfg::MT; ++i)
+#pragma unroll
+        for (int j = 0; j < Cfg::NT; ++j)
+            acc[i][j][0] = acc[i][j][1] = 0.0;
 
     if constexpr (Cfg::PAIRED) {
         // A pair fragments: one double2 per (i, q) = k-steps 2q and 2q+1; B per k-step.
@@ -474,12 +492,13 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
         double2 a2[2][Cfg::MT];
         double bf[2][Cfg::NT];
         if (ktiles > 0) {
-            mbar_wait(&full[0], 0);
-            load_a2(smem, 0, a2[0]);
-            load_b(smem, 0, bf[0]);
+            const int s0 = it0 % Cfg::STAGES;
+            mbar_wait(&full[s0], static_cast<uint32_t>(it0 / Cfg::STAGES) & 1u);
+            load_a2(smem + s0 * Cfg::STAGE_BYTES, 0, a2[0]);
+            load_b(smem + s0 * Cfg::STAGE_BYTES, 0, bf[0]);
         }
         for (int kt = 0; kt < ktiles; ++kt) {
-            const int s = kt % Cfg::STAGES;
+            const int s = (it0 + kt) % Cfg::STAGES;
             const uint8_t* sa = smem + s * Cfg::STAGE_BYTES;
             const uint8_t* sa2 = sa;
 #pragma unroll
@@ -496,8 +515,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
                     if (lane == 0)
                         mbar_arrive(&empty[s]);
                     if (kt + 1 < ktiles) {
-                        const int s2 = (kt + 1) % Cfg::STAGES;
-                        mbar_wait(&full[s2], static_cast<uint32_t>((kt + 1) / Cfg::STAGES) & 1u);
+                        const int s2 = (it0 + kt + 1) % Cfg::STAGES;
+                        mbar_wait(&full[s2], static_cast<uint32_t>((it0 + kt + 1) / Cfg::STAGES) & 1u);
                         sa2 = smem + s2 * Cfg::STAGE_BYTES;
                         load_b(sa2, 0, bf[bn2]);
                         load_a2(sa2, 0, a2[0]); // a2[0] is idle during k-steps 2 and 3
@@ -517,11 +536,12 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     // hides behind 32 DMMAs instead of stalling the warp.
     double af[2][Cfg::MT], bf[2][Cfg::NT];
     if (ktiles > 0) {
-        mbar_wait(&full[0], 0);
-        load_frags(smem, 0, af[0], bf[0]);
+        const int s0 = it0 % Cfg::STAGES;
+        mbar_wait(&full[s0], static_cast<uint32_t>(it0 / Cfg::STAGES) & 1u);
+        load_frags(smem + s0 * Cfg::STAGE_BYTES, 0, af[0], bf[0]);
     }
     for (int kt = 0; kt < ktiles; ++kt) {
-        const int s = kt % Cfg::STAGES;
+        const int s = (it0 + kt) % Cfg::STAGES;
         const uint8_t* sa = smem + s * Cfg::STAGE_BYTES;
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {
@@ -536,8 +556,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
                 if (lane == 0)
                     mbar_arrive(&empty[s]);
                 if (kt + 1 < ktiles) {
-                    const int s2 = (kt + 1) % Cfg::STAGES;
-                    mbar_wait(&full[s2], static_cast<uint32_t>((kt + 1) / Cfg::STAGES) & 1u);
+                    const int s2 = (it0 + kt + 1) % Cfg::STAGES;
+                    mbar_wait(&full[s2], static_cast<uint32_t>((it0 + kt + 1) / Cfg::STAGES) & 1u);
                     load_frags(smem + s2 * Cfg::STAGE_BYTES, 0, af[nxt], bf[nxt]);
                 }
             }
@@ -551,7 +571,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
 
     }
 
-    const bool c_vec = (p.ldc % 2 == 0) && (reinterpret_cast<uintptr_t>(p.c) % 16 == 0);
 #pragma unroll
     for (int i = 0; i < Cfg::MT; ++i) {
         const int row = bm + wm + i * 8 + g;
@@ -576,6 +595,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
             }
         }
     }
+    } // tile loop
 }
 
 using PFN_encodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -618,7 +638,7 @@ bool tma_eligible(const GemmParams& p)
            reinterpret_cast<uintptr_t>(p.b) % 16 == 0 && encode_fn() != nullptr;
 }
 
-template <class Cfg>
+template <class Cfg, bool PERSISTENT = false>
 kw_status launch_tma(cudaStream_t s, const GemmParams& p0);
 
 // Tile configurations (the DGEMM half of the work-division sweep, BASELINE.json configs[4]).
@@ -915,7 +935,18 @@ kw_status tile_from_wd(const kw_workdiv* wd, size_t m, size_t n, int* tile)
     return KW_OK;
 }
 
-template <class Cfg>
+int sm_count()
+{
+    static int sms = [] {
+        int d = 0, v = 148;
+        cudaGetDevice(&d);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
+        return v;
+    }();
+    return sms;
+}
+
+template <class Cfg, bool PERSISTENT>
 kw_status launch_tma(cudaStream_t s, const GemmParams& p0)
 {
     GemmParams p = p0;
@@ -937,7 +968,9 @@ kw_status launch_tma(cudaStream_t s, const GemmParams& p0)
             return kw::cuda_fail("dgemm: cudaFuncSetAttribute", e);
         attr = true;
     }
-    dgemm_tma_kernel<Cfg><<<static_cast<unsigned>(tiles), Cfg::THREADS, Cfg::SMEM, s>>>(ma, mb, p);
+    const long long resident = static_cast<long long>(sm_count()) * Cfg::MIN_BLOCKS;
+    const unsigned grid = static_cast<unsigned>(PERSISTENT && tiles > resident ? resident : tiles);
+    dgemm_tma_kernel<Cfg><<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(ma, mb, p);
     kw::g_launches.fetch_add(1, std::memory_order_relaxed);
     return KW_OK;
 }
@@ -950,7 +983,7 @@ using Tma128s7 = TmaCfg<128, 128, 64, 32, 7>; // 11: 7-stage ring (224 KiB)
 using Tma128x64x2 = TmaCfg<128, 64, 64, 32, 4, 2>; // 12: two CTAs per SM, 4 consumers each
 using Tma64x128x2 = TmaCfg<64, 128, 64, 32, 4, 2>; // 13
 using Tma128p = TmaCfg<128, 128, 64, 32, 6, 1, true>;       // 14: LDS.128 paired A fragments
-using Tma64x128x2p = TmaCfg<64, 128, 64, 32, 4, 2, true>;   // 15
+using Tma64x128x2p = TmaCfg<64, 128, 64, 32, 4, 2, true>;   // 16
 // (16 consumer warps of 32x32 were measured out: 104 registers per consumer spill.)
 
 struct CfgInfo {
@@ -977,6 +1010,7 @@ const CfgInfo kCfgs[] = {
     {Tma64x128x2::BM, Tma64x128x2::BN, Tma64x128x2::BK, Tma64x128x2::THREADS, Tma64x128x2::STAGES,
      launch_tma<Tma64x128x2>},
     {Tma128p::BM, Tma128p::BN, Tma128p::BK, Tma128p::THREADS, Tma128p::STAGES, launch_tma<Tma128p>},
+    {Tma128p::BM, Tma128p::BN, Tma128p::BK, Tma128p::THREADS, Tma128p::STAGES, launch_tma<Tma128p, true>}, // 15: persistent
     {Tma64x128x2p::BM, Tma64x128x2p::BN, Tma64x128x2p::BK, Tma64x128x2p::THREADS, Tma64x128x2p::STAGES,
      launch_tma<Tma64x128x2p>},
 };
