@@ -273,6 +273,35 @@ def run_ours(args, dist: Dist) -> dict:
     e2e_s = dist.max(t1 - t0)
     e2e_value = BYTES_PER_ELEM * N_AXPY * e2e_steps / e2e_s / 1e9
 
+    # ---- fp64 AXPY (the reference's own AxpyKernel dtype), same n, device-resident
+    f64 = None
+    if not args.no_f64:
+        x64 = kw.Buffer(dev, kw.IndexVec(n), 8)
+        y64 = kw.Buffer(dev, kw.IndexVec(n), 8)
+        L.check(lib.kw_memset(q.handle(), x64.data(), 0, n * 8))
+        L.check(lib.kw_memset(q.handle(), y64.data(), 0, n * 8))
+        t64 = kw.createExec(GPU, kw.axpyWorkDiv(GPU, n, args.tpb, max(2, args.ept // 2)), kw.AxpyKernel(),
+                            kw.AxpyArgs(n, 1.5, x64, y64))
+        for _ in range(3):
+            q.enqueue(t64)
+        q.wait()
+        dist.barrier()
+        a64, b64 = C.c_void_p(), C.c_void_p()
+        steps64 = max(10, args.steps // 4)
+        L.check(lib.kw_event_record(q.handle(), C.byref(a64)))
+        for _ in range(steps64):
+            q.enqueue(t64)
+        L.check(lib.kw_event_record(q.handle(), C.byref(b64)))
+        q.wait()
+        ms64 = C.c_float()
+        L.check(lib.kw_event_elapsed_ms(a64, b64, C.byref(ms64)))
+        lib.kw_event_destroy(a64)
+        lib.kw_event_destroy(b64)
+        t = dist.max(ms64.value)
+        f64 = {"value": round(24 * N_AXPY * steps64 / (t / 1e3) / 1e9, 1), "unit": "GB/s", "steps": steps64,
+               "bytes_per_elem": 24, "note": "AXPY fp64 n=2^28 (the reference's AxpyKernel dtype), HBM-resident"}
+        del x64, y64
+
     # ---- secondary: DGEMM
     dg = run_dgemm(args, dist, kw, L, lib, dev, q, sampler)
 
@@ -310,6 +339,7 @@ def run_ours(args, dist: Dist) -> dict:
                      "kernel": "axpy_vec_kernel<float,4>", "bytes_per_launch": BYTES_PER_ELEM * n},
         "gpu_launches": int(launches),
         "clocks": clocks,
+        "axpy_f64": f64,
         "dgemm": dg,
     }
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu:
@@ -528,7 +558,9 @@ def cpu_baseline_dgemm(a, b, c, alpha, beta, Cb, q, task, bw_task=None):
         secs = time.perf_counter() - t
     tf = 2 * rows * size * size / secs / 1e12
     err = np.abs(gpu_rows - out)
-    ok = bool(np.all(err <= (size + 4) * 2.0 ** -53 * np.abs(out)))
+    bound = (size + 4) * 2.0 ** -53 * np.abs(out)
+    ok = bool(np.all(err <= bound))
+    worst = float(np.max(err / bound))
     bitwise = None
     if bw_task is not None:
         Cb.upload(c)
@@ -539,7 +571,8 @@ def cpu_baseline_dgemm(a, b, c, alpha, beta, Cb, q, task, bw_task=None):
           "sample": f"{rows} of {size} rows of the 8192^3 workload (GemmTiledKernel tile 32, BlocksParallel); "
                     f"{secs:.2f} s"}
     return cb, {"check": "|dC| <= (K+4)*2^-53*|C_ref| on the sampled rows (DMMA kernel); bitwise equality "
-                         "on the same rows (bit-exact mode)", "match": ok, "bitwise_mode_match": bitwise}
+                         "on the same rows (bit-exact mode)", "match": ok, "max_err_over_bound": round(worst, 4),
+                "bitwise_mode_match": bitwise}
 
 
 def run_reference(args, dist: Dist) -> dict | None:
@@ -578,6 +611,7 @@ def main():
     ap.add_argument("--ref-steps", type=int, default=10)
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-dgemm", action="store_true")
+    ap.add_argument("--no-f64", action="store_true")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl")
     ap.add_argument("--same-gpu", action="store_true", help="self-test: all ranks on GPU 0 (gloo only)")
     ap.add_argument("--force-rowsharded", action="store_true",
