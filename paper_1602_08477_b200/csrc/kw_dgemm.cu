@@ -983,7 +983,8 @@ using Tma128s7 = TmaCfg<128, 128, 64, 32, 7>; // 11: 7-stage ring (224 KiB)
 using Tma128x64x2 = TmaCfg<128, 64, 64, 32, 4, 2>; // 12: two CTAs per SM, 4 consumers each
 using Tma64x128x2 = TmaCfg<64, 128, 64, 32, 4, 2>; // 13
 using Tma128p = TmaCfg<128, 128, 64, 32, 6, 1, true>;       // 14: LDS.128 paired A fragments
-using Tma64x128x2p = TmaCfg<64, 128, 64, 32, 4, 2, true>;   // 16
+using Tma64x128x2p = TmaCfg<64, 128, 64, 32, 4, 2, true>;   // 16: paired, two CTAs per SM
+using Tma64x64x3p = TmaCfg<64, 64, 32, 32, 4, 3, true>;     // 17: paired, three CTAs per SM
 // (16 consumer warps of 32x32 were measured out: 104 registers per consumer spill.)
 
 struct CfgInfo {
@@ -1013,15 +1014,34 @@ const CfgInfo kCfgs[] = {
     {Tma128p::BM, Tma128p::BN, Tma128p::BK, Tma128p::THREADS, Tma128p::STAGES, launch_tma<Tma128p, true>}, // 15: persistent
     {Tma64x128x2p::BM, Tma64x128x2p::BN, Tma64x128x2p::BK, Tma64x128x2p::THREADS, Tma64x128x2p::STAGES,
      launch_tma<Tma64x128x2p>},
+    {Tma64x64x3p::BM, Tma64x64x3p::BN, Tma64x64x3p::BK, Tma64x64x3p::THREADS, Tma64x64x3p::STAGES,
+     launch_tma<Tma64x64x3p>},
 };
 constexpr int kNumCfgs = sizeof(kCfgs) / sizeof(kCfgs[0]);
-int g_default_cfg128 = 14; // tile 128 -> TMA warp-specialised kernel, paired LDS.128 A fragments (tools/dgemm_ab.py)
-int g_default_cfg64 = 4;  // tile 64  -> this config
+// Tile choice for the GPU back-end. The tile work division (gemmTiledWorkDiv) is the coverage
+// contract; the kernel picks its CTA tile among the paired-k-map TMA configurations, which feed
+// every output element the identical DMMA sequence (test_paired_configs_are_bitwise_
+// interchangeable) — so the choice never changes a bit, and row panels, column panels and row
+// shards of one product still reproduce the single launch exactly.
+//   16: 64x128 tile, 2 CTAs/SM (best from ~1536 up: 35.4 TFLOP/s at 8192^3, 34.7 at 4096^3)
+//   17: 64x64 tile, 3 CTAs/SM  (best for small outputs: 26.4 at 1024^3, 33.0 at 2048^3)
+// Model: the busiest SM's output count, ceil(tiles / SMs) * tile area; take 17 when that is >3%
+// lower, or when 16 would not give every SM a tile (1 CTA per SM under-feeds the DMMA pipe).
+constexpr int kCfgWide = 16, kCfgSmall = 17;
+
+int pick_config(const GemmParams& p)
+{
+    const long long sms = sm_count();
+    const long long rows = (p.m + 63) / 64;
+    const long long t16 = rows * ((p.n + 127) / 128), t17 = rows * ((p.n + 63) / 64);
+    const long long load16 = (t16 + sms - 1) / sms * 8192, load17 = (t17 + sms - 1) / sms * 4096;
+    const bool small = t16 <= sms || static_cast<double>(load17) < 0.97 * static_cast<double>(load16);
+    return small ? kCfgSmall : kCfgWide;
+}
 
 kw_status launch_tiled(cudaStream_t s, int tile, const GemmParams& p)
 {
-    const int cfg = tile == 64 ? g_default_cfg64 : g_default_cfg128;
-    return kCfgs[cfg].launch(s, p);
+    return kCfgs[tile == 64 ? kCfgSmall : pick_config(p)].launch(s, p);
 }
 
 GemmParams make_params(size_t m, size_t n, size_t k, double alpha, const double* A, size_t lda, const double* B,

@@ -281,3 +281,26 @@ def test_tiled_bitwise_4096(gpu, oracle):
     n = 4096
     alpha, beta, a, b, c = oracle.workload_gemm(n, 42)
     assert np.array_equal(tiled_bitwise(gpu, alpha, beta, a, b, c), oracle.gemm(alpha, beta, a, b, c))
+
+
+def test_paired_configs_are_bitwise_interchangeable(gpu, oracle):
+    """Every TMA configuration with the paired k-slot map (14..17) feeds each output element the
+    same DMMA sequence, so tile shape / CTAs per SM / persistence change no bit — which is what
+    lets the library pick the tile by problem size without breaking the panel and row-shard
+    invariance."""
+    lib = L.lib()
+    paired = [c for c in range(lib.kw_dgemm_config_count()) if c >= 14]
+    rng = np.random.default_rng(31)
+    q = kw.Queue(gpu, kw.QueueFlavor.Async)
+    for (m, n, k) in ((300, 260, 170), (1024, 1024, 1024), (129, 640, 48)):
+        a, b, c = rng.random((m, k)) * 10, rng.random((k, n)) * 10, rng.random((m, n)) * 10
+        outs = []
+        for cfg in paired:
+            A, B, Cb = mat(gpu, a), mat(gpu, b), mat(gpu, c)
+            assert lib.kw_dgemm_with_config(q.handle(), cfg, m, n, k, 0.9, A.data(), A.leadingDim(), B.data(),
+                                            B.leadingDim(), 1.1, Cb.data(), Cb.leadingDim()) == 0
+            q.wait()
+            outs.append(Cb.download())
+        for o in outs[1:]:
+            assert np.array_equal(o, outs[0]), (m, n, k)
+        assert within_tol(outs[0], oracle.gemm(0.9, 1.1, a, b, c), k)[0]

@@ -16,7 +16,7 @@ from paper_1602_08477_b200 import kernelweave as kw  # noqa: E402
 
 def main():
     n = int(sys.argv[1])
-    cfgs = [int(c) for c in sys.argv[2].split(",")]
+    cfgs = [int(c) for c in sys.argv[2].split(",")]  # -1 = kw_dgemm's own tile choice
     rounds = int(sys.argv[3]) if len(sys.argv) > 3 else 5
     lib = L.lib()
     dev = kw.Device.gpu(0)
@@ -29,8 +29,13 @@ def main():
     res = {c: [] for c in cfgs}
     for _ in range(rounds):
         for cfg in cfgs:
-            go = lambda: L.check(lib.kw_dgemm_with_config(q.handle(), cfg, n, n, n, 1.0, A.data(), A.leadingDim(),  # noqa: E731
-                                                          B.data(), B.leadingDim(), 1.0, Cb.data(), Cb.leadingDim()))
+            if cfg < 0:  # the library's own choice (kw_dgemm, default division)
+                go = lambda: L.check(lib.kw_dgemm(q.handle(), None, n, n, n, 1.0, A.data(), A.leadingDim(),  # noqa: E731
+                                                  B.data(), B.leadingDim(), 1.0, Cb.data(), Cb.leadingDim()))
+            else:
+                go = lambda: L.check(lib.kw_dgemm_with_config(q.handle(), cfg, n, n, n, 1.0, A.data(),  # noqa: E731
+                                                              A.leadingDim(), B.data(), B.leadingDim(), 1.0,
+                                                              Cb.data(), Cb.leadingDim()))
             go()
             q.wait()
             e0, e1 = C.c_void_p(), C.c_void_p()
