@@ -433,6 +433,8 @@ def run_dgemm(args, dist, kw, L, lib, dev, q, sampler) -> dict:
                 entry["cpu_baseline"], entry["parity"] = cpu_baseline_dgemm(a, b, c, 1.25, 0.75, Cb, q, task, bw_task)
             res[f"n{size}"] = entry
             del A, B, Cb, hA, hB, hC
+        if not args.no_cublas:
+            res["cublas_same_box"] = cublas_dgemm(dist.local, (8192, 4096))
         res["value"] = res["n8192"]["value"]
         res["config"] = "DGEMM fp64 M=N=K=8192 (north-star headline) and 4096 (BASELINE configs[2]), 1 GPU"
         return res
@@ -475,6 +477,32 @@ def run_dgemm(args, dist, kw, L, lib, dev, q, sampler) -> dict:
                              "peak": round(FP64_NOMINAL_TFLOPS, 2), "unit": "TFLOP/s per GPU",
                              "frac": round(tflops / dist.world / FP64_NOMINAL_TFLOPS, 4)}})
     return res
+
+
+def cublas_dgemm(device: int, sizes) -> dict:
+    """cuBLAS DGEMM (torch.matmul fp64) on the same box, for context only — not on our path."""
+    try:
+        import torch
+        out = {}
+        for n in sizes:
+            a = torch.rand(n, n, dtype=torch.float64, device=f"cuda:{device}")
+            b = torch.rand(n, n, dtype=torch.float64, device=f"cuda:{device}")
+            for _ in range(2):
+                a @ b
+            torch.cuda.synchronize()
+            reps = max(3, int(2e12 / (2 * n ** 3)))
+            e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+            e0.record()
+            for _ in range(reps):
+                a @ b
+            e1.record()
+            torch.cuda.synchronize()
+            out[f"n{n}"] = round(2 * n ** 3 * reps / (e0.elapsed_time(e1) / 1e3) / 1e12, 3)
+            del a, b
+        out["unit"] = "TFLOP/s"
+        return out
+    except Exception as ex:  # noqa: BLE001
+        return {"error": str(ex)[:200]}
 
 
 # --------------------------------------------------------------------------------------------
@@ -588,13 +616,30 @@ def run_reference(args, dist: Dist) -> dict | None:
     cb = {"value": round(value, 2), "unit": "GB/s", "cores": cpu_threads(), "kind": kind,
           "sample": f"full workload n=2^28 fp32, median of {steps} reps (reference BlocksParallel engine, "
                     f"AxpyKernel functor for float, ept=4096)"}
+    dg = None
+    try:
+        from oracle import oracle as O
+        if O.ref_available():
+            size, rows = 8192, 64
+            g = np.random.default_rng(77)
+            a = g.random((rows, size)) * 10
+            b = g.random((size, size)) * 10
+            c = g.random((rows, size)) * 10
+            gsec = C.c_double()
+            assert O.ref().kwref_gemm_kernel(1, 1, rows, size, size, 1.25, 0.75, a.ctypes.data, size, b.ctypes.data,
+                                             size, c.ctypes.data, size, 32, 16, 8, C.byref(gsec)) == 0
+            dg = {"metric": "DGEMM fp64 TFLOP/s (2*M*N*K)", "value": round(2 * rows * size * size / gsec.value / 1e12, 5),
+                  "unit": "TFLOP/s", "sample": f"{rows} rows of 8192^3, GemmTiledKernel tile 32, BlocksParallel, "
+                                               f"{cpu_threads()} threads"}
+    except Exception as ex:  # noqa: BLE001
+        dg = {"error": str(ex)[:200]}
     return {"impl": "reference", "metric": "AXPY fp32 HBM GB/s (n=2^28, Y=alpha*X+Y, 12 B/elem)",
             "value": round(value, 2), "unit": "GB/s", "n_gpus": dist.world, "steps": steps,
             "warmup": args.warmup, "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": "AXPY fp32 n=2^28 index-sharded (BASELINE.json configs[1])", "n": N_AXPY},
             "cpu_baseline": cb, "e2e": {"value": round(value, 2), "unit": "GB/s", "h2d_bytes_per_step": 0,
-                                        "d2h_bytes_per_step": 0}}
+                                        "d2h_bytes_per_step": 0}, "dgemm": dg}
 
 
 def main():
@@ -612,6 +657,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-dgemm", action="store_true")
     ap.add_argument("--no-f64", action="store_true")
+    ap.add_argument("--no-cublas", action="store_true")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl")
     ap.add_argument("--same-gpu", action="store_true", help="self-test: all ranks on GPU 0 (gloo only)")
     ap.add_argument("--force-rowsharded", action="store_true",
