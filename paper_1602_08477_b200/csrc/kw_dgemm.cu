@@ -25,7 +25,9 @@
 
 #include <cuda.h>
 
+#include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <mutex>
 
 namespace {
@@ -1076,30 +1078,13 @@ kw_status dgemm_staged(kw::Queue* q, int tile, size_t m, size_t n, size_t k, dou
 {
     const size_t ldbs = round2(n), ldas = round2(k == 0 ? 1 : k), ldcs = round2(n);
     const size_t row_bytes = (ldas + ldcs) * sizeof(double);
-    // Panel height: whole 128-row tiles, chosen for wave efficiency (tiles per panel close to a
-    // multiple of the SM count) — a panel of 384 rows at n = 8192 fills 1.3 waves and wastes a
-    // third of the GPU. Among heights with >= 95% efficiency take the smallest (shortest
-    // pipeline fill); cap the slot at 1 GiB.
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, q->device);
-    const size_t tiles_n = kw::ceil_div(n, 128);
-    size_t R = 0;
-    double best = -1.0;
-    size_t best_R = 128;
-    for (size_t tm = 1; tm * 128 <= kw::ceil_div(m, 128) * 128 && tm * 128 * row_bytes <= (1ull << 30); ++tm) {
-        const size_t T = tm * tiles_n;
-        const double eff = static_cast<double>(T) / (kw::ceil_div(T, static_cast<size_t>(sms)) * sms);
-        if (eff >= 0.95 && T >= static_cast<size_t>(2 * sms)) {
-            R = tm * 128;
-            break;
-        }
-        if (eff > best) {
-            best = eff;
-            best_R = tm * 128;
-        }
-    }
-    if (R == 0)
-        R = best_R;
+    // Panel height: about m/16 in whole 64-row tiles (the launcher sizes its CTA tile to the
+    // panel, so small panels still fill the GPU), capped at 1 GiB per slot. Sixteen panels keep
+    // the pipeline fill (first upload) and drain (last compute + download) short; measured best
+    // or tied at 4096 and 8192 among 256..4096-row panels (profiles/e2e_dgemm_panel_sweep_r01.txt).
+    size_t R = kw::ceil_div(kw::ceil_div(m, static_cast<size_t>(16)), 64) * 64;
+    const size_t cap = std::max<size_t>(64, ((1ull << 30) / row_bytes) / 64 * 64);
+    R = std::min(std::max<size_t>(R, 64), cap);
     if (R > m)
         R = m;
     const int ring = 3;

@@ -1,6 +1,5 @@
-"""e2e DGEMM (host pinned A, B, C through the public API) at n: streamed full-copy schedule vs
-the panel ring (KW_DGEMM_FORCE_RING=1), median of 3 wall-clock steps."""
-import os
+"""e2e DGEMM (host pinned A, B, C through the public API) at n = 4096 and 8192, median of 3
+wall-clock steps."""
 import statistics
 import sys
 import time
@@ -10,11 +9,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_1602_08477_b200 import kernelweave as kw  # noqa: E402
 
 
-def run(n, ring):
-    if ring:
-        os.environ["KW_DGEMM_FORCE_RING"] = "1"
-    else:
-        os.environ.pop("KW_DGEMM_FORCE_RING", None)
+def run(n):
     GPU = kw.BackendKind.GpuCudaRt
     q = kw.Queue(kw.Device.gpu(0), kw.QueueFlavor.Async)
     host = kw.Device.host()
@@ -32,10 +27,9 @@ def run(n, ring):
         q.wait()
         ts.append(time.perf_counter() - t)
     med = statistics.median(ts)
-    print(f"n={n} ring={ring} {med*1e3:.1f} ms {2*n**3/med/1e12:.2f} TFLOP/s")
+    print(f"n={n} {med*1e3:.1f} ms {2*n**3/med/1e12:.2f} TFLOP/s")
 
 
 if __name__ == "__main__":
     for n in (4096, 8192):
-        run(n, False)
-        run(n, True)
+        run(n)
