@@ -341,6 +341,7 @@ template <typename T>
 kw_status axpy_entry(kw_queue qh, const kw_workdiv* wd, size_t n, T alpha, const T* x, T* y)
 {
     KW_CHECK_QUEUE(qh);
+    KW_ENQUEUE_LOCK(qh);
     auto* q = reinterpret_cast<kw::Queue*>(qh);
     kw_workdiv def;
     if (wd == nullptr) {

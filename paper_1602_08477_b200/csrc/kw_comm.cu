@@ -178,6 +178,7 @@ kw_status kw_comm_destroy(kw_comm c)
 kw_status kw_comm_broadcast(kw_comm c, kw_queue qh, void* buf, size_t bytes, int root)
 {
     KW_CHECK_QUEUE(qh);
+    KW_ENQUEUE_LOCK(qh);
     if (!c)
         return kw::usage("kw_comm_broadcast: null communicator");
     if (root < 0 || root >= c->world)
@@ -195,6 +196,7 @@ kw_status kw_dgemm_rowsharded(kw_comm c, kw_queue qh, size_t m_local, size_t n, 
                               size_t ldc, double* b_panels, int panels, int root)
 {
     KW_CHECK_QUEUE(qh);
+    KW_ENQUEUE_LOCK(qh);
     if (!c)
         return kw::usage("dgemm_rowsharded: null communicator");
     auto* q = reinterpret_cast<kw::Queue*>(qh);

@@ -27,7 +27,8 @@ struct Queue {
     cudaStream_t stream = nullptr; // in-order FIFO of the queue
     cudaStream_t aux = nullptr;    // D2H stream of the host-staged paths
     cudaStream_t h2d = nullptr;    // H2D stream of the host-staged paths
-    std::mutex mu;
+    std::mutex mu;       // failure bookkeeping
+    std::mutex enqueue;  // serialises enqueues from several host threads (queue.hpp:89-93)
     size_t failed = 0;
     std::string first_failure;
     bool shut = false;
@@ -92,3 +93,8 @@ inline size_t ceil_div(size_t a, size_t b) { return (a + b - 1) / b; }
         if (reinterpret_cast<kw::Queue*>(q)->shut)                                                 \
             return kw::usage("queue: enqueue after shutdown");                                     \
     } while (0)
+
+// Enqueue entry points hold the queue's enqueue lock for their whole body: arrival order at the
+// lock is the FIFO order, and the host-staging scratch/events of one queue are never shared by
+// two in-flight enqueues.
+#define KW_ENQUEUE_LOCK(q) std::lock_guard<std::mutex> kw_enqueue_guard_(reinterpret_cast<kw::Queue*>(q)->enqueue)

@@ -1248,6 +1248,7 @@ kw_status kw_dgemm(kw_queue qh, const kw_workdiv* wd, size_t m, size_t n, size_t
                    size_t lda, const double* B, size_t ldb, double beta, double* C, size_t ldc)
 {
     KW_CHECK_QUEUE(qh);
+    KW_ENQUEUE_LOCK(qh);
     auto* q = reinterpret_cast<kw::Queue*>(qh);
     kw_status st = validate_gemm(m, n, k, A, lda, B, ldb, C, ldc);
     if (st != KW_OK)
@@ -1280,6 +1281,7 @@ kw_status kw_dgemm_bitwise(kw_queue qh, const kw_workdiv* wd, size_t m, size_t n
                            const double* A, size_t lda, const double* B, size_t ldb, double beta, double* C, size_t ldc)
 {
     KW_CHECK_QUEUE(qh);
+    KW_ENQUEUE_LOCK(qh);
     auto* q = reinterpret_cast<kw::Queue*>(qh);
     kw_status st = validate_gemm(m, n, k, A, lda, B, ldb, C, ldc);
     if (st != KW_OK)
@@ -1325,6 +1327,7 @@ kw_status kw_dgemm_with_config(kw_queue qh, int cfg, size_t m, size_t n, size_t 
                                size_t lda, const double* B, size_t ldb, double beta, double* C, size_t ldc)
 {
     KW_CHECK_QUEUE(qh);
+    KW_ENQUEUE_LOCK(qh);
     auto* q = reinterpret_cast<kw::Queue*>(qh);
     if (cfg < 0 || cfg >= kNumCfgs)
         return kw::usage("dgemm config index out of range");
@@ -1346,6 +1349,7 @@ kw_status kw_dgemm_naive(kw_queue qh, const kw_workdiv* wd, size_t m, size_t n, 
                          const double* A, size_t lda, const double* B, size_t ldb, double beta, double* C, size_t ldc)
 {
     KW_CHECK_QUEUE(qh);
+    KW_ENQUEUE_LOCK(qh);
     auto* q = reinterpret_cast<kw::Queue*>(qh);
     kw_status st = validate_gemm(m, n, k, A, lda, B, ldb, C, ldc);
     if (st != KW_OK)

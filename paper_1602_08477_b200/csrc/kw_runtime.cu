@@ -241,6 +241,7 @@ kw_status kw_pointer_kind(const void* ptr, int* kind, int* device)
 kw_status kw_memset(kw_queue qh, void* ptr, int value, size_t bytes)
 {
     KW_CHECK_QUEUE(qh);
+    KW_ENQUEUE_LOCK(qh);
     auto* q = reinterpret_cast<Queue*>(qh);
     kw::DeviceGuard g(q->device);
     cudaError_t e = cudaMemsetAsync(ptr, value, bytes, q->stream);
@@ -405,6 +406,7 @@ kw_status kw_queue_complete_launch(kw_queue qh, int cuda_error, const char* what
 kw_status kw_event_record(kw_queue qh, kw_event* out)
 {
     KW_CHECK_QUEUE(qh);
+    KW_ENQUEUE_LOCK(qh);
     if (!out)
         return kw::usage("kw_event_record: null output");
     auto* q = reinterpret_cast<Queue*>(qh);
@@ -466,6 +468,7 @@ kw_status kw_copy(kw_queue qh, void* dst, size_t dst_pitch, const size_t dst_ext
                   size_t elem_size)
 {
     KW_CHECK_QUEUE(qh);
+    KW_ENQUEUE_LOCK(qh);
     auto* q = reinterpret_cast<Queue*>(qh);
     if (dim < 1 || dim > 3)
         return kw::usage("copy: buffer and extent dimensionalities must match");
@@ -567,6 +570,7 @@ uint64_t kw_launch_count(void) { return kw::g_launches.load(); }
 kw_status kw_l2_flush(kw_queue qh)
 {
     KW_CHECK_QUEUE(qh);
+    KW_ENQUEUE_LOCK(qh);
     auto* q = reinterpret_cast<Queue*>(qh);
     static void* flush_buf[64] = {}; // per device: 2 x L2 bytes, written once per call
     static size_t flush_bytes[64] = {};

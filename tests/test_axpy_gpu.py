@@ -229,3 +229,49 @@ def test_queue_shutdown_rejects_enqueue(gpu):
     assert x.download().tolist() == [2.0, 4.0]
     with pytest.raises(kw.UsageError, match="shutdown"):
         q.enqueue(kw.createExec(GPU, kw.axpyWorkDiv(GPU, 2, 32, 1), kw.AxpyKernel(), kw.AxpyArgs(2, 1.0, x, x)))
+
+
+def test_concurrent_enqueues_on_one_queue(gpu, oracle):
+    """Queue::enqueue is thread-safe (queue.hpp:89-93): four host threads push host-staged AXPYs
+    (which share the queue's staging scratch) onto one queue; every result is exact."""
+    import threading
+    q = kw.Queue(gpu, kw.QueueFlavor.Async)
+    n = (1 << 22) + 7
+    jobs = []
+    for t in range(4):
+        alpha, xs, ys = oracle.workload_axpy(n, 100 + t, True)
+        jobs.append((alpha, xs, ys.copy(), oracle.axpy(alpha, xs, ys)))
+    errs = []
+
+    def worker(job):
+        alpha, xs, ys, _ = job
+        for _ in range(3):
+            st = L.lib().kw_axpy_f32(q.handle(), None, n, float(alpha), xs.ctypes.data, ys.ctypes.data)
+            if st != 0:
+                errs.append(L.last_error())
+        # three applications: compare against three oracle applications below
+
+    threads = [threading.Thread(target=worker, args=(j,)) for j in jobs]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    q.wait()
+    assert not errs
+    for alpha, xs, ys, once in jobs:
+        want = oracle.axpy(alpha, xs, oracle.axpy(alpha, xs, once))
+        assert np.array_equal(ys, want)
+
+
+def test_mixed_host_and_device_operands(gpu, oracle):
+    n = (1 << 21) + 3
+    alpha, xs, ys = oracle.workload_axpy(n, 21, True)
+    want = oracle.axpy(alpha, xs, ys)
+    q = kw.Queue(gpu, kw.QueueFlavor.Sync)
+    xd = vec(gpu, xs, np.float32)
+    yh = ys.copy()
+    assert L.lib().kw_axpy_f32(q.handle(), None, n, float(alpha), xd.data(), yh.ctypes.data) == 0
+    assert np.array_equal(yh, want)
+    yd = vec(gpu, ys, np.float32)
+    assert L.lib().kw_axpy_f32(q.handle(), None, n, float(alpha), xs.ctypes.data, yd.data()) == 0
+    assert np.array_equal(yd.download(), want)

@@ -304,3 +304,23 @@ def test_paired_configs_are_bitwise_interchangeable(gpu, oracle):
         for o in outs[1:]:
             assert np.array_equal(o, outs[0]), (m, n, k)
         assert within_tol(outs[0], oracle.gemm(0.9, 1.1, a, b, c), k)[0]
+
+
+def test_mixed_residency_dgemm(gpu, oracle):
+    """B on the device, A and C on the host (and the other way round): the staged path uploads
+    only what is not resident; bits equal the all-device launch."""
+    rng = np.random.default_rng(12)
+    m, n, k = 700, 520, 300
+    a, b, c = rng.random((m, k)) * 10, rng.random((k, n)) * 10, rng.random((m, n)) * 10
+    want = tiled(gpu, 1.2, 0.4, a, b, c)
+    q = kw.Queue(gpu, kw.QueueFlavor.Sync)
+    B = mat(gpu, b)
+    ah, ch = a.copy(), c.copy()
+    assert L.lib().kw_dgemm(q.handle(), None, m, n, k, 1.2, ah.ctypes.data, k, B.data(), B.leadingDim(), 0.4,
+                            ch.ctypes.data, n) == 0
+    assert np.array_equal(ch, want)
+    A, Cd = mat(gpu, a), mat(gpu, c)
+    bh = b.copy()
+    assert L.lib().kw_dgemm(q.handle(), None, m, n, k, 1.2, A.data(), A.leadingDim(), bh.ctypes.data, n, 0.4,
+                            Cd.data(), Cd.leadingDim()) == 0
+    assert np.array_equal(Cd.download(), want)
