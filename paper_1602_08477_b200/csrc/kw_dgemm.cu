@@ -717,21 +717,26 @@ __global__ void dgemm_naive_kernel(GemmParams p, int er, int ec)
 //   i, j < 8 (64 independent accumulation chains); A staged row-major with a 144-byte row
 //   pitch (two rows read by one warp land in different banks), B row-major; 3-stage cp.async.
 // ------------------------------------------------------------------------------------------
-namespace bw {
-constexpr int BM = 128, BN = 128, BK = 16, THREADS = 256, STAGES = 3;
-constexpr int A_LD = BK + 2; // doubles; 144-byte rows
-constexpr int A_STAGE = BM * A_LD, B_STAGE = BK * BN;
-constexpr size_t SMEM = static_cast<size_t>(STAGES) * (A_STAGE + B_STAGE) * sizeof(double);
-} // namespace bw
+// Thread (ty, tx) of 16 x 16 owns C[ty + 16i][tx + 16j], i < 8, j < NJ; block tile 128 x 16*NJ.
+template <int NJ_, int MIN_BLOCKS_>
+struct BwCfg {
+    static constexpr int NJ = NJ_, MIN_BLOCKS = MIN_BLOCKS_;
+    static constexpr int BM = 128, BN = 16 * NJ, BK = 16, THREADS = 256, STAGES = 3;
+    static constexpr int A_LD = BK + 2; // doubles; 144-byte rows
+    static constexpr int A_STAGE = BM * A_LD, B_STAGE = BK * BN;
+    static constexpr size_t SMEM = static_cast<size_t>(STAGES) * (A_STAGE + B_STAGE) * sizeof(double);
+};
+using Bw128 = BwCfg<8, 1>; // 64 chains per thread, one CTA per SM (a 128 x 64 tile at two CTAs per SM
+                           // measured 1.3 % slower: the kernel is FP64-pipe bound, not latency bound)
 
-template <bool VEC16>
+template <class Cfg, bool VEC16>
 __device__ __forceinline__ void bw_load_stage(const GemmParams& p, double* sA, double* sB, int bm, int bn, int k0,
                                               int tid)
 {
 #pragma unroll
-    for (int it = 0; it < (bw::BM * bw::BK / 2) / bw::THREADS; ++it) {
-        const int c = tid + it * bw::THREADS;
-        const int row = c / (bw::BK / 2), kc = c % (bw::BK / 2);
+    for (int it = 0; it < (Cfg::BM * Cfg::BK / 2) / Cfg::THREADS; ++it) {
+        const int c = tid + it * Cfg::THREADS;
+        const int row = c / (Cfg::BK / 2), kc = c % (Cfg::BK / 2);
         const int gm = bm + row, gk = k0 + kc * 2;
         int valid = 0;
         if (gm < p.m) {
@@ -739,7 +744,7 @@ __device__ __forceinline__ void bw_load_stage(const GemmParams& p, double* sA, d
             valid = valid < 0 ? 0 : (valid > 2 ? 2 : valid);
         }
         const double* src = valid > 0 ? p.a + gm * p.lda + gk : p.a;
-        const uint32_t dst = smem_u32(sA + row * bw::A_LD + kc * 2);
+        const uint32_t dst = smem_u32(sA + row * Cfg::A_LD + kc * 2);
         if (VEC16) {
             cp_async16(dst, src, valid * 8);
         }
@@ -749,9 +754,9 @@ __device__ __forceinline__ void bw_load_stage(const GemmParams& p, double* sA, d
         }
     }
 #pragma unroll
-    for (int it = 0; it < (bw::BK * bw::BN / 2) / bw::THREADS; ++it) {
-        const int c = tid + it * bw::THREADS;
-        const int row = c / (bw::BN / 2), nc = c % (bw::BN / 2);
+    for (int it = 0; it < (Cfg::BK * Cfg::BN / 2) / Cfg::THREADS; ++it) {
+        const int c = tid + it * Cfg::THREADS;
+        const int row = c / (Cfg::BN / 2), nc = c % (Cfg::BN / 2);
         const int gk = k0 + row, gn = bn + nc * 2;
         int valid = 0;
         if (gk < p.k) {
@@ -759,7 +764,7 @@ __device__ __forceinline__ void bw_load_stage(const GemmParams& p, double* sA, d
             valid = valid < 0 ? 0 : (valid > 2 ? 2 : valid);
         }
         const double* src = valid > 0 ? p.b + gk * p.ldb + gn : p.b;
-        const uint32_t dst = smem_u32(sB + row * bw::BN + nc * 2);
+        const uint32_t dst = smem_u32(sB + row * Cfg::BN + nc * 2);
         if (VEC16) {
             cp_async16(dst, src, valid * 8);
         }
@@ -770,12 +775,29 @@ __device__ __forceinline__ void bw_load_stage(const GemmParams& p, double* sA, d
     }
 }
 
-template <bool VEC16>
-__global__ void __launch_bounds__(bw::THREADS, 1) dgemm_bitwise_kernel(GemmParams p)
+template <class Cfg>
+__device__ __forceinline__ void bw_kstep(double (&acc)[8][Cfg::NJ], const double* a_s, const double* b_s, int kk)
+{
+    double a[8], b[Cfg::NJ];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+        a[i] = a_s[i * 16 * Cfg::A_LD + kk];
+#pragma unroll
+    for (int j = 0; j < Cfg::NJ; ++j)
+        b[j] = b_s[kk * Cfg::BN + j * 16];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < Cfg::NJ; ++j)
+            acc[i][j] = __dadd_rn(acc[i][j], __dmul_rn(a[i], b[j])); // never contracted to DFMA
+}
+
+template <class Cfg, bool VEC16>
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS) dgemm_bitwise_kernel(GemmParams p)
 {
     extern __shared__ __align__(128) double smem[];
     double* sA = smem;
-    double* sB = smem + bw::STAGES * bw::A_STAGE;
+    double* sB = smem + Cfg::STAGES * Cfg::A_STAGE;
     constexpr int GROUP = 8;
     const int tile = blockIdx.x;
     const int per_group = GROUP * p.tiles_n;
@@ -783,71 +805,47 @@ __global__ void __launch_bounds__(bw::THREADS, 1) dgemm_bitwise_kernel(GemmParam
     const int first_m = group * GROUP;
     const int gsize = (p.tiles_m - first_m) < GROUP ? (p.tiles_m - first_m) : GROUP;
     const int in_group = tile - group * per_group;
-    const int bm = (first_m + in_group % gsize) * bw::BM;
-    const int bn = (in_group / gsize) * bw::BN;
+    const int bm = (first_m + in_group % gsize) * Cfg::BM;
+    const int bn = (in_group / gsize) * Cfg::BN;
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
 
-    double acc[8][8];
+    double acc[8][Cfg::NJ];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
+        for (int j = 0; j < Cfg::NJ; ++j)
             acc[i][j] = 0.0;
 
-    const int ktiles = (p.k + bw::BK - 1) / bw::BK;
+    const int ktiles = (p.k + Cfg::BK - 1) / Cfg::BK;
 #pragma unroll
-    for (int s = 0; s < bw::STAGES - 1; ++s) {
+    for (int s = 0; s < Cfg::STAGES - 1; ++s) {
         if (s < ktiles)
-            bw_load_stage<VEC16>(p, sA + s * bw::A_STAGE, sB + s * bw::B_STAGE, bm, bn, s * bw::BK, tid);
+            bw_load_stage<Cfg, VEC16>(p, sA + s * Cfg::A_STAGE, sB + s * Cfg::B_STAGE, bm, bn, s * Cfg::BK, tid);
         cp_async_commit();
     }
     for (int kt = 0; kt < ktiles; ++kt) {
-        cp_async_wait<bw::STAGES - 2>();
+        cp_async_wait<Cfg::STAGES - 2>();
         __syncthreads();
         {
-            const int nk = kt + bw::STAGES - 1;
+            const int nk = kt + Cfg::STAGES - 1;
             if (nk < ktiles) {
-                const int s = nk % bw::STAGES;
-                bw_load_stage<VEC16>(p, sA + s * bw::A_STAGE, sB + s * bw::B_STAGE, bm, bn, nk * bw::BK, tid);
+                const int s = nk % Cfg::STAGES;
+                bw_load_stage<Cfg, VEC16>(p, sA + s * Cfg::A_STAGE, sB + s * Cfg::B_STAGE, bm, bn, nk * Cfg::BK, tid);
             }
             cp_async_commit();
         }
-        const int s = kt % bw::STAGES;
-        const double* a_s = sA + s * bw::A_STAGE + ty * bw::A_LD;
-        const double* b_s = sB + s * bw::B_STAGE + tx;
-        const int kend = (p.k - kt * bw::BK) < bw::BK ? (p.k - kt * bw::BK) : bw::BK; // no padded terms
-        if (kend == bw::BK) {
+        const int s = kt % Cfg::STAGES;
+        const double* a_s = sA + s * Cfg::A_STAGE + ty * Cfg::A_LD;
+        const double* b_s = sB + s * Cfg::B_STAGE + tx;
+        const int kend = (p.k - kt * Cfg::BK) < Cfg::BK ? (p.k - kt * Cfg::BK) : Cfg::BK; // no padded terms
+        if (kend == Cfg::BK) {
 #pragma unroll
-            for (int kk = 0; kk < bw::BK; ++kk) {
-                double a[8], b[8];
-#pragma unroll
-                for (int i = 0; i < 8; ++i)
-                    a[i] = a_s[i * 16 * bw::A_LD + kk];
-#pragma unroll
-                for (int j = 0; j < 8; ++j)
-                    b[j] = b_s[kk * bw::BN + j * 16];
-#pragma unroll
-                for (int i = 0; i < 8; ++i)
-#pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                        acc[i][j] = __dadd_rn(acc[i][j], __dmul_rn(a[i], b[j]));
-            }
+            for (int kk = 0; kk < Cfg::BK; ++kk)
+                bw_kstep<Cfg>(acc, a_s, b_s, kk);
         }
         else {
-            for (int kk = 0; kk < kend; ++kk) {
-                double a[8], b[8];
-#pragma unroll
-                for (int i = 0; i < 8; ++i)
-                    a[i] = a_s[i * 16 * bw::A_LD + kk];
-#pragma unroll
-                for (int j = 0; j < 8; ++j)
-                    b[j] = b_s[kk * bw::BN + j * 16];
-#pragma unroll
-                for (int i = 0; i < 8; ++i)
-#pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                        acc[i][j] = __dadd_rn(acc[i][j], __dmul_rn(a[i], b[j]));
-            }
+            for (int kk = 0; kk < kend; ++kk)
+                bw_kstep<Cfg>(acc, a_s, b_s, kk);
         }
     }
     cp_async_wait<0>();
@@ -858,7 +856,7 @@ __global__ void __launch_bounds__(bw::THREADS, 1) dgemm_bitwise_kernel(GemmParam
             continue;
         double* crow = p.c + row * p.ldc;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < Cfg::NJ; ++j) {
             const int col = bn + tx + 16 * j;
             if (col < p.n)
                 crow[col] = __dadd_rn(__dmul_rn(p.alpha, acc[i][j]), __dmul_rn(p.beta, crow[col]));
@@ -866,28 +864,32 @@ __global__ void __launch_bounds__(bw::THREADS, 1) dgemm_bitwise_kernel(GemmParam
     }
 }
 
-kw_status launch_bitwise(cudaStream_t s, const GemmParams& p0)
+template <class Cfg>
+kw_status launch_bitwise_cfg(cudaStream_t s, const GemmParams& p0)
 {
     GemmParams p = p0;
-    p.tiles_m = static_cast<int>(kw::ceil_div(p.m, bw::BM));
-    p.tiles_n = static_cast<int>(kw::ceil_div(p.n, bw::BN));
+    p.tiles_m = static_cast<int>(kw::ceil_div(p.m, Cfg::BM));
+    p.tiles_n = static_cast<int>(kw::ceil_div(p.n, Cfg::BN));
     const long long tiles = static_cast<long long>(p.tiles_m) * p.tiles_n;
     if (tiles > INT_MAX)
         return kw::usage("dgemm: problem too large for the tile grid");
     const bool vec16 = (p.lda % 2 == 0) && (p.ldb % 2 == 0) && (reinterpret_cast<uintptr_t>(p.a) % 16 == 0) &&
                        (reinterpret_cast<uintptr_t>(p.b) % 16 == 0);
-    auto kern = vec16 ? dgemm_bitwise_kernel<true> : dgemm_bitwise_kernel<false>;
+    auto kern = vec16 ? dgemm_bitwise_kernel<Cfg, true> : dgemm_bitwise_kernel<Cfg, false>;
     static bool attr[2] = {false, false};
     if (!attr[vec16]) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bw::SMEM));
+        cudaError_t e =
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Cfg::SMEM));
         if (e != cudaSuccess)
             return kw::cuda_fail("dgemm_bitwise: cudaFuncSetAttribute", e);
         attr[vec16] = true;
     }
-    kern<<<static_cast<unsigned>(tiles), bw::THREADS, bw::SMEM, s>>>(p);
+    kern<<<static_cast<unsigned>(tiles), Cfg::THREADS, Cfg::SMEM, s>>>(p);
     kw::g_launches.fetch_add(1, std::memory_order_relaxed);
     return KW_OK;
 }
+
+kw_status launch_bitwise(cudaStream_t s, const GemmParams& p) { return launch_bitwise_cfg<Bw128>(s, p); }
 
 kw_status validate_gemm(size_t m, size_t n, size_t k, const double* A, size_t lda, const double* B, size_t ldb,
                         const double* C, size_t ldc)
