@@ -44,6 +44,13 @@ struct Queue {
     cudaEvent_t ev_b = nullptr;
     static constexpr int kBPanels = 8;
     cudaEvent_t ev_bp[kBPanels] = {}; // B column panel j uploaded (DGEMM e2e streaming)
+    // Streamed e2e DGEMM: the tile order (pinned host copy + device copy), the key it was built
+    // for and the event of its last upload.
+    void* order_host = nullptr;
+    void* order_dev = nullptr;
+    size_t order_bytes = 0;
+    size_t order_key[8] = {};
+    cudaEvent_t ev_order = nullptr;
 };
 
 // RAII device selector: the reference's queues are bound to one device; every entry point

@@ -28,7 +28,10 @@
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
+#include <utility>
+#include <vector>
 
 namespace {
 
@@ -106,6 +109,16 @@ struct GemmParams {
     double* c;
     long long ldc;
     int tiles_m, tiles_n;
+    // Streamed mode (host-resident operands, dgemm_streamed): the copy stream uploads A in row
+    // panels, B in column panels and C in blocks, and publishes each with a stream write of
+    // ready[] = 1: [npr A panels | npc B panels | npr*npc C blocks]. The persistent kernel walks
+    // tile_list (availability order) and waits for a tile's panels before loading them; every
+    // consumer warp bumps done[block] after storing its part of the block, which releases the
+    // block's download. nullptr = ordinary launch (operands already resident).
+    const int2* tile_list;
+    const uint32_t* ready;
+    uint32_t* done;
+    int panel_rows, panel_cols, npr, npc;
 };
 
 template <class Cfg, bool VEC16>
@@ -323,6 +336,23 @@ __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map)
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
 
+// Streamed mode: waits until the copy stream has published a panel (ready flag != 0). Bounded:
+// a flag that never arrives traps (a device fault the queue reports) instead of hanging the GPU.
+__device__ __forceinline__ void wait_ready(const uint32_t* flag)
+{
+    uint32_t ns = 64;
+    for (long long spins = 0;; ++spins) {
+        uint32_t v;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(flag) : "memory");
+        if (v != 0)
+            return;
+        if (spins > (1ll << 26))
+            __trap();
+        __nanosleep(ns);
+        ns = ns < 2048 ? ns * 2 : ns;
+    }
+}
+
 template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int MIN_BLOCKS_ = 1, bool PAIRED_ = false>
 struct TmaCfg {
     static constexpr int BM = BM_, BN = BN_, BK = 16, WM = WM_, WN = WN_, STAGES = STAGES_;
@@ -357,7 +387,7 @@ struct TmaCfg {
     static_assert(WN % 16 == 0 && BN % 16 == 0 && BM <= 256, "tile shape");
 };
 
-template <class Cfg>
+template <class Cfg, bool STREAMED = false>
 __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmParams p)
 {
@@ -374,6 +404,12 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     constexpr int GROUP = 8;
     const int ntiles = p.tiles_m * p.tiles_n;
     auto origin = [&](int tile, int& bm, int& bn) {
+        if constexpr (STREAMED) {
+            const int2 v = p.tile_list[tile];
+            bm = v.x * Cfg::BM;
+            bn = v.y * Cfg::BN;
+            return;
+        }
         const int per_group = GROUP * p.tiles_n;
         const int group = tile / per_group;
         const int first_m = group * GROUP;
@@ -406,6 +442,17 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
                 int bm, bn;
                 origin(tile, bm, bn);
+                if constexpr (STREAMED) {
+                    // A row panel, B column panel and the C block of this tile resident? The
+                    // consumers read C only after this stage's mbarrier, which orders them
+                    // after these acquires.
+                    const int pi = bm / p.panel_rows, pj = bn / p.panel_cols;
+                    wait_ready(p.ready + pi);
+                    wait_ready(p.ready + p.npr + pj);
+                    wait_ready(p.ready + p.npr + p.npc + pi * p.npc + pj);
+                    // the panels were written by the copy engine; order the TMA reads after
+                    asm volatile("fence.proxy.async.global;\n" ::: "memory");
+                }
                 for (int kt = 0; kt < ktiles; ++kt, ++it) {
                     const int s = it % Cfg::STAGES;
                     const uint32_t r = static_cast<uint32_t>(it / Cfg::STAGES);
@@ -597,6 +644,14 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
             }
         }
     }
+    if constexpr (STREAMED) {
+        // this warp's share of the block is stored: make it visible to the copy engine, count it
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence_system();
+            atomicAdd(p.done + (bm / p.panel_rows) * p.npc + bn / p.panel_cols, 1u);
+        }
+    }
     } // tile loop
 }
 
@@ -640,7 +695,7 @@ bool tma_eligible(const GemmParams& p)
            reinterpret_cast<uintptr_t>(p.b) % 16 == 0 && encode_fn() != nullptr;
 }
 
-template <class Cfg, bool PERSISTENT = false>
+template <class Cfg, bool PERSISTENT = false, bool STREAMED = false>
 kw_status launch_tma(cudaStream_t s, const GemmParams& p0);
 
 // Tile configurations (the DGEMM half of the work-division sweep, BASELINE.json configs[4]).
@@ -950,7 +1005,7 @@ int sm_count()
     return sms;
 }
 
-template <class Cfg, bool PERSISTENT>
+template <class Cfg, bool PERSISTENT, bool STREAMED>
 kw_status launch_tma(cudaStream_t s, const GemmParams& p0)
 {
     GemmParams p = p0;
@@ -959,14 +1014,20 @@ kw_status launch_tma(cudaStream_t s, const GemmParams& p0)
     const long long tiles = static_cast<long long>(p.tiles_m) * p.tiles_n;
     if (tiles > INT_MAX)
         return kw::usage("dgemm: problem too large for the tile grid");
-    if (!tma_eligible(p))
+    if (!tma_eligible(p)) {
+        if (p.ready)
+            return kw::usage("dgemm (streamed): operands not TMA-addressable");
         return launch_dmma<Cfg128>(s, p0); // unaligned operands: cp.async kernel
+    }
     CUtensorMap ma, mb;
-    if (!make_map(&ma, p.a, p.m, p.k, p.lda, Cfg::BM) || !make_map(&mb, p.b, p.k, p.n, p.ldb, 16))
+    if (!make_map(&ma, p.a, p.m, p.k, p.lda, Cfg::BM) || !make_map(&mb, p.b, p.k, p.n, p.ldb, 16)) {
+        if (p.ready)
+            return kw::usage("dgemm (streamed): tensor map encoding failed");
         return launch_dmma<Cfg128>(s, p0);
+    }
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(dgemm_tma_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(dgemm_tma_kernel<Cfg, STREAMED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(Cfg::SMEM));
         if (e != cudaSuccess)
             return kw::cuda_fail("dgemm: cudaFuncSetAttribute", e);
@@ -974,7 +1035,7 @@ kw_status launch_tma(cudaStream_t s, const GemmParams& p0)
     }
     const long long resident = static_cast<long long>(sm_count()) * Cfg::MIN_BLOCKS;
     const unsigned grid = static_cast<unsigned>(PERSISTENT && tiles > resident ? resident : tiles);
-    dgemm_tma_kernel<Cfg><<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(ma, mb, p);
+    dgemm_tma_kernel<Cfg, STREAMED><<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(ma, mb, p);
     kw::g_launches.fetch_add(1, std::memory_order_relaxed);
     return KW_OK;
 }
@@ -1064,6 +1125,11 @@ GemmParams make_params(size_t m, size_t n, size_t k, double alpha, const double*
     p.c = C;
     p.ldc = static_cast<long long>(ldc);
     p.tiles_m = p.tiles_n = 0;
+    p.tile_list = nullptr;
+    p.ready = nullptr;
+    p.done = nullptr;
+    p.panel_rows = p.panel_cols = 1;
+    p.npr = p.npc = 0;
     return p;
 }
 
@@ -1200,6 +1266,290 @@ kw_status dgemm_staged(kw::Queue* q, int tile, size_t m, size_t n, size_t k, dou
     return kw::after_enqueue(q, "dgemm");
 }
 
+// ------------------------------------------------------------------------------------------
+// Streamed e2e DGEMM (all three operands in pinned host memory). The row-panel schedule above
+// cannot compute anything useful until the whole of B has crossed PCIe (~10 ms at 8192), and
+// every panel launch ends in a partial wave. Here the operands go up in an order that grows
+// the computable region as a square — A row panel i, B column panel j, and the C blocks they
+// complete — while ONE persistent kernel walks the tiles in that availability order, waiting
+// per tile for its panels (ready flags written by the copy stream with cuStreamWriteValue32,
+// which fences the copy before the flag). Finished C blocks go back on the aux stream as soon
+// as every consumer warp of every tile in the block has counted in (cuStreamWaitValue32 on
+// done[block]). Same kernel arithmetic per tile -> bitwise identical to the resident launch.
+// Deadlock freedom: the kernel waits only on copies, the copies wait only on ev_start (before
+// the kernel), the downloads wait on the kernel; everything is enqueued in that order, so even
+// streams that share a hardware queue never block a producer behind its consumer.
+// ------------------------------------------------------------------------------------------
+using PFN_streamValue32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+struct StreamMemOps {
+    PFN_streamValue32 write = nullptr, wait = nullptr;
+};
+
+const StreamMemOps& stream_mem_ops()
+{
+    static StreamMemOps ops;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* w = nullptr;
+        void* t = nullptr;
+        cudaDriverEntryPointQueryResult qw, qt;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &w, cudaEnableDefault, &qw) == cudaSuccess &&
+            cudaGetDriverEntryPoint("cuStreamWaitValue32", &t, cudaEnableDefault, &qt) == cudaSuccess &&
+            qw == cudaDriverEntryPointSuccess && qt == cudaDriverEntryPointSuccess && w && t) {
+            ops.write = reinterpret_cast<PFN_streamValue32>(w);
+            ops.wait = reinterpret_cast<PFN_streamValue32>(t);
+        }
+        cudaGetLastError();
+    });
+    return ops;
+}
+
+template <class Cfg>
+kw_status launch_streamed(cudaStream_t s, const GemmParams& p) { return launch_tma<Cfg, true, true>(s, p); }
+
+// Returns KW_OK with *used = false (nothing enqueued) when the streamed schedule does not apply.
+kw_status dgemm_streamed(kw::Queue* q, int tile, size_t m, size_t n, size_t k, double alpha, const double* A,
+                         size_t lda, const double* B, size_t ldb, double beta, double* C, size_t ldc, bool* used)
+{
+    *used = false;
+    const char* env = std::getenv("KW_E2E_STREAMED");
+    if ((env && env[0] == '0') || k == 0 || m > INT_MAX || n > INT_MAX || k > INT_MAX)
+        return KW_OK;
+    // Only where compute is comparable to the PCIe time: below that the upload is the whole
+    // story and the fewer, larger copies of the row-panel schedule win (measured at 4096^3).
+    const char* mi = std::getenv("KW_E2E_MIN_INTENSITY");
+    const double min_intensity = mi ? std::atof(mi) : 400.0;
+    const double intensity = 2.0 * double(m) * double(n) * double(k) /
+                             (8.0 * (double(m) * double(k) + double(k) * double(n) + double(m) * double(n)));
+    if (intensity < min_intensity)
+        return KW_OK;
+    const StreamMemOps& ops = stream_mem_ops();
+    if (!ops.write || !ops.wait)
+        return KW_OK;
+    const size_t ldas = round2(k), ldbs = round2(n), ldcs = round2(n);
+    // Panel grid: P x P blocks (KW_E2E_PANELS, default 12 — profiles/e2e_dgemm_streamed_r01.txt),
+    // edges in whole 128s so both tile shapes nest in every panel.
+    const char* pe = std::getenv("KW_E2E_PANELS");
+    const long pv = pe ? std::atol(pe) : 0;
+    const size_t P = pv > 0 && pv <= 64 ? static_cast<size_t>(pv) : 12;
+    const size_t R = std::max<size_t>(128, kw::ceil_div(kw::ceil_div(m, P), 128) * 128);
+    const size_t W = std::max<size_t>(128, kw::ceil_div(kw::ceil_div(n, P), 128) * 128);
+    const size_t npr = kw::ceil_div(m, R), npc = kw::ceil_div(n, W);
+    const int cfg = tile == 64 ? kCfgSmall : pick_config(make_params(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc));
+    const int bm = kCfgs[cfg].bm, bn = kCfgs[cfg].bn;
+    const uint32_t consumers = cfg == kCfgWide ? Tma64x128x2p::CONSUMERS : Tma64x64x3p::CONSUMERS;
+    const size_t tiles = kw::ceil_div(m, bm) * kw::ceil_div(n, bn);
+    const size_t nflags = npr + npc + npr * npc, ndone = npr * npc;
+    const size_t mat_bytes = (m * ldas + k * ldbs + m * ldcs) * sizeof(double);
+    const size_t aux_bytes = (nflags + ndone) * sizeof(uint32_t) + 512;
+    if (q->scratch_bytes < mat_bytes + aux_bytes) {
+        // growing the scratch: only when the operands fit comfortably (a resource-manager query,
+        // so not on every call)
+        size_t free_b = 0, total_b = 0;
+        if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+            cudaGetLastError();
+            return KW_OK;
+        }
+        if (static_cast<double>(mat_bytes + aux_bytes) > 0.8 * static_cast<double>(free_b + q->scratch_bytes))
+            return KW_OK; // too large to hold whole: the row-panel ring schedule
+    }
+    kw_status st = kw::ensure_scratch(q, mat_bytes + aux_bytes);
+    if (st != KW_OK)
+        return st;
+    char* base = static_cast<char*>(q->scratch);
+    double* Ad = reinterpret_cast<double*>(base);
+    double* Bd = Ad + m * ldas;
+    double* Cd = Bd + k * ldbs;
+    char* tail = reinterpret_cast<char*>(Cd + m * ldcs);
+    tail = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(tail) + 255) & ~uintptr_t(255));
+    uint32_t* ready = reinterpret_cast<uint32_t*>(tail);
+    uint32_t* done = ready + nflags;
+
+    GemmParams p = make_params(m, n, k, alpha, Ad, ldas, Bd, ldbs, beta, Cd, ldcs);
+    if (!tma_eligible(p))
+        return KW_OK;
+
+    // The growth order: A_0, B_0, then add a B column panel while it is not ahead of the A row
+    // panels, else an A row panel; each addition completes the C blocks of its row/column.
+    struct Step {
+        bool is_a;
+        size_t idx;
+    };
+    std::vector<Step> steps;
+    std::vector<std::pair<size_t, size_t>> blocks; // C blocks in availability order
+    {
+        size_t a = 0, b = 0;
+        while (a < npr || b < npc) {
+            const bool add_b = b < npc && (a >= npr || b < a);
+            if (add_b) {
+                for (size_t i = 0; i < a; ++i)
+                    blocks.emplace_back(i, b);
+                steps.push_back({false, b++});
+            }
+            else {
+                for (size_t j = 0; j < b; ++j)
+                    blocks.emplace_back(a, j);
+                steps.push_back({true, a++});
+            }
+        }
+    }
+    std::vector<int2> order;
+    order.reserve(tiles);
+    for (const auto& bl : blocks) {
+        const size_t r0 = bl.first * R, r1 = std::min(m, r0 + R), c0 = bl.second * W, c1 = std::min(n, c0 + W);
+        for (size_t tr = r0 / bm; tr < kw::ceil_div(r1, bm); ++tr)
+            for (size_t tc = c0 / bn; tc < kw::ceil_div(c1, bn); ++tc)
+                order.push_back(make_int2(static_cast<int>(tr), static_cast<int>(tc)));
+    }
+    if (order.size() != tiles)
+        return kw::task_fail(q, "dgemm (streamed): tile order does not cover the output");
+
+    // The tile order goes up from a pinned copy, once per (scratch, shape, panel grid, tile).
+    const size_t key[8] = {m, n, R, W, static_cast<size_t>(cfg), 1, 0, 0};
+    const bool order_current = std::equal(key, key + 8, q->order_key);
+    auto flag = [&](size_t idx) { return reinterpret_cast<CUdeviceptr>(ready + idx); };
+    cudaError_t e = cudaMemsetAsync(ready, 0, (nflags + ndone) * sizeof(uint32_t), q->stream);
+    if (e == cudaSuccess && !order_current) {
+        if (q->ev_order)
+            e = cudaEventSynchronize(q->ev_order); // the previous upload still reads order_host
+        else
+            e = cudaEventCreateWithFlags(&q->ev_order, cudaEventDisableTiming);
+        const size_t bytes = tiles * sizeof(int2);
+        if (e == cudaSuccess && q->order_bytes < bytes) {
+            // earlier kernels on this queue may still read order_dev
+            e = cudaStreamSynchronize(q->stream);
+            if (q->order_host)
+                cudaFreeHost(q->order_host);
+            if (q->order_dev)
+                cudaFree(q->order_dev);
+            q->order_host = q->order_dev = nullptr;
+            q->order_bytes = 0;
+            if (e == cudaSuccess)
+                e = cudaHostAlloc(&q->order_host, bytes, cudaHostAllocDefault);
+            if (e == cudaSuccess)
+                e = cudaMalloc(&q->order_dev, bytes);
+            if (e == cudaSuccess)
+                q->order_bytes = bytes;
+        }
+        if (e == cudaSuccess) {
+            std::memcpy(q->order_host, order.data(), bytes);
+            e = cudaMemcpyAsync(q->order_dev, q->order_host, bytes, cudaMemcpyHostToDevice, q->stream);
+        }
+        if (e == cudaSuccess)
+            e = cudaEventRecord(q->ev_order, q->stream);
+        if (e == cudaSuccess)
+            std::copy(key, key + 8, q->order_key);
+        else
+            std::fill(q->order_key, q->order_key + 8, size_t(0));
+    }
+    if (e == cudaSuccess)
+        e = cudaEventRecord(q->ev_start, q->stream);
+    if (e == cudaSuccess)
+        e = cudaStreamWaitEvent(q->h2d, q->ev_start, 0);
+    if (e != cudaSuccess)
+        return kw::task_fail(q, std::string("dgemm (streamed): ") + cudaGetErrorString(e));
+    const bool trace = std::getenv("KW_E2E_TRACE") != nullptr;
+    cudaEvent_t tev[5] = {};
+    if (trace) {
+        for (auto& ev : tev)
+            cudaEventCreate(&ev);
+        cudaEventRecord(tev[0], q->stream);
+    }
+
+    // 1. uploads + ready flags (copy stream)
+    CUresult ce = CUDA_SUCCESS;
+    size_t a = 0, b = 0;
+    for (const Step& stp : steps) {
+        if (e != cudaSuccess || ce != CUDA_SUCCESS)
+            break;
+        if (stp.is_a) {
+            const size_t r0 = stp.idx * R, rows = std::min(m, r0 + R) - r0;
+            e = cudaMemcpy2DAsync(Ad + r0 * ldas, ldas * 8, A + r0 * lda, lda * 8, k * 8, rows,
+                                  cudaMemcpyHostToDevice, q->h2d);
+            if (e == cudaSuccess)
+                ce = ops.write(q->h2d, flag(stp.idx), 1, 0);
+            if (e == cudaSuccess && ce == CUDA_SUCCESS && b > 0) {
+                const size_t cols = std::min(n, b * W);
+                e = cudaMemcpy2DAsync(Cd + r0 * ldcs, ldcs * 8, C + r0 * ldc, ldc * 8, cols * 8, rows,
+                                      cudaMemcpyHostToDevice, q->h2d);
+                for (size_t j = 0; j < b && e == cudaSuccess && ce == CUDA_SUCCESS; ++j)
+                    ce = ops.write(q->h2d, flag(npr + npc + stp.idx * npc + j), 1, 0);
+            }
+            ++a;
+        }
+        else {
+            const size_t c0 = stp.idx * W, cols = std::min(n, c0 + W) - c0;
+            e = cudaMemcpy2DAsync(Bd + c0, ldbs * 8, B + c0, ldb * 8, cols * 8, k, cudaMemcpyHostToDevice, q->h2d);
+            if (e == cudaSuccess)
+                ce = ops.write(q->h2d, flag(npr + stp.idx), 1, 0);
+            if (e == cudaSuccess && ce == CUDA_SUCCESS && a > 0) {
+                const size_t rows = std::min(m, a * R);
+                e = cudaMemcpy2DAsync(Cd + c0, ldcs * 8, C + c0, ldc * 8, cols * 8, rows, cudaMemcpyHostToDevice,
+                                      q->h2d);
+                for (size_t i = 0; i < a && e == cudaSuccess && ce == CUDA_SUCCESS; ++i)
+                    ce = ops.write(q->h2d, flag(npr + npc + i * npc + stp.idx), 1, 0);
+            }
+            ++b;
+        }
+    }
+    if (e != cudaSuccess || ce != CUDA_SUCCESS)
+        return kw::task_fail(q, "dgemm (streamed): upload schedule failed");
+    *used = true;
+    if (trace)
+        cudaEventRecord(tev[3], q->h2d);
+    if (trace)
+        cudaEventRecord(tev[1], q->stream);
+
+    // 2. the persistent kernel (queue stream)
+    p.tile_list = static_cast<const int2*>(q->order_dev);
+    p.ready = ready;
+    p.done = done;
+    p.panel_rows = static_cast<int>(R);
+    p.panel_cols = static_cast<int>(W);
+    p.npr = static_cast<int>(npr);
+    p.npc = static_cast<int>(npc);
+    st = cfg == kCfgWide ? launch_streamed<Tma64x128x2p>(q->stream, p) : launch_streamed<Tma64x64x3p>(q->stream, p);
+    if (st != KW_OK)
+        return kw::task_fail(q, kw::last_error());
+    e = cudaGetLastError();
+    if (trace)
+        cudaEventRecord(tev[2], q->stream);
+
+    // 3. downloads, block by block as they complete (aux stream)
+    if (e == cudaSuccess)
+        e = cudaStreamWaitEvent(q->aux, q->ev_start, 0);
+    for (size_t bi = 0; bi < blocks.size() && e == cudaSuccess && ce == CUDA_SUCCESS; ++bi) {
+        const size_t i = blocks[bi].first, j = blocks[bi].second;
+        const size_t r0 = i * R, rows = std::min(m, r0 + R) - r0, c0 = j * W, cols = std::min(n, c0 + W) - c0;
+        const uint32_t expect = static_cast<uint32_t>(kw::ceil_div(rows, bm) * kw::ceil_div(cols, bn)) * consumers;
+        ce = ops.wait(q->aux, reinterpret_cast<CUdeviceptr>(done + i * npc + j), expect, 0 /* GEQ */);
+        if (ce == CUDA_SUCCESS)
+            e = cudaMemcpy2DAsync(C + r0 * ldc + c0, ldc * 8, Cd + r0 * ldcs + c0, ldcs * 8, cols * 8, rows,
+                                  cudaMemcpyDeviceToHost, q->aux);
+    }
+    if (e == cudaSuccess && ce == CUDA_SUCCESS) {
+        e = cudaEventRecord(q->ev_join, q->aux);
+        if (e == cudaSuccess)
+            e = cudaStreamWaitEvent(q->stream, q->ev_join, 0);
+    }
+    if (e != cudaSuccess || ce != CUDA_SUCCESS)
+        return kw::task_fail(q, "dgemm (streamed): download schedule failed");
+    if (trace) {
+        cudaEventRecord(tev[4], q->aux);
+        cudaEventSynchronize(tev[4]);
+        cudaStreamSynchronize(q->stream);
+        float t[5] = {};
+        for (int i = 1; i < 5; ++i)
+            cudaEventElapsedTime(&t[i], tev[0], tev[i]);
+        std::fprintf(stderr, "[kw trace] kernel start %.2f end %.2f | last upload %.2f | last download %.2f ms\n",
+                     t[1], t[2], t[3], t[4]);
+        for (auto& ev : tev)
+            cudaEventDestroy(ev);
+    }
+    return kw::after_enqueue(q, "dgemm");
+}
+
 } // namespace
 
 namespace kw {
@@ -1274,6 +1624,13 @@ kw_status kw_dgemm(kw_queue qh, const kw_workdiv* wd, size_t m, size_t n, size_t
         if (st != KW_OK)
             return kw::task_fail(q, kw::last_error());
         return kw::after_enqueue(q, "dgemm");
+    }
+    if (!a_dev && !b_dev && !c_dev && kw::pointer_kind(A, nullptr) == KW_MEM_PINNED &&
+        kw::pointer_kind(B, nullptr) == KW_MEM_PINNED && kw::pointer_kind(C, nullptr) == KW_MEM_PINNED) {
+        bool used = false;
+        st = dgemm_streamed(q, tile, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, &used);
+        if (st != KW_OK || used)
+            return st;
     }
     return dgemm_staged(q, tile, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, a_dev, b_dev, c_dev);
 }

@@ -321,6 +321,12 @@ kw_status kw_queue_destroy(kw_queue qh)
     for (cudaEvent_t e : q->ev_bp)
         if (e)
             cudaEventDestroy(e);
+    if (q->ev_order)
+        cudaEventDestroy(q->ev_order);
+    if (q->order_host)
+        cudaFreeHost(q->order_host);
+    if (q->order_dev)
+        cudaFree(q->order_dev);
     if (q->scratch)
         cudaFree(q->scratch);
     cudaStreamDestroy(q->h2d);

@@ -222,6 +222,54 @@ def test_host_buffers_are_staged(gpu, oracle):
     assert np.array_equal(Cb.host_view()[:, :n], want)
 
 
+@pytest.mark.parametrize("panels", ["1", "3", "8", "16"])
+def test_streamed_host_schedule_is_bitwise_the_resident_launch(gpu, panels, monkeypatch):
+    """The streamed e2e schedule (pinned A, B, C: panels uploaded in square-growth order, one
+    persistent kernel waiting on per-panel ready flags, C blocks downloaded as they complete)
+    gives the bits of the device-resident launch for ragged shapes, both tile contracts, several
+    panel grids and back-to-back enqueues on one queue (flags are reset per call)."""
+    monkeypatch.setenv("KW_E2E_PANELS", panels)
+    monkeypatch.setenv("KW_E2E_MIN_INTENSITY", "0")  # small shapes: force the streamed schedule
+    rng = np.random.default_rng(int(panels) + 40)
+    host = kw.Device.host()
+    q = kw.Queue(gpu, kw.QueueFlavor.Async)
+    for (m, n, k), tile in (((1500, 700, 333), 128), ((64, 64, 64), 128), ((129, 4100, 17), 128),
+                            ((2050, 260, 1000), 64), ((1, 1, 1), 128), ((3000, 2900, 520), 128)):
+        a, b, c = rng.random((m, k)) * 10, rng.random((k, n)) * 10, rng.random((m, n)) * 10
+        want = tiled(gpu, 0.7, 1.3, a, b, c, tile=tile)
+        A, B, Cb = (kw.Buffer(host, kw.IndexVec(*x.shape), 8) for x in (a, b, c))
+        for buf, x in ((A, a), (B, b), (Cb, c)):
+            buf.host_view()[:, : x.shape[1]] = x
+        task = kw.createExec(GPU, kw.gemmTiledWorkDiv(GPU, m, n, tile), kw.GemmTiledKernel(),
+                             kw.GemmArgs(m, n, k, 0.7, 1.3, A, B, Cb, tile))
+        q.enqueue(task)
+        q.wait()
+        assert np.array_equal(Cb.host_view()[:, :n], want), (m, n, k, tile)
+        # twice more back to back: C accumulates; compare against the resident path doing the same
+        q.enqueue(task)
+        q.enqueue(task)
+        q.wait()
+        want2 = tiled(gpu, 0.7, 1.3, a, b, tiled(gpu, 0.7, 1.3, a, b, want, tile=tile), tile=tile)
+        assert np.array_equal(Cb.host_view()[:, :n], want2), (m, n, k, tile, "repeat")
+
+
+def test_row_panel_host_schedule_still_matches(gpu, monkeypatch):
+    """KW_E2E_STREAMED=0 keeps the row-panel ring schedule (also the path for operands too large
+    to hold whole on the device); same bits."""
+    monkeypatch.setenv("KW_E2E_STREAMED", "0")
+    rng = np.random.default_rng(44)
+    m, n, k = 1800, 900, 410
+    a, b, c = rng.random((m, k)) * 10, rng.random((k, n)) * 10, rng.random((m, n)) * 10
+    want = tiled(gpu, 1.1, 0.6, a, b, c)
+    host = kw.Device.host()
+    A, B, Cb = (kw.Buffer(host, kw.IndexVec(*x.shape), 8) for x in (a, b, c))
+    for buf, x in ((A, a), (B, b), (Cb, c)):
+        buf.host_view()[:, : x.shape[1]] = x
+    kw.executeTask(GPU, kw.gemmTiledWorkDiv(GPU, m, n, 128), kw.GemmTiledKernel(),
+                   kw.GemmArgs(m, n, k, 1.1, 0.6, A, B, Cb))
+    assert np.array_equal(Cb.host_view()[:, :n], want)
+
+
 def test_4096_within_tolerance(gpu, oracle):
     """The configured 1-GPU point: Workload("gemm-tiled", 4096, 42)."""
     n = 4096

@@ -1,5 +1,6 @@
-"""e2e DGEMM (host pinned A, B, C through the public API) at n = 4096 and 8192, median of 3
+"""e2e DGEMM (host pinned A, B, C through the public API) at n = 4096 and 8192, median of 5
 wall-clock steps."""
+import os
 import statistics
 import sys
 import time
@@ -21,15 +22,16 @@ def run(n):
     q.enqueue(task)
     q.wait()
     ts = []
-    for _ in range(3):
+    for _ in range(8):
         t = time.perf_counter()
         q.enqueue(task)
         q.wait()
         ts.append(time.perf_counter() - t)
     med = statistics.median(ts)
-    print(f"n={n} {med*1e3:.1f} ms {2*n**3/med/1e12:.2f} TFLOP/s")
+    tag = f"streamed={os.environ.get('KW_E2E_STREAMED', '1')} panels={os.environ.get('KW_E2E_PANELS', '12')}"
+    print(f"{tag} conn={os.environ.get('CUDA_DEVICE_MAX_CONNECTIONS', '-')} n={n} {med*1e3:.1f} ms {2*n**3/med/1e12:.2f} TFLOP/s steps " + " ".join(f"{t*1e3:.1f}" for t in ts))
 
 
 if __name__ == "__main__":
-    for n in (4096, 8192):
+    for n in [int(v) for v in os.environ.get("KW_E2E_SIZES", "4096,8192").split(",")]:
         run(n)
