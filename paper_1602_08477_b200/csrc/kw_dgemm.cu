@@ -336,15 +336,20 @@ __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map)
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
 
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* flag)
+{
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(flag) : "memory");
+    return v;
+}
+
 // Streamed mode: waits until the copy stream has published a panel (ready flag != 0). Bounded:
 // a flag that never arrives traps (a device fault the queue reports) instead of hanging the GPU.
 __device__ __forceinline__ void wait_ready(const uint32_t* flag)
 {
     uint32_t ns = 64;
     for (long long spins = 0;; ++spins) {
-        uint32_t v;
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(flag) : "memory");
-        if (v != 0)
+        if (ld_acquire_gpu(flag) != 0)
             return;
         if (spins > (1ll << 26))
             __trap();
@@ -443,13 +448,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
                 int bm, bn;
                 origin(tile, bm, bn);
                 if constexpr (STREAMED) {
-                    // A row panel, B column panel and the C block of this tile resident? The
-                    // consumers read C only after this stage's mbarrier, which orders them
-                    // after these acquires.
-                    const int pi = bm / p.panel_rows, pj = bn / p.panel_cols;
-                    wait_ready(p.ready + pi);
-                    wait_ready(p.ready + p.npr + pj);
-                    wait_ready(p.ready + p.npr + p.npc + pi * p.npc + pj);
+                    // A row panel and B column panel of this tile resident? (The C block is
+                    // waited for before the last k-tile, below.)
+                    wait_ready(p.ready + bm / p.panel_rows);
+                    wait_ready(p.ready + p.npr + bn / p.panel_cols);
                     // the panels were written by the copy engine; order the TMA reads after
                     asm volatile("fence.proxy.async.global;\n" ::: "memory");
                 }
@@ -457,6 +459,14 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
                     const int s = it % Cfg::STAGES;
                     const uint32_t r = static_cast<uint32_t>(it / Cfg::STAGES);
                     mbar_wait(&empty[s], (r & 1u) ^ 1u);
+                    if constexpr (STREAMED) {
+                        // The consumers read C in the epilogue, after this last stage's full
+                        // barrier (release by this arrive, acquire by their wait): acquiring the
+                        // C block's flag here orders those reads after its upload, and leaves
+                        // the upload a whole tile of slack.
+                        if (kt == ktiles - 1)
+                            wait_ready(p.ready + p.npr + p.npc + (bm / p.panel_rows) * p.npc + bn / p.panel_cols);
+                    }
                     mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
                     const uint32_t sa = smem_u32(smem + s * Cfg::STAGE_BYTES);
                     tma_load_2d(sa, &tmA, kt * Cfg::BK, bm, &full[s]);
