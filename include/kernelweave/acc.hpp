@@ -24,8 +24,10 @@ public:
             throw UsageError("AccContext: index and work-division dimensionalities differ");
     }
     KW_HD AccContext(const kw_workdiv& wd, const IndexVec& gridBlockIdx, const IndexVec& blockThreadIdx,
-                     std::byte* shared = nullptr, std::size_t sharedBytes = 0) noexcept
-        : m_wd(wd), m_block(gridBlockIdx), m_thread(blockThreadIdx), m_shared(shared), m_sharedBytes(sharedBytes)
+                     std::byte* shared = nullptr, std::size_t sharedBytes = 0,
+                     std::uint32_t* failSlot = nullptr) noexcept
+        : m_wd(wd), m_block(gridBlockIdx), m_thread(blockThreadIdx), m_shared(shared), m_sharedBytes(sharedBytes),
+          m_fail(failSlot)
     {
     }
     AccContext(const AccContext&) = default;
@@ -40,6 +42,8 @@ public:
     KW_HD std::byte* sharedBase() const noexcept { return m_shared; }
     KW_HD std::size_t sharedBytes() const noexcept { return m_sharedBytes; }
     KW_HD std::size_t& sharedCursor() const noexcept { return m_cursor; }
+    // Device launches: the task's failure slot (kw_queue_fail_slot), set by failTask().
+    KW_HD std::uint32_t* failSlot() const noexcept { return m_fail; }
 
 private:
     kw_workdiv m_wd;
@@ -47,6 +51,7 @@ private:
     IndexVec m_thread;
     std::byte* m_shared = nullptr;
     std::size_t m_sharedBytes = 0;
+    std::uint32_t* m_fail = nullptr;
     mutable std::size_t m_cursor = 0;
 };
 

@@ -9,6 +9,9 @@
  *                                                  sequence, zero-initialised (accel.cpp:286-292)
  *   syncBlockThreads(acc)                       -> __syncthreads (accel.cpp:294-302)
  *   atomicAdd(acc, cell, v) f64 / i64 / u64     -> native global atomics (accel.cpp:304-321)
+ *   failTask(acc, code)                         -> the device form of throwing from a functor
+ *                                                  (accel.cpp:240-248): the task fails, wait()
+ *                                                  raises TaskError, later tasks still run
  * Buffers cross into device code as BufferView (pointer, pitch, extent): a host Buffer object
  * cannot be dereferenced on the GPU.
  *
@@ -102,6 +105,16 @@ __device__ inline T* allocSharedMem(const AccContext& acc, std::size_t count)
 
 __device__ inline void syncBlockThreads(const AccContext&) { __syncthreads(); }
 
+/// Fails the running task with a non-zero code (any thread, any number of times; one code is
+/// kept). Device code cannot throw, so the functor returns after calling this — the reference's
+/// `throw` inside operator() (test_accel.cpp:403-430). Reported by Queue::wait() as TaskError and
+/// by the task's TaskHandle as TaskState::Failed; later tasks on the queue still run.
+__device__ inline void failTask(const AccContext& acc, unsigned code = 1)
+{
+    if (std::uint32_t* s = acc.failSlot())
+        *reinterpret_cast<volatile std::uint32_t*>(s) = code ? code : 1u;
+}
+
 __device__ inline double atomicAdd(const AccContext&, double& cell, double operand)
 {
     return ::atomicAdd(&cell, operand);
@@ -129,7 +142,8 @@ struct SharedBytesOf<Kernel, std::void_t<decltype(Kernel::sharedMemBytes)>> {
 };
 
 template <class Kernel, class... Args>
-__global__ void functorKernel(kw_workdiv wd, std::size_t sharedBytes, Kernel kernel, Args... args)
+__global__ void functorKernel(kw_workdiv wd, std::size_t sharedBytes, std::uint32_t* failSlot, Kernel kernel,
+                              Args... args)
 {
     extern __shared__ __align__(16) std::byte kwSharedArena[];
     // Last work-division component = CUDA x (index_vec.hpp:15-24 axis rule). Built from
@@ -142,7 +156,7 @@ __global__ void functorKernel(kw_workdiv wd, std::size_t sharedBytes, Kernel ker
     const IndexVec tIdx = d == 1 ? IndexVec(threadIdx.x)
                           : d == 2 ? IndexVec(threadIdx.y, threadIdx.x)
                                    : IndexVec(threadIdx.z, threadIdx.y, threadIdx.x);
-    const AccContext acc(wd, bIdx, tIdx, kwSharedArena, sharedBytes);
+    const AccContext acc(wd, bIdx, tIdx, kwSharedArena, sharedBytes, failSlot);
     kernel(acc, args...);
 }
 
@@ -184,6 +198,10 @@ struct DeviceLauncher {
             st = kw_queue_device(q, &dev);
         if (st != KW_OK)
             return st;
+        std::uint32_t* failSlot = nullptr;
+        st = kw_queue_fail_slot(q, "device functor", &failSlot);
+        if (st != KW_OK)
+            return st;
         int prev = 0;
         cudaGetDevice(&prev);
         cudaSetDevice(dev);
@@ -193,7 +211,7 @@ struct DeviceLauncher {
             cudaFuncSetAttribute(functorKernel<Kernel, Args...>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem));
         functorKernel<Kernel, Args...><<<toDim3(w.blocks, w.dim), toDim3(w.threads, w.dim), smem,
-                                         static_cast<cudaStream_t>(stream)>>>(w, smem, kernel, args...);
+                                         static_cast<cudaStream_t>(stream)>>>(w, smem, failSlot, kernel, args...);
         const int err = static_cast<int>(cudaGetLastError());
         st = kw_queue_complete_launch(q, err, "device functor");
         cudaSetDevice(prev);

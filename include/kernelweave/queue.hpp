@@ -35,7 +35,9 @@ public:
     }
     std::exception_ptr error() const
     {
-        return state() == TaskState::Failed ? std::make_exception_ptr(TaskError(1, m_message)) : nullptr;
+        return state() == TaskState::Failed
+                   ? std::make_exception_ptr(TaskError(1, m_message.empty() ? "task failed on the device" : m_message))
+                   : nullptr;
     }
 
 private:

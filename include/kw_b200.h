@@ -119,6 +119,14 @@ KW_EXPORT kw_status kw_queue_shutdown(kw_queue q);
  * Sync queue completes the task before returning. */
 KW_EXPORT kw_status kw_queue_complete_launch(kw_queue q, int cuda_error, const char* what);
 
+/* Device-side task failure (the GPU form of "a kernel exception fails the task; later tasks
+ * still run", queue.hpp:86-93 / accel.cpp:240-248): returns a zeroed 32-bit slot the NEXT launch
+ * on q may set to a non-zero code from device code (kernelweave::failTask). The slot is
+ * resolved when q's stream has drained (kw_queue_wait, or inside the enqueue of a Sync queue):
+ * a non-zero code counts as one failed task, reported as `what: ... (code N)`. The next
+ * kw_event_record on q attaches the slot to its event, whose state is then FAILED. */
+KW_EXPORT kw_status kw_queue_fail_slot(kw_queue q, const char* what, uint32_t** slot);
+
 /* TaskHandle (queue.hpp:36-52) as a CUDA event recorded after the last enqueued task. State is
  * PENDING until the event completes, then DONE (FAILED on a device fault). A task's own launch
  * failure is the KW_TASK returned by its kw_* call (the C++/Python handles carry it). */

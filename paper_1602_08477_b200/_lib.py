@@ -52,6 +52,7 @@ SIGNATURES = {
     "kw_queue_stream": (st, [vp, C.POINTER(vp)]),
     "kw_queue_shutdown": (st, [vp]),
     "kw_queue_complete_launch": (st, [vp, C.c_int, C.c_char_p]),
+    "kw_queue_fail_slot": (st, [vp, C.c_char_p, C.POINTER(C.POINTER(C.c_uint32))]),
     "kw_event_record": (st, [vp, C.POINTER(vp)]),
     "kw_event_state": (st, [vp, C.POINTER(C.c_int)]),
     "kw_event_destroy": (st, [vp]),

@@ -9,8 +9,10 @@
 
 #include <atomic>
 #include <cstdio>
+#include <memory>
 #include <mutex>
 #include <string>
+#include <vector>
 
 namespace kw {
 
@@ -20,6 +22,20 @@ const std::string& last_error();
 
 // Number of kernels launched by this library (the bench's gpu_launches claim).
 extern std::atomic<uint64_t> g_launches;
+
+// A device-side failure slot of one launch (kw_queue_fail_slot): mapped pinned memory the
+// kernel may write; resolved (copied to `code`, slot recycled) once the queue's stream drained.
+struct FailSlot {
+    std::mutex mu;
+    uint32_t* slot = nullptr; // nullptr once resolved
+    uint32_t code = 0;
+    std::string what;
+    uint32_t read()
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        return slot ? *reinterpret_cast<volatile uint32_t*>(slot) : code;
+    }
+};
 
 struct Queue {
     int device = 0;
@@ -51,6 +67,10 @@ struct Queue {
     size_t order_bytes = 0;
     size_t order_key[8] = {};
     cudaEvent_t ev_order = nullptr;
+    // Device-side failure slots of launches not yet resolved (guarded by mu), and the slot the
+    // next kw_event_record attaches to its event.
+    std::vector<std::shared_ptr<FailSlot>> pending_slots;
+    std::shared_ptr<FailSlot> last_slot;
 };
 
 // RAII device selector: the reference's queues are bound to one device; every entry point
@@ -82,6 +102,10 @@ kw_status task_fail(Queue* q, const std::string& msg);
 // After enqueuing one task: surfaces launch errors into the queue's failure list and, for a
 // Sync queue, completes the task before returning (queue.cpp:21-23, 57-72).
 kw_status after_enqueue(Queue* q, const char* what);
+
+// Reads, counts (if `count_failures`) and recycles q's pending device-side failure slots; the
+// caller guarantees q->stream has drained.
+kw_status resolve_slots(Queue* q, bool count_failures);
 
 // Ensures q->scratch holds at least `bytes` of device memory on q's device.
 kw_status ensure_scratch(Queue* q, size_t bytes);

@@ -49,6 +49,62 @@ kw_status task_fail(Queue* q, const std::string& msg)
     return KW_TASK;
 }
 
+namespace {
+std::mutex g_slot_mu;
+std::vector<uint32_t*> g_free_slots; // mapped pinned pages carved into 32-bit slots
+
+uint32_t* slot_alloc()
+{
+    std::lock_guard<std::mutex> lock(g_slot_mu);
+    if (g_free_slots.empty()) {
+        constexpr size_t kSlots = 4096;
+        void* page = nullptr;
+        if (cudaHostAlloc(&page, kSlots * sizeof(uint32_t), cudaHostAllocMapped | cudaHostAllocPortable) !=
+            cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        for (size_t i = 0; i < kSlots; ++i)
+            g_free_slots.push_back(static_cast<uint32_t*>(page) + i);
+    }
+    uint32_t* s = g_free_slots.back();
+    g_free_slots.pop_back();
+    *reinterpret_cast<volatile uint32_t*>(s) = 0;
+    return s;
+}
+
+void slot_release(uint32_t* s)
+{
+    std::lock_guard<std::mutex> lock(g_slot_mu);
+    g_free_slots.push_back(s);
+}
+} // namespace
+
+// Called once q->stream has drained: every pending device-side failure slot is read, counted
+// as a failed task if set, and recycled.
+kw_status resolve_slots(Queue* q, bool count_failures)
+{
+    std::vector<std::shared_ptr<FailSlot>> done;
+    {
+        std::lock_guard<std::mutex> lock(q->mu);
+        done.swap(q->pending_slots);
+    }
+    kw_status st = KW_OK;
+    for (auto& fs : done) {
+        uint32_t code = 0;
+        {
+            std::lock_guard<std::mutex> lock(fs->mu);
+            code = *reinterpret_cast<volatile uint32_t*>(fs->slot);
+            fs->code = code;
+            slot_release(fs->slot);
+            fs->slot = nullptr;
+        }
+        if (code != 0 && count_failures)
+            st = task_fail(q, fs->what + ": device functor reported failure (code " + std::to_string(code) + ")");
+    }
+    return st;
+}
+
 kw_status after_enqueue(Queue* q, const char* what)
 {
     cudaError_t e = cudaGetLastError();
@@ -58,6 +114,7 @@ kw_status after_enqueue(Queue* q, const char* what)
         e = cudaStreamSynchronize(q->stream);
         if (e != cudaSuccess)
             return task_fail(q, std::string(what) + ": " + cudaGetErrorString(e));
+        return resolve_slots(q, true);
     }
     return KW_OK;
 }
@@ -114,6 +171,7 @@ struct kw_event_s {
     int device;
     cudaEvent_t ev;
     Queue* q;
+    std::shared_ptr<kw::FailSlot> slot; // device-side failure slot of the task, if any
 };
 
 extern "C" {
@@ -321,6 +379,7 @@ kw_status kw_queue_destroy(kw_queue qh)
     for (cudaEvent_t e : q->ev_bp)
         if (e)
             cudaEventDestroy(e);
+    kw::resolve_slots(q, false);
     if (q->ev_order)
         cudaEventDestroy(q->ev_order);
     if (q->order_host)
@@ -345,6 +404,8 @@ kw_status kw_queue_wait(kw_queue qh)
     cudaError_t e = cudaStreamSynchronize(q->stream);
     if (e != cudaSuccess)
         kw::task_fail(q, std::string("stream: ") + cudaGetErrorString(e));
+    else
+        kw::resolve_slots(q, true);
     std::lock_guard<std::mutex> lock(q->mu);
     if (q->failed == 0)
         return KW_OK;
@@ -407,6 +468,25 @@ kw_status kw_queue_complete_launch(kw_queue qh, int cuda_error, const char* what
     return kw::after_enqueue(q, w.c_str());
 }
 
+kw_status kw_queue_fail_slot(kw_queue qh, const char* what, uint32_t** slot)
+{
+    if (!qh || !slot)
+        return kw::usage("kw_queue_fail_slot: null argument");
+    auto* q = reinterpret_cast<Queue*>(qh);
+    auto fs = std::make_shared<kw::FailSlot>();
+    fs->slot = kw::slot_alloc();
+    if (!fs->slot)
+        return kw::resource("kw_queue_fail_slot: mapped pinned allocation failed");
+    fs->what = what ? what : "kernel";
+    {
+        std::lock_guard<std::mutex> lock(q->mu);
+        q->pending_slots.push_back(fs);
+        q->last_slot = fs;
+    }
+    *slot = fs->slot; // mapped + UVA: the host address is the device address
+    return KW_OK;
+}
+
 // ---- task events --------------------------------------------------------------------------
 
 kw_status kw_event_record(kw_queue qh, kw_event* out)
@@ -417,7 +497,12 @@ kw_status kw_event_record(kw_queue qh, kw_event* out)
         return kw::usage("kw_event_record: null output");
     auto* q = reinterpret_cast<Queue*>(qh);
     kw::DeviceGuard g(q->device);
-    auto* ev = new kw_event_s{q->device, nullptr, q};
+    auto* ev = new kw_event_s{q->device, nullptr, q, nullptr};
+    {
+        std::lock_guard<std::mutex> lock(q->mu);
+        ev->slot = std::move(q->last_slot);
+        q->last_slot.reset();
+    }
     cudaError_t e = cudaEventCreate(&ev->ev);
     if (e == cudaSuccess)
         e = cudaEventRecord(ev->ev, q->stream);
@@ -441,8 +526,13 @@ kw_status kw_event_state(kw_event ev, int* state)
         return KW_OK;
     }
     // A task's own launch failure is returned synchronously by its kw_* call (and collected for
-    // kw_queue_wait); the event reports completion, or a device fault (sticky, context-wide).
-    *state = e == cudaSuccess ? KW_TASK_DONE : KW_TASK_FAILED;
+    // kw_queue_wait); the event reports completion, a device-side failure its functor recorded
+    // (kw_queue_fail_slot), or a device fault (sticky, context-wide).
+    if (e != cudaSuccess) {
+        *state = KW_TASK_FAILED;
+        return KW_OK;
+    }
+    *state = ev->slot && ev->slot->read() != 0 ? KW_TASK_FAILED : KW_TASK_DONE;
     return KW_OK;
 }
 

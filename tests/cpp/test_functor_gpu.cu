@@ -115,6 +115,213 @@ struct TooMuchSharedKernel {
 };
 KW_DEVICE_FUNCTOR(TooMuchSharedKernel)
 
+// test_accel.cpp:403-430: the functor "throws" in block 3 — on the GPU, failTask + return.
+struct FailKernel {
+    __device__ void operator()(const AccContext& acc, unsigned code) const
+    {
+        const IndexVec b = idx::getIdx<Grid, Blocks>(acc);
+        if (b.get(0) == 3) {
+            failTask(acc, code);
+            return;
+        }
+    }
+};
+KW_DEVICE_FUNCTOR(FailKernel)
+
+// test_accel.cpp:111-127 / 365-401: int64, f64 and u64 atomics from a 256 x 16 grid.
+struct IncKernel {
+    __device__ void operator()(const AccContext& acc, BufferView cells) const
+    {
+        atomicAdd(acc, cells.rowData<std::int64_t>(0)[0], std::int64_t{1});
+        atomicAdd(acc, cells.rowData<double>(0)[1], 0.5);
+        atomicAdd(acc, cells.rowData<std::uint64_t>(0)[2], std::uint64_t{2});
+    }
+};
+KW_DEVICE_FUNCTOR(IncKernel)
+
+// Adding zero returns the old value and leaves the cell unchanged (test_accel.cpp:389-400).
+struct ZeroAddKernel {
+    __device__ void operator()(const AccContext& acc, BufferView cell, BufferView old) const
+    {
+        old.rowData<double>(0)[0] = atomicAdd(acc, cell.rowData<double>(0)[0], 0.0);
+    }
+};
+KW_DEVICE_FUNCTOR(ZeroAddKernel)
+
+// test_accel.cpp:151-170: two successive allocations are zeroed and disjoint.
+struct TwoAllocKernel {
+    __device__ void operator()(const AccContext& acc, BufferView out) const
+    {
+        double* first = allocSharedMem<double>(acc, 16);
+        double* second = allocSharedMem<double>(acc, 16);
+        bool zeroed = true;
+        for (int i = 0; i < 16; ++i)
+            zeroed = zeroed && first[i] == 0.0 && second[i] == 0.0;
+        const bool disjoint = (first + 16 <= second) || (second + 16 <= first);
+        const std::size_t b = idx::getIdx<Grid, Blocks>(acc).get(0);
+        const std::size_t t = idx::getIdx<Block, Threads>(acc).get(0);
+        out.rowData<std::int64_t>(0)[2 * (b * 32 + t)] = zeroed ? 1 : 0;
+        out.rowData<std::int64_t>(0)[2 * (b * 32 + t) + 1] = disjoint ? 1 : 0;
+    }
+};
+KW_DEVICE_FUNCTOR(TwoAllocKernel)
+
+// test_accel.cpp:172-196 + 198-244: thread 0 writes a block-unique token, the barrier publishes
+// it to every thread of the block, and no other (concurrently resident) block disturbs it.
+struct AliasKernel {
+    static constexpr std::size_t sharedMemBytes = 1024;
+    __device__ void operator()(const AccContext& acc, BufferView out) const
+    {
+        double* shared = allocSharedMem<double>(acc, 64);
+        const std::size_t b = idx::getIdx<Grid, Blocks>(acc).get(0);
+        const std::size_t t = idx::getIdx<Block, Threads>(acc).get(0);
+        if (t == 0)
+            for (int i = 0; i < 64; ++i)
+                shared[i] = static_cast<double>(b * 64 + i);
+        syncBlockThreads(acc);
+        double sink = 0.0;
+        for (int spin = 0; spin < 2000; ++spin)
+            sink += shared[spin % 64];
+        bool intact = sink >= 0.0;
+        for (int i = 0; i < 64; ++i)
+            intact = intact && shared[i] == static_cast<double>(b * 64 + i);
+        out.rowData<std::int64_t>(0)[b * 8 + t] = intact ? 1 : 0;
+    }
+};
+KW_DEVICE_FUNCTOR(AliasKernel)
+
+// test_accel.cpp:300-341: staged power-of-two tree reduction, one barrier per stage.
+struct TreeReduceKernel {
+    __device__ void operator()(const AccContext& acc, BufferView in, BufferView out, std::size_t n) const
+    {
+        const std::size_t threads = getWorkDiv(acc, Level::Block, Unit::Threads).get(0);
+        const std::size_t t = getIdx(acc, Level::Block, Unit::Threads).get(0);
+        std::int64_t* partial = allocSharedMem<std::int64_t>(acc, threads);
+        const std::int64_t* data = in.rowData<std::int64_t>(0);
+        std::int64_t local = 0;
+        for (std::size_t i = t; i < n; i += threads)
+            local += data[i];
+        partial[t] = local;
+        syncBlockThreads(acc);
+        for (std::size_t stride = threads / 2; stride > 0; stride /= 2) {
+            if (t < stride)
+                partial[t] += partial[t + stride];
+            syncBlockThreads(acc);
+        }
+        if (t == 0)
+            out.rowData<std::int64_t>(0)[0] = partial[0];
+    }
+};
+KW_DEVICE_FUNCTOR(TreeReduceKernel)
+
+struct EmptyKernel {
+    __device__ void operator()(const AccContext&) const {}
+};
+KW_DEVICE_FUNCTOR(EmptyKernel)
+
+TEST_CASE("kernel failure fails the task; later tasks still run (test_accel.cpp:403-430, queue.hpp:86-93)")
+{
+    // executeTask (synchronous) surfaces it as TaskError
+    bool threw = false;
+    try {
+        executeTask(kBk, WorkDiv(IndexVec(8), IndexVec(32), IndexVec(1)), FailKernel{}, 7u);
+    }
+    catch (const TaskError& e) {
+        threw = e.failedCount() == 1 && std::string(e.what()).find("code 7") != std::string::npos;
+    }
+    CHECK(threw);
+    // Async: two failing tasks around a good one; handles, count, and a clean second wait
+    Buffer counts = upload(std::vector<std::uint64_t>(64, 0));
+    Queue q(kGpu, QueueFlavor::Async);
+    TaskHandle bad1 = q.enqueue(createExec(kBk, WorkDiv(IndexVec(4), IndexVec(16), IndexVec(1)), FailKernel{}, 3u));
+    TaskHandle good = q.enqueue(createExec(kBk, WorkDiv(IndexVec(1), IndexVec(64), IndexVec(1)), MarkKernel{},
+                                           view(counts)));
+    TaskHandle bad2 = q.enqueue(createExec(kBk, WorkDiv(IndexVec(4), IndexVec(16), IndexVec(1)), FailKernel{}, 5u));
+    std::size_t failed = 0;
+    try {
+        q.wait();
+    }
+    catch (const TaskError& e) {
+        failed = e.failedCount();
+    }
+    CHECK(failed == 2);
+    CHECK(bad1.state() == TaskState::Failed);
+    CHECK(bad1.error() != nullptr);
+    CHECK(bad2.state() == TaskState::Failed);
+    CHECK(good.state() == TaskState::Done);
+    const auto got = download<std::uint64_t>(counts, 64);
+    bool ok = true;
+    for (auto v : got)
+        ok = ok && v == 1;
+    CHECK(ok);
+    q.wait();
+    // a task without the failing block succeeds
+    TaskHandle fine = q.enqueue(createExec(kBk, WorkDiv(IndexVec(3), IndexVec(16), IndexVec(1)), FailKernel{}, 9u));
+    q.wait();
+    CHECK(fine.state() == TaskState::Done);
+}
+
+TEST_CASE("a 256x16 grid performs 4096 invocations; atomics int64/f64/u64 (test_accel.cpp:111-127, 365-401)")
+{
+    Buffer cells = upload(std::vector<std::uint64_t>(3, 0));
+    executeTask(kBk, WorkDiv(IndexVec(256), IndexVec(16), IndexVec(1)), IncKernel{}, view(cells));
+    const auto got = download<std::uint64_t>(cells, 3);
+    double f = 0.0;
+    std::memcpy(&f, &got[1], 8);
+    CHECK(got[0] == 4096);
+    CHECK(f == 2048.0);
+    CHECK(got[2] == 8192);
+    Buffer cell = upload(std::vector<double>{123.5});
+    Buffer old = upload(std::vector<double>{0.0});
+    executeTask(kBk, WorkDiv(IndexVec(1), IndexVec(1), IndexVec(1)), ZeroAddKernel{}, view(cell), view(old));
+    CHECK(download<double>(cell, 1)[0] == 123.5);
+    CHECK(download<double>(old, 1)[0] == 123.5);
+}
+
+TEST_CASE("empty kernel completes without effect (test_accel.cpp:101-109)")
+{
+    executeTask(kBk, WorkDiv(IndexVec(2, 2), IndexVec(1, 2), IndexVec(1, 1)), EmptyKernel{});
+    CHECK(true);
+}
+
+TEST_CASE("shared memory: successive allocations zeroed and disjoint; blocks never alias (test_accel.cpp:151-244)")
+{
+    Buffer out = upload(std::vector<std::int64_t>(2 * 4 * 32, 0));
+    executeTask(kBk, WorkDiv(IndexVec(4), IndexVec(32), IndexVec(1)), TwoAllocKernel{}, view(out));
+    bool ok = true;
+    for (auto v : download<std::int64_t>(out, 2 * 4 * 32))
+        ok = ok && v == 1;
+    CHECK(ok);
+    const std::size_t blocks = 592; // four resident waves' worth on 148 SMs
+    Buffer alias = upload(std::vector<std::int64_t>(blocks * 8, 0));
+    executeTask(kBk, WorkDiv(IndexVec(blocks), IndexVec(8), IndexVec(1)), AliasKernel{}, view(alias));
+    ok = true;
+    for (auto v : download<std::int64_t>(alias, blocks * 8))
+        ok = ok && v == 1;
+    CHECK(ok);
+}
+
+TEST_CASE("staged shared-memory reduction matches the sequential sum (test_accel.cpp:322-341)")
+{
+    std::mt19937_64 rng(314);
+    for (std::size_t threads : {2u, 4u, 8u, 16u, 256u, 1024u}) {
+        for (int iter = 0; iter < 5; ++iter) {
+            const std::size_t n = 1 + rng() % (1u << 14);
+            std::vector<std::int64_t> v(n);
+            std::int64_t expected = 0;
+            for (auto& e : v) {
+                e = static_cast<std::int64_t>(rng() % 1000) - 500;
+                expected += e;
+            }
+            Buffer in = upload(v);
+            Buffer out = upload(std::vector<std::int64_t>{0});
+            executeTask(kBk, WorkDiv(IndexVec(1), IndexVec(threads), IndexVec(1)), TreeReduceKernel{}, view(in),
+                        view(out), n);
+            CHECK(download<std::int64_t>(out, 1)[0] == expected);
+        }
+    }
+}
+
 TEST_CASE("failed tasks are collected, later tasks still run, wait() reports TaskError (queue.hpp:86-93)")
 {
     Buffer counts = upload(std::vector<std::uint64_t>(64, 0));
