@@ -74,3 +74,21 @@ def test_kwbench_gpu_csv_and_verification(programs, tmp_path):
     p = subprocess.run([exe, "--kernel", "axpy", "--sizes", "1000", "--reps", "3", "--verify"], capture_output=True,
                        text=True, timeout=120, env=env)
     assert p.returncode == 1, p.stdout
+
+
+@pytest.mark.gpu
+def test_criterion10_pessimization_analogue(programs, tmp_path):
+    """acceptance.cpp:616-650 on the GPU: kwbench --pessimize runs gemm-tiled at n = 512 both
+    tuned and degraded (the naive one-thread kernel in place of the tiled one); the degraded
+    median must be at least 2x slower."""
+    import csv
+    import statistics
+    out = tmp_path / "p.csv"
+    p = subprocess.run([str(programs["kwbench"]), "--kernel", "gemm-tiled", "--sizes", "512", "--tile", "128",
+                        "--reps", "3", "--pessimize", "--csv", str(out)], capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, (p.stdout, p.stderr)
+    recs = list(csv.DictReader(out.open()))
+    tuned = [float(r["seconds"]) for r in recs if r["tile"] == "128"]
+    degraded = [float(r["seconds"]) for r in recs if r["tile"] == "1"]
+    assert tuned and degraded
+    assert statistics.median(degraded) / statistics.median(tuned) >= 2.0

@@ -263,11 +263,16 @@ Point runGemm(const Config& c, std::size_t n, Queue& q, bool pessimized)
                 ref.rowData<double>(r)[col] = alpha * acc[col] + beta * hc.rowData<double>(r)[col];
         }
     }
-    const bool tiled = c.kernel == "gemm-tiled";
-    const std::size_t tile = pessimized ? 64 : c.tile;
+    // --pessimize (runner.cpp:148-153, acceptance crit. 10): gemm-naive degrades to one thread
+    // owning the whole output; gemm-tiled degrades to "tile = 1" — each thread one output
+    // element, no shared-memory reuse (the untiled kernel) — recorded with tile 1 like the
+    // reference's degraded rows.
+    const bool tiled = c.kernel == "gemm-tiled" && !pessimized;
+    const std::size_t tile = pessimized ? 1 : c.tile;
     const WorkDiv wd = tiled ? gemmTiledWorkDiv(BackendKind::GpuCudaRt, n, n, tile)
-                       : pessimized ? WorkDiv(IndexVec(1, 1), IndexVec(1, 1), IndexVec(n, n)) // one thread owns all
-                                    : gemmNaiveWorkDiv(BackendKind::GpuCudaRt, n, n, c.tpb, c.ept);
+                       : !pessimized ? gemmNaiveWorkDiv(BackendKind::GpuCudaRt, n, n, c.tpb, c.ept)
+                       : c.kernel == "gemm-tiled" ? gemmNaiveWorkDiv(BackendKind::GpuCudaRt, n, n, 16, 1)
+                                                  : WorkDiv(IndexVec(1, 1), IndexVec(1, 1), IndexVec(n, n));
     const GemmArgs args{n, n, n, alpha, beta, &a, &b, &cc, tile};
     Point pt;
     for (int rep = -1; rep < c.reps; ++rep) {
@@ -303,7 +308,7 @@ Point runGemm(const Config& c, std::size_t n, Queue& q, bool pessimized)
         }
         pt.failed |= !ok;
         pt.records.push_back({c.kernel, "gpu", n, wd.threadsPerBlock().product(), wd.elementsPerThread().product(),
-                              tiled ? tile : 0, rep, s, flopCount(c.kernel, n) / s / 1e9, ok});
+                              c.kernel == "gemm-tiled" ? tile : 0, rep, s, flopCount(c.kernel, n) / s / 1e9, ok});
     }
     return pt;
 }
