@@ -146,18 +146,25 @@ __global__ void functorKernel(kw_workdiv wd, std::size_t sharedBytes, std::uint3
                               Args... args)
 {
     extern __shared__ __align__(16) std::byte kwSharedArena[];
-    // Last work-division component = CUDA x (index_vec.hpp:15-24 axis rule). Built from
-    // scalars: local index arrays here were once assigned one stack slot by nvcc 12.9 (the block
-    // index read back as the thread index) — keep this path array-free.
+    // One CUDA block walks logical blocks lb = blockIdx.x, +gridDim.x, ... (the grid is sized to
+    // what is resident, so huge divisions cost no block-scheduling overhead and are not bound by
+    // CUDA's grid limits). Last work-division component = fastest (index_vec.hpp:15-24). Built
+    // from scalars: local index arrays here were once assigned one stack slot by nvcc 12.9 (the
+    // block index read back as the thread index) — keep this path array-free.
     const unsigned d = wd.dim;
-    const IndexVec bIdx = d == 1 ? IndexVec(blockIdx.x)
-                          : d == 2 ? IndexVec(blockIdx.y, blockIdx.x)
-                                   : IndexVec(blockIdx.z, blockIdx.y, blockIdx.x);
     const IndexVec tIdx = d == 1 ? IndexVec(threadIdx.x)
                           : d == 2 ? IndexVec(threadIdx.y, threadIdx.x)
                                    : IndexVec(threadIdx.z, threadIdx.y, threadIdx.x);
-    const AccContext acc(wd, bIdx, tIdx, kwSharedArena, sharedBytes, failSlot);
-    kernel(acc, args...);
+    const std::size_t bLast = wd.blocks[d - 1], bMid = d >= 2 ? wd.blocks[d - 2] : 1;
+    const std::size_t nb = bLast * bMid * (d == 3 ? wd.blocks[0] : 1);
+    for (std::size_t lb = blockIdx.x; lb < nb; lb += gridDim.x) {
+        const std::size_t c = lb % bLast, r = lb / bLast;
+        const IndexVec bIdx = d == 1 ? IndexVec(c) : d == 2 ? IndexVec(r, c) : IndexVec(r / bMid, r % bMid, c);
+        const AccContext acc(wd, bIdx, tIdx, kwSharedArena, sharedBytes, failSlot);
+        kernel(acc, args...);
+        if (lb + gridDim.x < nb)
+            __syncthreads(); // the next logical block reuses the shared arena
+    }
 }
 
 template <class T>
@@ -182,10 +189,6 @@ struct DeviceLauncher {
             threads *= w.threads[k];
         if (threads > 1024)
             throw UsageError("device functor: threadsPerBlock exceeds the sm_100a block limit of 1024");
-        const std::size_t maxGrid[3] = {65535, 65535, 2147483647};
-        for (std::uint32_t k = 0; k < w.dim; ++k)
-            if (w.blocks[k] > maxGrid[3 - w.dim + k])
-                throw UsageError("device functor: blocksPerGrid exceeds the grid limits");
         if (w.elems[0] * w.elems[1] * w.elems[2] == 0)
             throw UsageError("WorkDiv: every level extent is at least 1");
     }
@@ -210,8 +213,35 @@ struct DeviceLauncher {
         if (smem > 48 * 1024)
             cudaFuncSetAttribute(functorKernel<Kernel, Args...>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem));
-        functorKernel<Kernel, Args...><<<toDim3(w.blocks, w.dim), toDim3(w.threads, w.dim), smem,
-                                         static_cast<cudaStream_t>(stream)>>>(w, smem, failSlot, kernel, args...);
+        // Resident grid: occupancy x SMs CUDA blocks, each walking logical blocks.
+        std::size_t nb = 1;
+        for (std::uint32_t k = 0; k < w.dim; ++k)
+            nb *= w.blocks[k];
+        const dim3 block = toDim3(w.threads, w.dim);
+        int perSm = 0, sms = 0;
+        const int threads = static_cast<int>(block.x * block.y * block.z);
+        static thread_local int cachedThreads = -1, cachedDev = -1, cachedPerSm = 0, cachedSms = 0;
+        if (cachedThreads == threads && cachedDev == dev) {
+            perSm = cachedPerSm;
+            sms = cachedSms;
+        }
+        else if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perSm, functorKernel<Kernel, Args...>, threads, smem) ==
+                     cudaSuccess &&
+                 cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess) {
+            cachedThreads = threads;
+            cachedDev = dev;
+            cachedPerSm = perSm;
+            cachedSms = sms;
+        }
+        else {
+            cudaGetLastError();
+            perSm = 1;
+            sms = 1;
+        }
+        const std::size_t resident = static_cast<std::size_t>(perSm > 0 ? perSm : 1) * static_cast<std::size_t>(sms);
+        const unsigned grid = static_cast<unsigned>(nb < resident ? nb : resident);
+        functorKernel<Kernel, Args...><<<grid, block, smem, static_cast<cudaStream_t>(stream)>>>(w, smem, failSlot,
+                                                                                                kernel, args...);
         const int err = static_cast<int>(cudaGetLastError());
         st = kw_queue_complete_launch(q, err, "device functor");
         cudaSetDevice(prev);
