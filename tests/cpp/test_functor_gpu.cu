@@ -481,18 +481,14 @@ TEST_CASE("criterion 08 analogue: a generic functor runs within 1.5x of the nati
         executeTask(kBk, kernels::axpyWorkDiv(kBk, n, 512, 2), kernels::AxpyKernel{},
                     kernels::AxpyArgs{n, 0.5, &x, &y});
     });
-    // ept 2 is the tuned division for this functor: it keeps the reference's per-thread
-    // contiguous chunk [t*V, t*V+V), so lanes stride by V — measured ept 1/2/4/8: 0.50 / 0.34 /
-    // 0.68 / 1.94 ms (1 = block-scheduling bound, >= 4 = uncoalesced).
-    double functor = 1e30;
-    for (std::size_t ept : {1u, 2u}) {
-        const double t = median_ms([&] {
-            executeTask(kBk, divideForBackend(IndexVec(n), kBk, IndexVec(256), IndexVec(ept)), ScaleKernel{}, n, 0.5,
-                        view(x), view(y));
-        });
-        std::printf("  generic functor, %zu element(s) per thread: %.3f ms\n", ept, t);
-        functor = std::min(functor, t);
-    }
+    // Tuned division for this functor (it keeps the reference's per-thread contiguous chunk
+    // [t*V, t*V+V), so lanes stride by V): 1024 threads x 2 elements. Measured (ms) for
+    // tpb 128/256/512/1024 x V 1/2/3: 0.82/0.51/0.45, 0.50/0.35/0.34, 0.36/0.31/0.36,
+    // 0.39/0.29/0.30 — native 0.25.
+    const double functor = median_ms([&] {
+        executeTask(kBk, divideForBackend(IndexVec(n), kBk, IndexVec(1024), IndexVec(2)), ScaleKernel{}, n, 0.5,
+                    view(x), view(y));
+    });
     std::printf("  axpy 2^26 f64: native %.3f ms, generic functor %.3f ms (%.2fx, bound 1.5x)\n", native, functor,
                 functor / native);
     CHECK(functor <= 1.5 * native);
