@@ -148,7 +148,11 @@ kw_status kw_comm_init(kw_comm* out, int device, int world, int rank, const unsi
         delete c;
         return nccl_fail("ncclCommInitRank", r);
     }
-    cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    // Highest priority: the broadcast kernels get SMs ahead of the queued GEMM CTAs, so panel
+    // j+1 lands while panel j computes.
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaError_t e = cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, hi);
     if (e == cudaSuccess)
         e = cudaEventCreateWithFlags(&c->start, cudaEventDisableTiming);
     if (e != cudaSuccess) {
@@ -227,6 +231,12 @@ kw_status kw_dgemm_rowsharded(kw_comm c, kw_queue qh, size_t m_local, size_t n, 
     cudaError_t e = cudaEventRecord(c->start, q->stream); // B and C may come from earlier tasks
     if (e == cudaSuccess)
         e = cudaStreamWaitEvent(c->stream, c->start, 0);
+    // Panel launches alternate between the queue stream and its aux stream: panel j+1's CTAs
+    // fill the SMs while panel j's last wave drains (disjoint C columns, same per-element
+    // arithmetic — bits unchanged). A panel launch ends in a partial wave otherwise: one rank's
+    // 2048..8192-row block lost 2-13 % (tools/rowshard_rank_probe.py).
+    if (e == cudaSuccess)
+        e = cudaStreamWaitEvent(q->aux, c->start, 0);
     ncclResult_t r = ncclSuccess;
     size_t off = 0;
     for (int j = 0; j < np && e == cudaSuccess && r == ncclSuccess; ++j) {
@@ -240,15 +250,20 @@ kw_status kw_dgemm_rowsharded(kw_comm c, kw_queue qh, size_t m_local, size_t n, 
         }
         if (e == cudaSuccess)
             e = cudaEventRecord(c->panel_ready[j], c->stream);
+        cudaStream_t cs = (j & 1) ? q->aux : q->stream;
         if (e == cudaSuccess)
-            e = cudaStreamWaitEvent(q->stream, c->panel_ready[j], 0);
+            e = cudaStreamWaitEvent(cs, c->panel_ready[j], 0);
         if (e == cudaSuccess && m_local > 0) {
-            st = kw::dgemm_device(q->stream, 128, m_local, wj, k, alpha, A, lda, panel, wj, beta, C + n0, ldc);
+            st = kw::dgemm_device(cs, 128, m_local, wj, k, alpha, A, lda, panel, wj, beta, C + n0, ldc);
             if (st != KW_OK)
                 return kw::task_fail(q, kw::last_error());
         }
         off += k * wj;
     }
+    if (e == cudaSuccess)
+        e = cudaEventRecord(q->ev_join, q->aux);
+    if (e == cudaSuccess)
+        e = cudaStreamWaitEvent(q->stream, q->ev_join, 0);
     if (r != ncclSuccess)
         return kw::task_fail(q, std::string("ncclBroadcast: ") + ncclGetErrorString(r));
     if (e != cudaSuccess)
