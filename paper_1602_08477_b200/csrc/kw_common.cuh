@@ -43,6 +43,7 @@ struct Queue {
     cudaStream_t stream = nullptr; // in-order FIFO of the queue
     cudaStream_t aux = nullptr;    // D2H stream of the host-staged paths
     cudaStream_t h2d = nullptr;    // H2D stream of the host-staged paths
+    cudaStream_t comp2 = nullptr;  // second compute stream (panel launches overlap their tails)
     std::mutex mu;       // failure bookkeeping
     std::mutex enqueue;  // serialises enqueues from several host threads (queue.hpp:89-93)
     size_t failed = 0;
@@ -56,6 +57,7 @@ struct Queue {
     cudaEvent_t ev_free[kRing] = {};   // chunk drained  -> slot reusable
     cudaEvent_t ev_h2d[kRing] = {};    // chunk uploaded -> compute may start
     cudaEvent_t ev_join = nullptr;
+    cudaEvent_t ev_join2 = nullptr;
     cudaEvent_t ev_start = nullptr;
     cudaEvent_t ev_b = nullptr;
     static constexpr int kBPanels = 8;

@@ -1178,6 +1178,8 @@ kw_status dgemm_staged(kw::Queue* q, int tile, size_t m, size_t n, size_t k, dou
     cudaError_t e = cudaEventRecord(q->ev_start, q->stream);
     if (e == cudaSuccess)
         e = cudaStreamWaitEvent(q->h2d, q->ev_start, 0);
+    if (e == cudaSuccess)
+        e = cudaStreamWaitEvent(q->comp2, q->ev_start, 0);
     // B streaming: B is uploaded in column panels into its dense device copy; the first row
     // panel is computed block by block as the B panels land, the remaining row panels (full
     // width) after the last one. Start latency = A_0 + C_0 + one B panel instead of all of B.
@@ -1200,6 +1202,9 @@ kw_status dgemm_staged(kw::Queue* q, int tile, size_t m, size_t n, size_t k, dou
     for (size_t pi = 0; pi < npanels && e == cudaSuccess; ++pi) {
         const int s = static_cast<int>(pi % ring);
         const size_t r0 = pi * R, rows = m - r0 < R ? m - r0 : R;
+        // Odd panels compute on the second stream: a panel launch is a fraction of a wave at
+        // these heights, so consecutive panels overlap instead of each ending in a tail.
+        cudaStream_t comp = (pi & 1) ? q->comp2 : q->stream;
         double* as = reinterpret_cast<double*>(slots + s * slot_bytes);
         double* cs = as + R * ldas;
         if (pi >= static_cast<size_t>(ring))
@@ -1224,7 +1229,7 @@ kw_status dgemm_staged(kw::Queue* q, int tile, size_t m, size_t n, size_t k, dou
         if (e == cudaSuccess && uploaded) {
             e = cudaEventRecord(q->ev_h2d[s], q->h2d);
             if (e == cudaSuccess)
-                e = cudaStreamWaitEvent(q->stream, q->ev_h2d[s], 0);
+                e = cudaStreamWaitEvent(comp, q->ev_h2d[s], 0);
         }
         if (e != cudaSuccess)
             break;
@@ -1248,13 +1253,19 @@ kw_status dgemm_staged(kw::Queue* q, int tile, size_t m, size_t n, size_t k, dou
             }
         }
         else {
-            st = launch_tiled(q->stream, tile, make_params(rows, n, k, alpha, Ad, ldad, Bd, ldbd, beta, Cd, ldcd));
+            if (stream_b && pi == 1) {
+                // the column-panel uploads of B were waited for on the first stream only
+                e = cudaStreamWaitEvent(comp, q->ev_bp[nbp - 1], 0);
+                if (e != cudaSuccess)
+                    break;
+            }
+            st = launch_tiled(comp, tile, make_params(rows, n, k, alpha, Ad, ldad, Bd, ldbd, beta, Cd, ldcd));
             if (st != KW_OK)
                 return st;
         }
         e = cudaGetLastError();
         if (e == cudaSuccess && !c_dev) {
-            e = cudaEventRecord(q->ev_ready[s], q->stream);
+            e = cudaEventRecord(q->ev_ready[s], comp);
             if (e == cudaSuccess)
                 e = cudaStreamWaitEvent(q->aux, q->ev_ready[s], 0);
             if (e == cudaSuccess)
@@ -1263,13 +1274,17 @@ kw_status dgemm_staged(kw::Queue* q, int tile, size_t m, size_t n, size_t k, dou
                 e = cudaEventRecord(q->ev_free[s], q->aux);
         }
         else if (e == cudaSuccess) {
-            e = cudaEventRecord(q->ev_free[s], q->stream);
+            e = cudaEventRecord(q->ev_free[s], comp);
         }
     }
     if (e == cudaSuccess) {
         e = cudaEventRecord(q->ev_join, q->aux);
         if (e == cudaSuccess)
             e = cudaStreamWaitEvent(q->stream, q->ev_join, 0);
+        if (e == cudaSuccess)
+            e = cudaEventRecord(q->ev_join2, q->comp2);
+        if (e == cudaSuccess)
+            e = cudaStreamWaitEvent(q->stream, q->ev_join2, 0);
     }
     if (e != cudaSuccess)
         return kw::task_fail(q, std::string("dgemm (host-staged): ") + cudaGetErrorString(e));

@@ -128,6 +128,7 @@ kw_status ensure_scratch(Queue* q, size_t bytes)
         cudaStreamSynchronize(q->stream);
         cudaStreamSynchronize(q->aux);
         cudaStreamSynchronize(q->h2d);
+        cudaStreamSynchronize(q->comp2);
         cudaFree(q->scratch);
         q->scratch = nullptr;
         q->scratch_bytes = 0;
@@ -332,6 +333,8 @@ kw_status kw_queue_create(int device, int flavor, kw_queue* out)
         e = cudaStreamCreateWithFlags(&q->aux, cudaStreamNonBlocking);
     if (e == cudaSuccess)
         e = cudaStreamCreateWithFlags(&q->h2d, cudaStreamNonBlocking);
+    if (e == cudaSuccess)
+        e = cudaStreamCreateWithFlags(&q->comp2, cudaStreamNonBlocking);
     for (int i = 0; e == cudaSuccess && i < Queue::kRing; ++i) {
         e = cudaEventCreateWithFlags(&q->ev_ready[i], cudaEventDisableTiming);
         if (e == cudaSuccess)
@@ -341,6 +344,8 @@ kw_status kw_queue_create(int device, int flavor, kw_queue* out)
     }
     if (e == cudaSuccess)
         e = cudaEventCreateWithFlags(&q->ev_join, cudaEventDisableTiming);
+    if (e == cudaSuccess)
+        e = cudaEventCreateWithFlags(&q->ev_join2, cudaEventDisableTiming);
     if (e == cudaSuccess)
         e = cudaEventCreateWithFlags(&q->ev_start, cudaEventDisableTiming);
     if (e == cudaSuccess)
@@ -373,7 +378,7 @@ kw_status kw_queue_destroy(kw_queue qh)
         if (q->ev_h2d[i])
             cudaEventDestroy(q->ev_h2d[i]);
     }
-    for (cudaEvent_t e : {q->ev_join, q->ev_start, q->ev_b})
+    for (cudaEvent_t e : {q->ev_join, q->ev_join2, q->ev_start, q->ev_b})
         if (e)
             cudaEventDestroy(e);
     for (cudaEvent_t e : q->ev_bp)
@@ -388,6 +393,8 @@ kw_status kw_queue_destroy(kw_queue qh)
         cudaFree(q->order_dev);
     if (q->scratch)
         cudaFree(q->scratch);
+    cudaStreamSynchronize(q->comp2);
+    cudaStreamDestroy(q->comp2);
     cudaStreamDestroy(q->h2d);
     cudaStreamDestroy(q->aux);
     cudaStreamDestroy(q->stream);
