@@ -50,6 +50,17 @@ __device__ __forceinline__ double2 axpyv(double a, double2 x, double2 y)
     return make_double2(axpy1(a, x.x, y.x), axpy1(a, x.y, y.y));
 }
 
+// Programmatic dependent launch (launch_pdl below): every CTA first lets the next grid on the
+// stream be admitted, then waits until the previous grid has completed and its writes are
+// visible — so back-to-back launches (an in-place Y updated step after step) overlap one grid's
+// launch latency with the previous grid's tail without ever reading a stale Y. Without the
+// launch attribute both instructions are no-ops.
+__device__ __forceinline__ void griddep_enter()
+{
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+}
+
 // Streaming loads/stores: X and Y are touched exactly once per launch.
 __device__ __forceinline__ float4 ld_stream(const float4* p) { return __ldcs(p); }
 __device__ __forceinline__ double2 ld_stream(const double2* p) { return __ldcs(p); }
@@ -61,6 +72,7 @@ template <typename T, int U>
 __global__ void __launch_bounds__(1024) axpy_vec_kernel(size_t limit, T alpha, const T* __restrict__ x,
                                                        T* __restrict__ y, uint32_t vecs_per_thread)
 {
+    griddep_enter();
     using V = typename Vec<T>::type;
     constexpr int W = Vec<T>::W;
     const size_t threads = blockDim.x;
@@ -146,6 +158,7 @@ template <typename T, int U>
 __global__ void __launch_bounds__(1024) axpy_v32_kernel(size_t limit, T alpha, const T* __restrict__ x,
                                                        T* __restrict__ y, uint32_t vecs_per_thread)
 {
+    griddep_enter();
     constexpr int W = V32<T>::W;
     const size_t threads = blockDim.x;
     const size_t block_elems = threads * vecs_per_thread * W;
@@ -198,6 +211,7 @@ template <typename T>
 __global__ void __launch_bounds__(1024) axpy_scalar_kernel(size_t limit, T alpha, const T* __restrict__ x,
                                                           T* __restrict__ y, uint32_t elems_per_thread)
 {
+    griddep_enter();
     const size_t threads = blockDim.x;
     const size_t base = static_cast<size_t>(blockIdx.x) * threads * elems_per_thread;
     for (uint32_t j = 0; j < elems_per_thread; ++j) {
@@ -230,6 +244,32 @@ kw_status validate_wd(const kw_workdiv* wd, size_t n, size_t& blocks, uint32_t& 
     return KW_OK;
 }
 
+// KW_PDL=0 disables programmatic dependent launch (A/B switch).
+bool pdl_policy()
+{
+    static const bool on = [] {
+        const char* e = std::getenv("KW_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+template <typename... Params, typename... Args>
+void launch_pdl(void (*kernel)(Params...), unsigned grid, unsigned threads, cudaStream_t s, Args... args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_policy() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kernel, static_cast<Params>(args)...);
+}
+
 template <typename T>
 void launch_device(cudaStream_t s, size_t blocks, uint32_t threads, uint32_t elems, size_t limit, T alpha,
                    const T* x, T* y)
@@ -247,21 +287,21 @@ void launch_device(cudaStream_t s, size_t blocks, uint32_t threads, uint32_t ele
     if (vector_bytes_policy() == 32 && aligned32 && elems % W32 == 0) {
         const uint32_t vpt = elems / W32;
         if (vpt >= 2)
-            axpy_v32_kernel<T, 2><<<grid, threads, 0, s>>>(limit, alpha, x, y, vpt);
+            launch_pdl(axpy_v32_kernel<T, 2>, grid, threads, s, limit, alpha, x, y, vpt);
         else
-            axpy_v32_kernel<T, 1><<<grid, threads, 0, s>>>(limit, alpha, x, y, vpt);
+            launch_pdl(axpy_v32_kernel<T, 1>, grid, threads, s, limit, alpha, x, y, vpt);
     }
     else if (aligned && elems % W == 0) {
         const uint32_t vpt = elems / W;
         if (vpt >= 4)
-            axpy_vec_kernel<T, 4><<<grid, threads, 0, s>>>(limit, alpha, x, y, vpt);
+            launch_pdl(axpy_vec_kernel<T, 4>, grid, threads, s, limit, alpha, x, y, vpt);
         else if (vpt >= 2)
-            axpy_vec_kernel<T, 2><<<grid, threads, 0, s>>>(limit, alpha, x, y, vpt);
+            launch_pdl(axpy_vec_kernel<T, 2>, grid, threads, s, limit, alpha, x, y, vpt);
         else
-            axpy_vec_kernel<T, 1><<<grid, threads, 0, s>>>(limit, alpha, x, y, vpt);
+            launch_pdl(axpy_vec_kernel<T, 1>, grid, threads, s, limit, alpha, x, y, vpt);
     }
     else {
-        axpy_scalar_kernel<T><<<grid, threads, 0, s>>>(limit, alpha, x, y, elems);
+        launch_pdl(axpy_scalar_kernel<T>, grid, threads, s, limit, alpha, x, y, elems);
     }
     kw::g_launches.fetch_add(1, std::memory_order_relaxed);
 }
