@@ -26,6 +26,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <atomic>
 #include <climits>
 #include <cstdlib>
 #include <cstring>
@@ -1394,6 +1395,9 @@ kw_status dgemm_streamed(kw::Queue* q, int tile, size_t m, size_t n, size_t k, d
     GemmParams p = make_params(m, n, k, alpha, Ad, ldas, Bd, ldbs, beta, Cd, ldcs);
     if (!tma_eligible(p))
         return KW_OK;
+    static std::atomic<int> mem_ops_ok{-1};
+    if (mem_ops_ok.load() == 0)
+        return KW_OK;
 
     // The growth order: A_0, B_0, then add a B column panel while it is not ahead of the A row
     // panels, else an A row panel; each addition completes the C blocks of its row/column.
@@ -1474,6 +1478,18 @@ kw_status dgemm_streamed(kw::Queue* q, int tile, size_t m, size_t n, size_t k, d
         e = cudaStreamWaitEvent(q->h2d, q->ev_start, 0);
     if (e != cudaSuccess)
         return kw::task_fail(q, std::string("dgemm (streamed): ") + cudaGetErrorString(e));
+    if (mem_ops_ok.load() < 0) {
+        // Once per process, ordered after the reset above: the stream memory operations must be
+        // accepted on this device (a write of the value the reset stored, a wait already
+        // satisfied); otherwise nothing but the reset was enqueued and the row-panel schedule runs.
+        const bool ok = ops.write(q->h2d, reinterpret_cast<CUdeviceptr>(ready), 0, 0) == CUDA_SUCCESS &&
+                        ops.wait(q->h2d, reinterpret_cast<CUdeviceptr>(ready), 0, 0) == CUDA_SUCCESS;
+        if (!ok)
+            cudaGetLastError();
+        mem_ops_ok.store(ok ? 1 : 0);
+        if (!ok)
+            return KW_OK;
+    }
     const bool trace = std::getenv("KW_E2E_TRACE") != nullptr;
     cudaEvent_t tev[5] = {};
     if (trace) {
