@@ -253,6 +253,42 @@ def test_streamed_host_schedule_is_bitwise_the_resident_launch(gpu, panels, monk
         assert np.array_equal(Cb.host_view()[:, :n], want2), (m, n, k, tile, "repeat")
 
 
+def test_streamed_schedules_on_two_queues_concurrently(gpu, monkeypatch):
+    """Two host threads, two queues, streamed host DGEMMs in flight at once (per-queue flags,
+    counters and tile orders): every round equals the resident launch bit for bit."""
+    import threading
+    monkeypatch.setenv("KW_E2E_MIN_INTENSITY", "0")
+    rng = np.random.default_rng(46)
+    host = kw.Device.host()
+    jobs = []
+    for m, n, k in ((1100, 900, 700), (640, 1500, 520)):
+        a, b, c = rng.random((m, k)) * 10, rng.random((k, n)) * 10, rng.random((m, n)) * 10
+        bufs = tuple(kw.Buffer(host, kw.IndexVec(*x.shape), 8) for x in (a, b, c))
+        for buf, x in zip(bufs, (a, b, c)):
+            buf.host_view()[:, : x.shape[1]] = x
+        jobs.append((m, n, k, c, bufs, tiled(gpu, 0.9, 1.1, a, b, c)))
+    errs = []
+
+    def run(job):
+        m, n, k, c, (A, B, Cb), want = job
+        q = kw.Queue(gpu, kw.QueueFlavor.Async)
+        task = kw.createExec(GPU, kw.gemmTiledWorkDiv(GPU, m, n, 128), kw.GemmTiledKernel(),
+                             kw.GemmArgs(m, n, k, 0.9, 1.1, A, B, Cb))
+        for r in range(4):
+            Cb.host_view()[:, :n] = c
+            q.enqueue(task)
+            q.wait()
+            if not np.array_equal(Cb.host_view()[:, :n], want):
+                errs.append((m, n, k, r))
+
+    threads = [threading.Thread(target=run, args=(j,)) for j in jobs]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errs, errs
+
+
 def test_row_panel_host_schedule_still_matches(gpu, monkeypatch):
     """KW_E2E_STREAMED=0 keeps the row-panel ring schedule (also the path for operands too large
     to hold whole on the device); same bits."""
