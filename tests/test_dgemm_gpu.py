@@ -361,6 +361,41 @@ def test_tiled_bitwise_mode_is_bit_exact(gpu, oracle, golden):
             assert np.array_equal(got, oracle.gemm(1.5, -0.5, a, b, c)), (m, n, k, align)
 
 
+def test_criterion01_gemm_half_bitwise(gpu, oracle):
+    """acceptance.cpp:87-155, GEMM half, the reference's exact instances: the seed-101 stream
+    continues past the 100 AXPY draws, then 100 naive + 100 tiled instances over sizes 1..64,
+    65, 100, 127, 128, 256 with alpha = 0.5 + r%8 and beta = r%2 (0 or 1). Naive and the tiled
+    kernel's bit-exact mode must equal gemmReference bitwise; the default (DMMA) tiled mode is
+    checked against the (K+4)u bound on the same instances."""
+    rng = oracle.MT64(seed=101)
+    for _ in range(100):  # the AXPY half's draws (n, x, y, alpha)
+        n = 1 + rng() % (1 << 16)
+        rng.fill_uniform(n)
+        rng.fill_uniform(n)
+        rng()
+    sizes = list(range(1, 65)) + [65, 100, 127, 128, 256]
+    fails = []
+    for kernel in ("naive", "tiled"):
+        for it in range(100):
+            n = sizes[rng() % len(sizes)]
+            a = rng.fill_uniform(n * n).reshape(n, n)
+            b = rng.fill_uniform(n * n).reshape(n, n)
+            c0 = rng.fill_uniform(n * n).reshape(n, n)
+            alpha = 0.5 + float(rng() % 8)
+            beta = float(rng() % 2)
+            want = oracle.gemm(alpha, beta, a, b, c0)
+            if kernel == "naive":
+                got = naive(gpu, alpha, beta, a, b, c0, 4, 4)
+                if not np.array_equal(got, want):
+                    fails.append((kernel, it, n))
+            else:
+                if not np.array_equal(tiled_bitwise(gpu, alpha, beta, a, b, c0), want):
+                    fails.append(("tiled-bitwise", it, n))
+                if not within_tol(tiled(gpu, alpha, beta, a, b, c0), want, n)[0]:
+                    fails.append(("tiled-dmma", it, n))
+    assert not fails, fails[:10]
+
+
 def test_tiled_bitwise_4096(gpu, oracle):
     n = 4096
     alpha, beta, a, b, c = oracle.workload_gemm(n, 42)
