@@ -100,6 +100,8 @@ def ref() -> C.CDLL:
         r.kwref_run_bench.restype = C.c_int
         r.kwref_csv_roundtrip.argtypes = [C.c_char_p]
         r.kwref_csv_roundtrip.restype = C.c_long
+        r.kwref_buffer_csv_roundtrip.argtypes = [C.c_char_p]
+        r.kwref_buffer_csv_roundtrip.restype = C.c_long
         _r = r
     return _r
 

@@ -346,4 +346,25 @@ long kwref_csv_roundtrip(const char* path)
     return os.str() == original.str() ? static_cast<long>(recs.size()) : -2;
 }
 
+// Reads a matrix CSV with the reference's readBufferCsv and writes it back with its
+// writeBufferCsv: returns rows*cols when the rewrite is byte-identical to the input, -2 when it
+// differs, -1 on a UsageError (buffer_csv.cpp; pins the drop-in's buffer_csv.hpp format).
+long kwref_buffer_csv_roundtrip(const char* path)
+{
+    std::ifstream in(path, std::ios::binary);
+    std::stringstream original;
+    original << in.rdbuf();
+    try {
+        std::istringstream is(original.str());
+        kernelweave::Buffer b = kernelweave::readBufferCsv(is);
+        std::ostringstream os;
+        kernelweave::writeBufferCsv(b, os);
+        return os.str() == original.str() ? static_cast<long>(b.extent().product()) : -2;
+    }
+    catch (const std::exception& e) {
+        g_error = e.what();
+        return -1;
+    }
+}
+
 } // extern "C"

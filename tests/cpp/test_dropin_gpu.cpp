@@ -7,8 +7,11 @@
 #include "check.hpp"
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+#include <fstream>
 #include <random>
+#include <sstream>
 #include <vector>
 
 using namespace kernelweave;
@@ -268,6 +271,61 @@ TEST_CASE("pitched copies never touch bytes outside the box (acceptance crit. 7 
     }
     CHECK(ok);
     CHECK_THROWS_AS(createCopy(ddst, dsrc, IndexVec(6, 9)), UsageError);
+}
+
+TEST_CASE("buffer CSV round-trips bitwise, host and GPU buffers (test_buffer.cpp:275-310)")
+{
+    Buffer buf(Device::host(), IndexVec(7, 5), 8);
+    std::mt19937_64 rng(99);
+    fillUniform<double>(buf, rng, 0.0, 10.0);
+    buf.at<double>(IndexVec(0, 0)) = 1.0 / 3.0;
+    buf.at<double>(IndexVec(6, 4)) = -0.0;
+    std::stringstream first;
+    writeBufferCsv(buf, first);
+    // the text the reference's writer produces for these values (%.17g per value)
+    if (const char* path = std::getenv("KW_CSV_OUT")) {
+        std::ofstream f(path, std::ios::binary);
+        f << first.str();
+    }
+    for (Device where : {Device::host(), Device::gpu(0)}) {
+        std::stringstream in(first.str());
+        Buffer parsed = readBufferCsv(in, where);
+        CHECK(parsed.extent() == buf.extent());
+        CHECK(parsed.device() == where);
+        std::stringstream second;
+        writeBufferCsv(parsed, second); // a GPU buffer is staged through the host
+        CHECK(second.str() == first.str());
+        Buffer back(Device::host(), buf.extent(), 8);
+        Queue q(Device::gpu(0), QueueFlavor::Sync);
+        copyBuffer(q, back, parsed, buf.extent());
+        bool same = true;
+        for (std::size_t r = 0; r < 7; ++r)
+            same = same && std::memcmp(back.rowData<double>(r), buf.rowData<double>(r), 5 * 8) == 0;
+        CHECK(same);
+    }
+    auto throwsUsage = [](const std::string& text) {
+        std::stringstream in(text);
+        try {
+            readBufferCsv(in);
+        }
+        catch (const UsageError&) {
+            return true;
+        }
+        return false;
+    };
+    CHECK(throwsUsage("1,2\n3\n"));
+    CHECK(throwsUsage(""));
+    CHECK(throwsUsage("1,x\n"));
+    Buffer vec(Device::host(), IndexVec(4), 8);
+    std::stringstream out;
+    bool threw = false;
+    try {
+        writeBufferCsv(vec, out);
+    }
+    catch (const UsageError&) {
+        threw = true;
+    }
+    CHECK(threw);
 }
 
 int main()

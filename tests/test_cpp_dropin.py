@@ -25,10 +25,17 @@ def test_dropin_host_logic(programs):
 
 
 @pytest.mark.gpu
-def test_dropin_gpu_kernels(programs):
+def test_dropin_gpu_kernels(programs, tmp_path, monkeypatch):
+    """The C++ drop-in's GPU cases; its matrix CSV writer must produce exactly the text the
+    reference's own readBufferCsv/writeBufferCsv (oracle/_ref) reproduces byte for byte."""
+    csv_path = tmp_path / "m.csv"
+    monkeypatch.setenv("KW_CSV_OUT", str(csv_path))
     p = run(programs["test_dropin_gpu"])
     assert p.returncode == 0, p.stdout + p.stderr
     assert "0 failures" in p.stdout
+    from oracle import oracle as O
+    if O.ref_available():
+        assert O.ref().kwref_buffer_csv_roundtrip(str(csv_path).encode()) == 35, O.ref().kwref_last_error()
 
 
 @pytest.mark.gpu
