@@ -6,6 +6,7 @@
 
 #include "check.hpp"
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -271,6 +272,47 @@ TEST_CASE("pitched copies never touch bytes outside the box (acceptance crit. 7 
     }
     CHECK(ok);
     CHECK_THROWS_AS(createCopy(ddst, dsrc, IndexVec(6, 9)), UsageError);
+}
+
+TEST_CASE("element access layout; buffers move, never copy (test_buffer.cpp:53-110)")
+{
+    Buffer buf(Device::host(), IndexVec(10, 10), 8, 128);
+    CHECK(buf.rowPitch() == 128);
+    CHECK(buf.byteOffset(IndexVec(2, 3)) == 2 * 128 + 3 * 8);
+    buf.at<double>(IndexVec(2, 3)) = 42.5;
+    CHECK(buf.at<double>(IndexVec(2, 3)) == 42.5);
+    CHECK(static_cast<const std::byte*>(buf.elementPtr(IndexVec(2, 3))) == buf.data() + 2 * 128 + 24);
+    auto usage = [](auto&& f) {
+        try {
+            f();
+        }
+        catch (const UsageError&) {
+            return true;
+        }
+        return false;
+    };
+    CHECK(usage([&] { (void)buf.byteOffset(IndexVec(10, 0)); }));
+    CHECK(usage([&] { (void)buf.byteOffset(IndexVec(0, 10)); }));
+    CHECK(usage([&] { (void)buf.byteOffset(IndexVec(3)); }));
+    CHECK(usage([&] { (void)buf.at<float>(IndexVec(0, 0)); }));
+    // every element of the extent has its own offset
+    std::vector<std::size_t> offs;
+    for (std::size_t r = 0; r < 10; ++r)
+        for (std::size_t c = 0; c < 10; ++c)
+            offs.push_back(buf.byteOffset(IndexVec(r, c)));
+    std::sort(offs.begin(), offs.end());
+    CHECK(std::adjacent_find(offs.begin(), offs.end()) == offs.end());
+    // move-only ownership, for host and device storage alike
+    for (Device where : {Device::host(), Device::gpu(0)}) {
+        Buffer a(where, IndexVec(4, 4), 8);
+        const std::byte* storage = a.data();
+        Buffer b = std::move(a);
+        CHECK(b.data() == storage);
+        Buffer c(where, IndexVec(2), 8);
+        c = std::move(b);
+        CHECK(c.data() == storage);
+        CHECK(c.extent() == IndexVec(4, 4));
+    }
 }
 
 TEST_CASE("buffer CSV round-trips bitwise, host and GPU buffers (test_buffer.cpp:275-310)")
