@@ -12,6 +12,9 @@
 
 #include "kernelweave/work_div.hpp"
 
+#include <cstdint>
+#include <string>
+
 namespace kernelweave {
 
 class AccContext {
@@ -175,5 +178,34 @@ KW_HD inline IndexVec getWorkDiv(const AccContext& acc) noexcept
     return IndexVec(e0, e1, detail::extentComponent(w, 2, o, u));
 }
 } // namespace workdiv
+
+#if !defined(__CUDACC__)
+// Kernel-side services for host-compiled translation units (acc.hpp:84-106 declarations). This
+// build has no CPU back-end: a functor that uses them runs on the GPU only, compiled by nvcc
+// against kernelweave/cuda_exec.cuh (which defines the device versions). A host-compiled
+// functor still compiles; calling these on the host is a usage error.
+[[noreturn]] inline void hostKernelServiceUnavailable(const char* what)
+{
+    throw UsageError(std::string(what) +
+                     ": kernel-side service of a device functor — compile the functor with nvcc against "
+                     "kernelweave/cuda_exec.cuh (there is no CPU back-end in the B200 build)");
+}
+inline void* allocSharedMem(const AccContext&, std::size_t, std::size_t) { hostKernelServiceUnavailable("allocSharedMem"); }
+template <class T>
+T* allocSharedMem(const AccContext& acc, std::size_t count)
+{
+    return static_cast<T*>(allocSharedMem(acc, count, sizeof(T)));
+}
+inline void syncBlockThreads(const AccContext&) { hostKernelServiceUnavailable("syncBlockThreads"); }
+inline double atomicAdd(const AccContext&, double&, double) { hostKernelServiceUnavailable("atomicAdd"); }
+inline std::int64_t atomicAdd(const AccContext&, std::int64_t&, std::int64_t)
+{
+    hostKernelServiceUnavailable("atomicAdd");
+}
+inline std::uint64_t atomicAdd(const AccContext&, std::uint64_t&, std::uint64_t)
+{
+    hostKernelServiceUnavailable("atomicAdd");
+}
+#endif
 
 } // namespace kernelweave

@@ -105,6 +105,29 @@ TEST_CASE("no CPU back-end in the B200 build")
     CHECK_THROWS_AS(parseBackend("cuda-emulated"), UsageError);
 }
 
+// A reference-style functor using the kernel-side services compiles in a host (g++) unit;
+// it can only run on the GPU (nvcc + cuda_exec.cuh), so calling the services here throws.
+struct HostCompiledReduce {
+    void operator()(const AccContext& acc, double* out) const
+    {
+        double* partial = allocSharedMem<double>(acc, 4);
+        partial[0] = 1.0;
+        syncBlockThreads(acc);
+        atomicAdd(acc, *out, partial[0]);
+    }
+};
+
+TEST_CASE("host-compiled functors using kernel-side services compile; the services are GPU-only")
+{
+    kw_workdiv w{1, {1, 1, 1}, {4, 1, 1}, {1, 1, 1}};
+    const AccContext acc(w, IndexVec(0), IndexVec(0));
+    double out = 0.0;
+    CHECK_THROWS_AS(HostCompiledReduce{}(acc, &out), UsageError);
+    std::int64_t cell = 0;
+    CHECK_THROWS_AS(atomicAdd(acc, cell, std::int64_t{1}), UsageError);
+    CHECK_THROWS_AS(syncBlockThreads(acc), UsageError);
+}
+
 TEST_CASE("C-ABI usage errors come back as UsageError")
 {
     CHECK_THROWS_AS(detail::check(kw_total_extent(nullptr, 0, 0, nullptr)), UsageError);
