@@ -31,6 +31,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <set>
 #include <utility>
 #include <vector>
 
@@ -121,6 +122,24 @@ struct GemmParams {
     uint32_t* done;
     int panel_rows, panel_cols, npr, npc;
 };
+
+// Dynamic shared memory above 48 KiB is opted into per kernel AND per device: a process that
+// drives several GPUs must set the attribute on each of them.
+kw_status ensure_smem(const void* fn, size_t bytes, const char* what)
+{
+    int dev = 0;
+    cudaGetDevice(&dev);
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> done;
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.count({fn, dev}))
+        return KW_OK;
+    const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+    if (e != cudaSuccess)
+        return kw::cuda_fail(what, e);
+    done.insert({fn, dev});
+    return KW_OK;
+}
 
 template <class Cfg, bool VEC16>
 __device__ __forceinline__ void load_stage(const GemmParams& p, double* sA, double* sB, int bm, int bn, int k0,
@@ -729,15 +748,10 @@ kw_status launch_dmma(cudaStream_t s, const GemmParams& p0)
         return kw::usage("dgemm: problem too large for the tile grid");
     const bool vec16 = (p.lda % 2 == 0) && (p.ldb % 2 == 0) && (reinterpret_cast<uintptr_t>(p.a) % 16 == 0) &&
                        (reinterpret_cast<uintptr_t>(p.b) % 16 == 0);
-    static bool attr_set[2] = {false, false};
     auto kern = vec16 ? dgemm_dmma_kernel<Cfg, true> : dgemm_dmma_kernel<Cfg, false>;
-    if (!attr_set[vec16]) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(Cfg::SMEM));
-        if (e != cudaSuccess)
-            return kw::cuda_fail("dgemm: cudaFuncSetAttribute", e);
-        attr_set[vec16] = true;
-    }
+    const kw_status st = ensure_smem(reinterpret_cast<const void*>(kern), Cfg::SMEM, "dgemm: cudaFuncSetAttribute");
+    if (st != KW_OK)
+        return st;
     kern<<<static_cast<unsigned>(tiles), Cfg::THREADS, Cfg::SMEM, s>>>(p);
     kw::g_launches.fetch_add(1, std::memory_order_relaxed);
     return KW_OK;
@@ -942,14 +956,10 @@ kw_status launch_bitwise_cfg(cudaStream_t s, const GemmParams& p0)
     const bool vec16 = (p.lda % 2 == 0) && (p.ldb % 2 == 0) && (reinterpret_cast<uintptr_t>(p.a) % 16 == 0) &&
                        (reinterpret_cast<uintptr_t>(p.b) % 16 == 0);
     auto kern = vec16 ? dgemm_bitwise_kernel<Cfg, true> : dgemm_bitwise_kernel<Cfg, false>;
-    static bool attr[2] = {false, false};
-    if (!attr[vec16]) {
-        cudaError_t e =
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Cfg::SMEM));
-        if (e != cudaSuccess)
-            return kw::cuda_fail("dgemm_bitwise: cudaFuncSetAttribute", e);
-        attr[vec16] = true;
-    }
+    const kw_status st =
+        ensure_smem(reinterpret_cast<const void*>(kern), Cfg::SMEM, "dgemm_bitwise: cudaFuncSetAttribute");
+    if (st != KW_OK)
+        return st;
     kern<<<static_cast<unsigned>(tiles), Cfg::THREADS, Cfg::SMEM, s>>>(p);
     kw::g_launches.fetch_add(1, std::memory_order_relaxed);
     return KW_OK;
@@ -1005,15 +1015,23 @@ kw_status tile_from_wd(const kw_workdiv* wd, size_t m, size_t n, int* tile)
     return KW_OK;
 }
 
-int sm_count()
+int sm_count() // of the current device (cached per device)
 {
-    static int sms = [] {
-        int d = 0, v = 148;
-        cudaGetDevice(&d);
-        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
-        return v;
-    }();
-    return sms;
+    static std::atomic<int> cache[64] = {};
+    int d = 0;
+    cudaGetDevice(&d);
+    if (d < 0 || d >= 64)
+        d = 0;
+    int v = cache[d].load(std::memory_order_relaxed);
+    if (v == 0) {
+        v = 148;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d) != cudaSuccess) {
+            cudaGetLastError();
+            v = 148;
+        }
+        cache[d].store(v, std::memory_order_relaxed);
+    }
+    return v;
 }
 
 template <class Cfg, bool PERSISTENT, bool STREAMED>
@@ -1036,14 +1054,10 @@ kw_status launch_tma(cudaStream_t s, const GemmParams& p0)
             return kw::usage("dgemm (streamed): tensor map encoding failed");
         return launch_dmma<Cfg128>(s, p0);
     }
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(dgemm_tma_kernel<Cfg, STREAMED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(Cfg::SMEM));
-        if (e != cudaSuccess)
-            return kw::cuda_fail("dgemm: cudaFuncSetAttribute", e);
-        attr = true;
-    }
+    const kw_status st = ensure_smem(reinterpret_cast<const void*>(dgemm_tma_kernel<Cfg, STREAMED>), Cfg::SMEM,
+                                     "dgemm: cudaFuncSetAttribute");
+    if (st != KW_OK)
+        return st;
     const long long resident = static_cast<long long>(sm_count()) * Cfg::MIN_BLOCKS;
     const unsigned grid = static_cast<unsigned>(PERSISTENT && tiles > resident ? resident : tiles);
     dgemm_tma_kernel<Cfg, STREAMED><<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(ma, mb, p);
