@@ -440,6 +440,10 @@ def run_dgemm(args, dist, kw, L, lib, dev, q, sampler) -> dict:
         return res
 
     # N > 1: 16384^3, A/C row blocks per rank, B broadcast from rank 0 in column panels.
+    if args.same_gpu:
+        # NCCL refuses two ranks on one GPU: the --same-gpu harness self-test covers the AXPY
+        # shards and timing reductions only (the panel pipeline has --force-rowsharded).
+        return {"skipped": "--same-gpu self-test: NCCL needs one GPU per rank (see --force-rowsharded)"}
     size = 16384
     from paper_1602_08477_b200 import sharding as S
     r0, r1 = S.dgemm_rows(size, dist.world, dist.rank)
