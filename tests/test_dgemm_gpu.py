@@ -396,6 +396,25 @@ def test_criterion01_gemm_half_bitwise(gpu, oracle):
     assert not fails, fails[:10]
 
 
+def test_outputs_bitwise_identical_across_divisions_and_runs(gpu, oracle):
+    """test_kernels.cpp:308-329 on the GPU: the tiled kernel's bits do not depend on the tile
+    contract (64 or 128) or on the run; the bit-exact mode and the naive kernel equal the oracle
+    on the same instances (seed 2026, n <= 200)."""
+    rng = oracle.MT64(seed=2026)
+    for _ in range(6):
+        n = 1 + rng() % 200
+        a = rng.fill_uniform(n * n).reshape(n, n)
+        b = rng.fill_uniform(n * n).reshape(n, n)
+        c0 = rng.fill_uniform(n * n).reshape(n, n)
+        first = tiled(gpu, 1.5, 0.5, a, b, c0, tile=128)
+        assert np.array_equal(tiled(gpu, 1.5, 0.5, a, b, c0, tile=64), first), n
+        assert np.array_equal(tiled(gpu, 1.5, 0.5, a, b, c0, tile=128), first), n
+        want = oracle.gemm(1.5, 0.5, a, b, c0)
+        assert np.array_equal(tiled_bitwise(gpu, 1.5, 0.5, a, b, c0), want), n
+        assert np.array_equal(naive(gpu, 1.5, 0.5, a, b, c0), want), n
+        assert within_tol(first, want, n)[0], n
+
+
 def test_tiled_bitwise_4096(gpu, oracle):
     n = 4096
     alpha, beta, a, b, c = oracle.workload_gemm(n, 42)
