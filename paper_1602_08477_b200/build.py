@@ -73,11 +73,12 @@ def build_cpp_tests(force: bool = False) -> list[Path]:
             _run(["g++", "-O2", "-std=c++20", "-Wall", "-Wextra", f"-I{INCLUDE}", str(src), "-o", str(exe),
                   f"-L{PKG}", "-lkw_b200", f"-Wl,-rpath,{PKG}", "-Wl,-rpath,$ORIGIN/..", "-lpthread"])
         out.append(exe)
-    kwb = ROOT / "tools" / "kwbench" / "kwbench.cpp"
+    # kwbench carries its own plain CUDA kernels (the "native" back-end), so nvcc builds it
+    kwb = ROOT / "tools" / "kwbench" / "kwbench.cu"
     exe = BUILD / "kwbench"
     if force or _stale(exe, [kwb, LIB] + hdrs):
-        _run(["g++", "-O2", "-std=c++20", "-Wall", "-Wextra", f"-I{INCLUDE}", str(kwb), "-o", str(exe), f"-L{PKG}",
-              "-lkw_b200", f"-Wl,-rpath,{PKG}", "-lpthread"])
+        _run([NVCC, *ARCH, "-O2", "-std=c++20", "-lineinfo", f"-I{INCLUDE}", str(kwb), "-o", str(exe), f"-L{PKG}",
+              "-lkw_b200", f"-Xlinker=-rpath,{PKG}", "-lcudart"])
     out.append(exe)
     for src in sorted(cpp_dir.glob("*.cu")):
         exe = BUILD / src.stem

@@ -50,7 +50,7 @@ def test_generic_device_functors(programs):
 def test_kwbench_usage_errors_exit_2(programs):
     """tools/bench/main.cpp exit-code contract: 2 for usage errors (acceptance crit. 11)."""
     for argv in (["--kernel", "foo"], ["--reps", "2"], ["--sizes", "0"], ["--backend", "blocks"],
-                 ["--kernel", "axpy", "--pessimize"], ["--bogus"]):
+                 ["--kernel", "axpy", "--pessimize"], ["--bogus"], ["--baseline", "serial"]):
         p = subprocess.run([str(programs["kwbench"]), *argv], capture_output=True, text=True, timeout=60)
         assert p.returncode == 2, (argv, p.stdout, p.stderr)
 
@@ -81,6 +81,34 @@ def test_kwbench_gpu_csv_and_verification(programs, tmp_path):
     p = subprocess.run([exe, "--kernel", "axpy", "--sizes", "1000", "--reps", "3", "--verify"], capture_output=True,
                        text=True, timeout=120, env=env)
     assert p.returncode == 1, p.stdout
+
+
+@pytest.mark.gpu
+def test_kwbench_native_backend_and_baseline_report(programs, tmp_path):
+    """--backend native|all and --baseline (runner.cpp:238-328): the native back-end (plain CUDA
+    kernels, no library API) is verified bitwise like the library's, is benchmarked when only
+    named as the baseline, and every median is reported relative to the baseline."""
+    import csv
+    exe = str(programs["kwbench"])
+    for argv, backends in ((["--kernel", "axpy", "--sizes", "1000003", "--backend", "all", "--baseline", "native"],
+                            {"gpu", "native"}),
+                           (["--kernel", "axpy", "--dtype", "f32", "--sizes", "4099", "--backend", "native"],
+                            {"native"}),
+                           (["--kernel", "gemm-naive", "--sizes", "100", "--backend", "native", "--baseline", "gpu"],
+                            {"gpu", "native"}),
+                           (["--kernel", "gemm-tiled", "--sizes", "200", "--backend", "all", "--baseline", "native"],
+                            {"gpu", "native"})):
+        out = tmp_path / "r.csv"
+        p = subprocess.run([exe, *argv, "--reps", "3", "--verify", "--csv", str(out)], capture_output=True,
+                           text=True, timeout=600)
+        assert p.returncode == 0, (argv, p.stdout, p.stderr)
+        recs = list(csv.DictReader(out.open()))
+        assert {r["backend"] for r in recs} == backends, argv
+        assert len(recs) == 3 * len(backends) and all(r["verified"] == "1" for r in recs), argv
+        if "--baseline" in argv:
+            base = argv[argv.index("--baseline") + 1]
+            assert f"median time relative to {base}:" in p.stdout
+            assert f" {base} n=" in p.stdout.split("relative to")[1] and "1.000x" in p.stdout
 
 
 @pytest.mark.gpu

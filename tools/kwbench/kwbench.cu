@@ -1,9 +1,17 @@
 // kwbench for the B200 build — the reference's benchmark harness contract (tools/bench/main.cpp,
-// runner.cpp:238-284, records.cpp) on the drop-in API, backend "gpu".
+// runner.cpp:238-355, records.cpp) on the drop-in API.
 //
-//   kwbench --kernel axpy|gemm-naive|gemm-tiled [--backend gpu|all] [--sizes a,b,..] [--reps N>=3]
-//           [--seed S] [--tile T] [--tpb B] [--ept V] [--dtype f64|f32] [--verify] [--csv PATH]
-//           [--pessimize]
+//   kwbench --kernel axpy|gemm-naive|gemm-tiled [--backend gpu|native|all] [--sizes a,b,..]
+//           [--reps N>=3] [--seed S] [--tile T] [--tpb B] [--ept V] [--dtype f64|f32] [--verify]
+//           [--csv PATH] [--baseline gpu|native] [--pessimize]
+//
+// Back-ends: "gpu" = the library's kernels through createExec/Queue; "native" = plain CUDA kernels
+// launched directly on the raw device pointers, without the library's API — the GPU counterpart
+// of the reference's native loops (runner.cpp:160-171; the zero-overhead analogue of acceptance
+// criterion 08): a grid-stride AXPY and a one-thread-per-element GEMM with the reference's exact
+// arithmetic (bitwise equal to axpyReference / gemmReference). --baseline prints every median
+// relative to that back-end (benchmarked if not selected, relativeReport runner.cpp:303-328);
+// --pessimize adds the degraded division and its slowdown summary (runner.cpp:330-355).
 //
 // Per point (runner.cpp:252-281): seed-deterministic uniform [0,10) inputs drawn exactly like
 // Workload (seed_seq{seed, n, fnv1a(kernel)}, alpha, beta, fillUniform — runner.cpp:56-85), one
@@ -33,6 +41,39 @@ namespace {
 
 using Clock = std::chrono::steady_clock;
 
+// ---- the "native" back-end: plain CUDA, no kernelweave API ---------------------------------
+__device__ __forceinline__ float native_axpy1(float a, float x, float y) { return __fadd_rn(__fmul_rn(a, x), y); }
+__device__ __forceinline__ double native_axpy1(double a, double x, double y) { return __dadd_rn(__dmul_rn(a, x), y); }
+
+template <class T>
+__global__ void native_axpy(std::size_t n, T a, const T* __restrict__ x, T* __restrict__ y)
+{
+    const std::size_t stride = static_cast<std::size_t>(gridDim.x) * blockDim.x;
+    for (std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        y[i] = native_axpy1(a, x[i], y[i]);
+}
+
+// C = alpha*A*B + beta*C, one thread per element, ascending p, separately rounded (gemmReference)
+__global__ void native_gemm(std::size_t n, double alpha, double beta, const double* __restrict__ A, std::size_t lda,
+                            const double* __restrict__ B, std::size_t ldb, double* __restrict__ C, std::size_t ldc)
+{
+    const std::size_t c = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const std::size_t r = static_cast<std::size_t>(blockIdx.y) * blockDim.y + threadIdx.y;
+    if (r >= n || c >= n)
+        return;
+    double acc = 0.0;
+    for (std::size_t p = 0; p < n; ++p)
+        acc = __dadd_rn(acc, __dmul_rn(A[r * lda + p], B[p * ldb + c]));
+    C[r * ldc + c] = __dadd_rn(__dmul_rn(alpha, acc), __dmul_rn(beta, C[r * ldc + c]));
+}
+
+cudaStream_t streamOf(Queue& q)
+{
+    void* s = nullptr;
+    detail::check(kw_queue_stream(q.native(), &s));
+    return static_cast<cudaStream_t>(s);
+}
+
 // KWBENCH_INJECT_FAULT (runner.cpp:28-32): corrupt one output byte after every timed run so the
 // verification-failure path (exit code 1) can be exercised end to end.
 bool injectFault()
@@ -49,7 +90,8 @@ struct Config {
     std::uint64_t seed = 42;
     std::size_t tile = 128, tpb = 512, ept = 4;
     bool verify = false, pessimize = false, f32 = false;
-    std::string csv;
+    std::string csv, baseline;
+    std::vector<std::string> backends; // resolved from --backend (+ the baseline if missing)
 };
 
 struct Record {
@@ -136,6 +178,8 @@ Config parse(int argc, char** argv)
             c.pessimize = true;
         else if (a == "--csv")
             c.csv = val();
+        else if (a == "--baseline")
+            c.baseline = val();
         else
             throw UsageError("unknown option " + a);
     }
@@ -143,9 +187,17 @@ Config parse(int argc, char** argv)
     if (c.kernel != "axpy" && c.kernel != "gemm-naive" && c.kernel != "gemm-tiled")
         throw UsageError("unknown kernel '" + c.kernel + "' (expected axpy, gemm-naive or gemm-tiled)");
     if (c.backend == "all")
-        c.backend = "gpu";
-    if (c.backend != "gpu")
-        throw UsageError("backend '" + c.backend + "' does not exist in the B200 build (use gpu)");
+        c.backends = {"gpu", "native"};
+    else if (c.backend == "gpu" || c.backend == "native")
+        c.backends = {c.backend};
+    else
+        throw UsageError("backend '" + c.backend + "' does not exist in the B200 build (gpu, native or all)");
+    if (!c.baseline.empty()) {
+        if (c.baseline != "gpu" && c.baseline != "native")
+            throw UsageError("baseline '" + c.baseline + "' is not a back-end (gpu or native)");
+        if (std::find(c.backends.begin(), c.backends.end(), c.baseline) == c.backends.end())
+            c.backends.push_back(c.baseline); // benchmarked when missing (runner.cpp:238-251)
+    }
     if (c.reps < 3)
         throw UsageError("reps must be at least 3");
     if (c.sizes.empty())
@@ -192,8 +244,9 @@ struct Point {
 };
 
 template <class T>
-Point runAxpy(const Config& c, std::size_t n, Queue& q)
+Point runAxpy(const Config& c, std::size_t n, Queue& q, const std::string& backend)
 {
+    const bool native = backend == "native";
     std::seed_seq seq{c.seed, static_cast<std::uint64_t>(n), kernelTag("axpy")};
     std::mt19937_64 rng(seq);
     const double alpha = static_cast<double>(rng() >> 11) * 0x1.0p-53 * 10.0;
@@ -217,8 +270,16 @@ Point runAxpy(const Config& c, std::size_t n, Queue& q)
         q.wait();
         ExecTask task = createExec(BackendKind::GpuCudaRt, wd, AxpyKernel{},
                                    AxpyArgsT<T>{n, static_cast<T>(alpha), &x, &y});
+        const unsigned grid = static_cast<unsigned>(std::min<std::size_t>((n + 255) / 256, 148 * 8));
         const auto t0 = Clock::now();
-        q.enqueue(std::move(task));
+        if (native) {
+            native_axpy<T><<<grid, 256, 0, streamOf(q)>>>(n, static_cast<T>(alpha), x.rowData<T>(0), y.rowData<T>(0));
+            if (cudaGetLastError() != cudaSuccess)
+                throw std::runtime_error("native axpy launch failed");
+        }
+        else {
+            q.enqueue(std::move(task));
+        }
         q.wait();
         const double s = std::chrono::duration<double>(Clock::now() - t0).count();
         if (rep < 0)
@@ -232,14 +293,16 @@ Point runAxpy(const Config& c, std::size_t n, Queue& q)
             ok = sameBits<T>(out, ref);
         }
         pt.failed |= !ok;
-        pt.records.push_back({"axpy", "gpu", n, wd.threadsPerBlock().product(), wd.elementsPerThread().product(), 0,
-                              rep, s, flopCount("axpy", n) / s / 1e9, ok});
+        pt.records.push_back({"axpy", backend, n, native ? 256 : wd.threadsPerBlock().product(),
+                              native ? 1 : wd.elementsPerThread().product(), 0, rep, s,
+                              flopCount("axpy", n) / s / 1e9, ok});
     }
     return pt;
 }
 
-Point runGemm(const Config& c, std::size_t n, Queue& q, bool pessimized)
+Point runGemm(const Config& c, std::size_t n, Queue& q, bool pessimized, const std::string& backend)
 {
+    const bool native = backend == "native";
     std::seed_seq seq{c.seed, static_cast<std::uint64_t>(n), kernelTag(c.kernel)};
     std::mt19937_64 rng(seq);
     const double alpha = static_cast<double>(rng() >> 11) * 0x1.0p-53 * 10.0;
@@ -267,7 +330,7 @@ Point runGemm(const Config& c, std::size_t n, Queue& q, bool pessimized)
     // owning the whole output; gemm-tiled degrades to "tile = 1" — each thread one output
     // element, no shared-memory reuse (the untiled kernel) — recorded with tile 1 like the
     // reference's degraded rows.
-    const bool tiled = c.kernel == "gemm-tiled" && !pessimized;
+    const bool tiled = c.kernel == "gemm-tiled" && !pessimized && !native;
     const std::size_t tile = pessimized ? 1 : c.tile;
     const WorkDiv wd = tiled ? gemmTiledWorkDiv(BackendKind::GpuCudaRt, n, n, tile)
                        : !pessimized ? gemmNaiveWorkDiv(BackendKind::GpuCudaRt, n, n, c.tpb, c.ept)
@@ -281,7 +344,17 @@ Point runGemm(const Config& c, std::size_t n, Queue& q, bool pessimized)
         ExecTask task = tiled ? createExec(BackendKind::GpuCudaRt, wd, GemmTiledKernel{}, args)
                               : createExec(BackendKind::GpuCudaRt, wd, GemmNaiveKernel{}, args);
         const auto t0 = Clock::now();
-        q.enqueue(std::move(task));
+        if (native) {
+            native_gemm<<<dim3(static_cast<unsigned>((n + 15) / 16), static_cast<unsigned>((n + 15) / 16)), dim3(16, 16), 0,
+                          streamOf(q)>>>(n, alpha, beta, a.rowData<double>(0), a.leadingDim<double>(),
+                                         b.rowData<double>(0), b.leadingDim<double>(), cc.rowData<double>(0),
+                                         cc.leadingDim<double>());
+            if (cudaGetLastError() != cudaSuccess)
+                throw std::runtime_error("native gemm launch failed");
+        }
+        else {
+            q.enqueue(std::move(task));
+        }
         q.wait();
         const double s = std::chrono::duration<double>(Clock::now() - t0).count();
         if (rep < 0)
@@ -307,8 +380,10 @@ Point runGemm(const Config& c, std::size_t n, Queue& q, bool pessimized)
             }
         }
         pt.failed |= !ok;
-        pt.records.push_back({c.kernel, "gpu", n, wd.threadsPerBlock().product(), wd.elementsPerThread().product(),
-                              c.kernel == "gemm-tiled" ? tile : 0, rep, s, flopCount(c.kernel, n) / s / 1e9, ok});
+        pt.records.push_back({c.kernel, backend, n, native ? 256 : wd.threadsPerBlock().product(),
+                              native ? 1 : wd.elementsPerThread().product(),
+                              c.kernel == "gemm-tiled" && !native ? tile : 0, rep, s, flopCount(c.kernel, n) / s / 1e9,
+                              ok});
     }
     return pt;
 }
@@ -342,12 +417,14 @@ int main(int argc, char** argv)
         Queue q(Device::gpu(0), QueueFlavor::Sync);
         for (std::size_t n : cfg.sizes) {
             std::vector<Point> pts;
-            if (cfg.kernel == "axpy")
-                pts.push_back(cfg.f32 ? runAxpy<float>(cfg, n, q) : runAxpy<double>(cfg, n, q));
-            else {
-                pts.push_back(runGemm(cfg, n, q, false));
-                if (cfg.pessimize)
-                    pts.push_back(runGemm(cfg, n, q, true));
+            for (const std::string& be : cfg.backends) {
+                if (cfg.kernel == "axpy")
+                    pts.push_back(cfg.f32 ? runAxpy<float>(cfg, n, q, be) : runAxpy<double>(cfg, n, q, be));
+                else {
+                    pts.push_back(runGemm(cfg, n, q, false, be));
+                    if (cfg.pessimize && be == "gpu") // a division of the library's kernels
+                        pts.push_back(runGemm(cfg, n, q, true, be));
+                }
             }
             for (auto& p : pts) {
                 failed |= p.failed;
@@ -357,8 +434,9 @@ int main(int argc, char** argv)
                 const double med = median(secs);
                 const Record& r0 = p.records.front();
                 const double bytes = cfg.kernel == "axpy" ? 3.0 * n * (cfg.f32 ? 4 : 8) : 0.0;
-                std::printf("%-10s gpu n=%-9zu b=%-5zu v=%-7zu tile=%-4zu median %.6g s  %.4g GFLOP/s%s%s\n",
-                            r0.kernel.c_str(), n, r0.b, r0.v, r0.tile, med, flopCount(cfg.kernel, n) / med / 1e9,
+                std::printf("%-10s %-6s n=%-9zu b=%-5zu v=%-7zu tile=%-4zu median %.6g s  %.4g GFLOP/s%s%s\n",
+                            r0.kernel.c_str(), r0.backend.c_str(), n, r0.b, r0.v, r0.tile, med,
+                            flopCount(cfg.kernel, n) / med / 1e9,
                             bytes > 0 ? ("  " + fmt(bytes / med / 1e9) + " GB/s").c_str() : "",
                             cfg.verify ? (p.failed ? "  VERIFY FAILED" : "  verified") : "");
                 all.insert(all.end(), p.records.begin(), p.records.end());
@@ -368,6 +446,37 @@ int main(int argc, char** argv)
     catch (const std::exception& e) {
         std::fprintf(stderr, "kwbench: %s\n", e.what());
         return 2;
+    }
+    // pessimizeSummary (runner.cpp:330-355): degraded vs tuned division, per point
+    auto medianOf = [&](const std::string& be, std::size_t n, int pess) {
+        std::vector<double> v;
+        for (const auto& r : all) {
+            const bool degraded = cfg.kernel == "gemm-tiled" ? (r.tile == 1 && cfg.tile != 1) : (r.v == r.n * r.n);
+            if (r.backend == be && r.n == n && (pess < 0 || degraded == (pess == 1)))
+                v.push_back(r.seconds);
+        }
+        return v.empty() ? 0.0 : median(v);
+    };
+    if (cfg.pessimize) {
+        std::printf("\npessimized division slowdown (median vs tuned division):\n");
+        for (std::size_t n : cfg.sizes) {
+            const double tuned = medianOf("gpu", n, 0), bad = medianOf("gpu", n, 1);
+            if (tuned > 0.0 && bad > 0.0)
+                std::printf("  %s gpu n=%zu: %.2fx slower\n", cfg.kernel.c_str(), n, bad / tuned);
+        }
+    }
+    // relativeReport (runner.cpp:303-328): every back-end's median over the baseline's
+    if (!cfg.baseline.empty()) {
+        std::printf("\nmedian time relative to %s:\n", cfg.baseline.c_str());
+        for (std::size_t n : cfg.sizes) {
+            const double base = medianOf(cfg.baseline, n, 0);
+            if (!(base > 0.0)) {
+                std::fprintf(stderr, "kwbench: no '%s' records at n=%zu\n", cfg.baseline.c_str(), n);
+                return 2;
+            }
+            for (const std::string& be : cfg.backends)
+                std::printf("  %s %s n=%zu: %.3fx\n", cfg.kernel.c_str(), be.c_str(), n, medianOf(be, n, 0) / base);
+        }
     }
     if (!cfg.csv.empty()) {
         std::ofstream os(cfg.csv);
