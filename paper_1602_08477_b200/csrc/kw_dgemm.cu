@@ -793,21 +793,23 @@ __global__ void dgemm_naive_kernel(GemmParams p, int er, int ec)
 // in ascending order with separately rounded products and sums (DMUL then DADD, never DFMA),
 // then fl(fl(alpha*acc) + fl(beta*c)). Padded k never enters a sum. FP64 pipe bound: two
 // pipe operations per term, so at most half the DFMA rate.
-//   block tile 128 x 128, k-tile 16, 256 threads; thread (ty, tx) owns C[ty + 16i][tx + 16j],
+//   block tile 128 x 128, k-tile 32 (2 stages), 256 threads; thread (ty, tx) owns C[ty + 16i][tx + 16j],
 //   i, j < 8 (64 independent accumulation chains); A staged row-major with a 144-byte row
-//   pitch (two rows read by one warp land in different banks), B row-major; 3-stage cp.async.
+//   pitch (two rows read by one warp land in different banks), B row-major; STAGES-deep cp.async ring.
 // ------------------------------------------------------------------------------------------
 // Thread (ty, tx) of 16 x 16 owns C[ty + 16i][tx + 16j], i < 8, j < NJ; block tile 128 x 16*NJ.
-template <int NJ_, int MIN_BLOCKS_>
+template <int NJ_, int MIN_BLOCKS_, int BK_ = 16, int STAGES_ = 3>
 struct BwCfg {
     static constexpr int NJ = NJ_, MIN_BLOCKS = MIN_BLOCKS_;
-    static constexpr int BM = 128, BN = 16 * NJ, BK = 16, THREADS = 256, STAGES = 3;
-    static constexpr int A_LD = BK + 2; // doubles; 144-byte rows
+    static constexpr int BM = 128, BN = 16 * NJ, BK = BK_, THREADS = 256, STAGES = STAGES_;
+    static constexpr int A_LD = BK + 2; // doubles: two rows a warp reads land in different banks
     static constexpr int A_STAGE = BM * A_LD, B_STAGE = BK * BN;
     static constexpr size_t SMEM = static_cast<size_t>(STAGES) * (A_STAGE + B_STAGE) * sizeof(double);
 };
-using Bw128 = BwCfg<8, 1>; // 64 chains per thread, one CTA per SM (a 128 x 64 tile at two CTAs per SM
-                           // measured 1.3 % slower: the kernel is FP64-pipe bound, not latency bound)
+// 64 chains per thread, one CTA per SM, k-tile 32 in a 2-stage ring: half the block barriers of
+// k-tile 16 (+1.2 %, tools/bitwise_ab.py: 16.35 vs 16.16 TFLOP/s at 8192^3; a 4th stage gains
+// nothing). A 128 x 64 tile at two CTAs per SM measured 1.3 % slower: FP64-pipe bound.
+using Bw128 = BwCfg<8, 1, 32, 2>;
 
 template <class Cfg, bool VEC16>
 __device__ __forceinline__ void bw_load_stage(const GemmParams& p, double* sA, double* sB, int bm, int bn, int k0,
