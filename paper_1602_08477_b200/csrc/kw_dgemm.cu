@@ -794,7 +794,7 @@ __global__ void dgemm_naive_kernel(GemmParams p, int er, int ec)
 // then fl(fl(alpha*acc) + fl(beta*c)). Padded k never enters a sum. FP64 pipe bound: two
 // pipe operations per term, so at most half the DFMA rate.
 //   block tile 128 x 128, k-tile 32 (2 stages), 256 threads; thread (ty, tx) owns C[ty + 16i][tx + 16j],
-//   i, j < 8 (64 independent accumulation chains); A staged row-major with a 144-byte row
+//   i, j < 8 (64 independent accumulation chains); A staged row-major with a (BK + 2)-double row
 //   pitch (two rows read by one warp land in different banks), B row-major; STAGES-deep cp.async ring.
 // ------------------------------------------------------------------------------------------
 // Thread (ty, tx) of 16 x 16 owns C[ty + 16i][tx + 16j], i < 8, j < NJ; block tile 128 x 16*NJ.
