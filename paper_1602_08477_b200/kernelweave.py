@@ -596,6 +596,46 @@ def copyBuffer(q: Queue, dst: Buffer, src: Buffer, extent: IndexVec) -> TaskHand
     return q.enqueue(createCopy(dst, src, extent))
 
 
+# ---- matrix CSV (buffer_csv.hpp; the text of the reference's writer, "%.17g" per value) ----------
+def writeBufferCsv(buf: Buffer, stream) -> None:
+    """One line per row, ',' between values; 2-D double buffers only (GPU buffers are read back)."""
+    if buf.dim() != 2:
+        raise UsageError("writeBufferCsv: only 2-D buffers are supported")
+    if buf.elemSize() != 8:
+        raise UsageError("writeBufferCsv: only double elements are supported")
+    for row in buf.download():
+        stream.write(",".join("%.17g" % v for v in row) + "\n")
+
+
+def readBufferCsv(stream, device: Optional[Device] = None) -> Buffer:
+    """Parses a CSV matrix into a new 2-D double buffer; ragged, empty or malformed input is a
+    UsageError (buffer_csv.cpp semantics: a final newline ends the input)."""
+    rows = []
+    for line in stream.read().split("\n"):
+        rows.append(line)
+    if rows and rows[-1] == "":
+        rows.pop()
+    values = []
+    for line in rows:
+        line = line.rstrip("\r")
+        try:
+            vals = [float(t) for t in line.split(",")]
+        except ValueError:
+            raise UsageError(f"readBufferCsv: malformed number in '{line}'") from None
+        if values and len(vals) != len(values[0]):
+            raise UsageError("readBufferCsv: ragged rows")
+        values.append(vals)
+    if not values or not values[0]:
+        raise UsageError("readBufferCsv: empty input")
+    arr = np.asarray(values, dtype=np.float64)
+    out = Buffer(device or Device.host(), IndexVec(*arr.shape), 8)
+    if out.device().isHost():
+        out.host_view()[:, : arr.shape[1]] = arr
+    else:
+        out.upload(arr)
+    return out
+
+
 # ---- kernels (kernels/axpy.hpp, kernels/gemm.hpp) ----------------------------------------------
 @dataclass
 class AxpyArgs:

@@ -313,3 +313,28 @@ def test_sync_queue_shutdown_rejects_enqueue(gpu):
     x = dev_vec(gpu, [1.0])
     with pytest.raises(kw.UsageError, match="shutdown"):
         q.enqueue(axpy_task(1, 1.0, x, x))
+
+
+def test_matrix_csv_round_trip_python_mirror(gpu, oracle):
+    """buffer_csv.hpp through the Python mirror: bitwise round trip (host and GPU buffers), the
+    reference's "%.17g" text, and its usage errors (test_buffer.cpp:275-310)."""
+    import io
+    src = kw.Buffer(HOST, kw.IndexVec(7, 5), 8)
+    vals = oracle.MT64(seed=99).fill_uniform(35).reshape(7, 5)
+    vals[0, 0], vals[6, 4] = 1.0 / 3.0, -0.0
+    put(src, vals)
+    first = io.StringIO()
+    kw.writeBufferCsv(src, first)
+    assert first.getvalue().splitlines()[0].split(",")[0] == "%.17g" % (1.0 / 3.0)
+    for where in (HOST, gpu):
+        back = kw.readBufferCsv(io.StringIO(first.getvalue()), where)
+        assert back.extent() == src.extent()
+        assert elements(back).tobytes() == vals.tobytes()
+        again = io.StringIO()
+        kw.writeBufferCsv(back, again)
+        assert again.getvalue() == first.getvalue()
+    for bad in ("1,2\n3\n", "", "1,x\n"):
+        with pytest.raises(kw.UsageError):
+            kw.readBufferCsv(io.StringIO(bad))
+    with pytest.raises(kw.UsageError):
+        kw.writeBufferCsv(kw.Buffer(HOST, kw.IndexVec(4), 8), io.StringIO())
