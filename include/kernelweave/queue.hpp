@@ -25,8 +25,8 @@ class TaskHandle {
 public:
     TaskState state() const
     {
-        if (!m_event)
-            return TaskState::Failed;
+        if (!m_event) // a Sync queue's task: complete when enqueue returned
+            return m_failed || !m_completed ? TaskState::Failed : TaskState::Done;
         int s = 0;
         detail::check(kw_event_state(m_event.get(), &s));
         if (m_failed)
@@ -42,16 +42,17 @@ public:
 
 private:
     friend class Queue;
-    TaskHandle(kw_event ev, bool failed, std::string msg)
+    TaskHandle(kw_event ev, bool failed, std::string msg, bool completed = false)
         : m_event(ev, [](kw_event e) {
               if (e)
                   kw_event_destroy(e);
           }),
-          m_failed(failed), m_message(std::move(msg))
+          m_failed(failed), m_completed(completed), m_message(std::move(msg))
     {
     }
     std::shared_ptr<kw_event_s> m_event;
     bool m_failed;
+    bool m_completed;
     std::string m_message;
 };
 
@@ -136,6 +137,10 @@ private:
         if (st == KW_USAGE || st == KW_RESOURCE)
             detail::check(st);
         const std::string msg = st == KW_TASK ? kw_last_error() : "";
+        // A Sync queue completed the task inside the call (queue.cpp:21-23): its handle needs no
+        // event — recording one would add a GPU round trip to the next wait().
+        if (m_flavor == QueueFlavor::Sync)
+            return TaskHandle(nullptr, st == KW_TASK, msg, true);
         kw_event ev = nullptr;
         if (kw_event_record(m_q, &ev) != KW_OK)
             ev = nullptr;

@@ -480,6 +480,8 @@ class TaskHandle:
     def state(self) -> TaskState:
         if self._failed is not None:
             return TaskState.Failed
+        if self._ev is None:  # a Sync queue's task: complete when enqueue returned
+            return TaskState.Done
         s = C.c_int()
         _raise_for(L.lib().kw_event_state(self._ev, C.byref(s)))
         return TaskState(s.value)
@@ -547,10 +549,13 @@ class Queue:
                 _raise_for(st)  # preconditions fail before anything is enqueued
             if st == L.KW_RESOURCE:
                 _raise_for(st)
+            failed = TaskError(1, L.last_error()) if st == L.KW_TASK else None
+            if self._flavor == QueueFlavor.Sync:  # completed inside the call: no event needed
+                return TaskHandle(None, failed)
             ev = C.c_void_p()
             if L.lib().kw_event_record(self._h, C.byref(ev)) != L.KW_OK:
                 return TaskHandle(None, TaskError(1, L.last_error()))
-            return TaskHandle(ev.value, TaskError(1, L.last_error()) if st == L.KW_TASK else None)
+            return TaskHandle(ev.value, failed)
 
     def wait(self) -> None:
         _raise_for(L.lib().kw_queue_wait(self._h))
