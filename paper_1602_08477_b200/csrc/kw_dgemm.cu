@@ -758,30 +758,39 @@ kw_status launch_dmma(cudaStream_t s, const GemmParams& p0)
 }
 
 // ------------------------------------------------------------------------------------------
-// K3: GemmNaiveKernel on the GPU — bit-exact. Grid thread (r, c) owns rows [r*er, r*er+er) x
-// cols [c*ec, c*ec+ec) clamped at (m, n) (gemm.cpp:13-22); per element one ascending-p dot
-// product from +0.0 with separately rounded products and sums, then the two-rounding epilogue
-// (gemm.cpp:30-36). Axis rule: the last (fastest) work-division component is CUDA x.
+// K3: GemmNaiveKernel on the GPU — bit-exact. The division covers the outputs of gemm.cpp:13-22
+// (grid thread (r, c) owns rows [r*er, r*er+er) x cols [c*ec, c*ec+ec), clamped at (m, n)); per
+// element one ascending-p dot product from +0.0 with separately rounded products and sums, then
+// the two-rounding epilogue (gemm.cpp:30-36). Axis rule: the last (fastest) work-division
+// component is CUDA x.
 // ------------------------------------------------------------------------------------------
 __global__ void dgemm_naive_kernel(GemmParams p, int er, int ec)
 {
-    const long long r = static_cast<long long>(blockIdx.y) * blockDim.y + threadIdx.y;
-    const long long c = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const long long row_first = r * er, col_first = c * ec;
-    if (row_first >= p.m || col_first >= p.n)
+    // Block (by, bx) covers exactly the reference blocks' outputs: rows [by*TY*er, +TY*er) x
+    // cols [bx*TX*ec, +TX*ec) (gemm.cpp:13-22 summed over the block's threads). Inside the block
+    // the elements go to lanes in column order, so consecutive lanes read consecutive B columns
+    // and write consecutive C columns (coalesced) whatever the division — the reference's
+    // gemmNaiveWorkDiv puts its threads along rows. No bit depends on which thread computes an
+    // element: each one is its own ascending-p dot product.
+    const long long tile_rows = static_cast<long long>(blockDim.y) * er;
+    const long long tile_cols = static_cast<long long>(blockDim.x) * ec;
+    const long long row0 = static_cast<long long>(blockIdx.y) * tile_rows;
+    const long long col0 = static_cast<long long>(blockIdx.x) * tile_cols;
+    if (row0 >= p.m || col0 >= p.n)
         return;
-    const long long row_end = row_first + er < p.m ? row_first + er : p.m;
-    const long long col_end = col_first + ec < p.n ? col_first + ec : p.n;
-    for (long long row = row_first; row < row_end; ++row) {
-        for (long long col = col_first; col < col_end; ++col) {
-            double acc = 0.0;
-            const double* ap = p.a + row * p.lda;
-            const double* bp = p.b + col;
-            for (int q = 0; q < p.k; ++q)
-                acc = __dadd_rn(acc, __dmul_rn(ap[q], bp[q * p.ldb]));
-            double* cp = p.c + row * p.ldc + col;
-            *cp = __dadd_rn(__dmul_rn(p.alpha, acc), __dmul_rn(p.beta, *cp));
-        }
+    const long long rows = p.m - row0 < tile_rows ? p.m - row0 : tile_rows;
+    const long long cols = p.n - col0 < tile_cols ? p.n - col0 : tile_cols;
+    const long long nthr = static_cast<long long>(blockDim.x) * blockDim.y;
+    const long long tid = static_cast<long long>(threadIdx.y) * blockDim.x + threadIdx.x;
+    for (long long e = tid; e < rows * cols; e += nthr) {
+        const long long row = row0 + e / cols, col = col0 + e % cols;
+        double acc = 0.0;
+        const double* ap = p.a + row * p.lda;
+        const double* bp = p.b + col;
+        for (int q = 0; q < p.k; ++q)
+            acc = __dadd_rn(acc, __dmul_rn(ap[q], bp[q * p.ldb]));
+        double* cp = p.c + row * p.ldc + col;
+        *cp = __dadd_rn(__dmul_rn(p.alpha, acc), __dmul_rn(p.beta, *cp));
     }
 }
 
