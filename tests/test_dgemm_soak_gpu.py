@@ -1,0 +1,82 @@
+"""Randomised cross-path soak of kw_dgemm: for random shapes, scalars and leading dimensions,
+every execution path — resident, host-pinned (streamed or row-panel schedule, random panel grid),
+pageable host arrays, mixed residency, either tile contract — must give the bits of the resident
+launch, which itself must sit within (K+4)u of gemmReference (the oracle) — for these signed
+inputs relative to |alpha||A||B| + |beta||C|, since cancellation voids a bound on |C_ref|."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from paper_1602_08477_b200 import _lib as L
+from paper_1602_08477_b200 import kernelweave as kw
+
+pytestmark = pytest.mark.gpu
+GPU = kw.BackendKind.GpuCudaRt
+U = 2.0 ** -53
+
+
+def dev_mat(gpu, a):
+    b = kw.Buffer(gpu, kw.IndexVec(*a.shape), 8)
+    b.upload(a)
+    return b
+
+
+def host_mat(a):
+    b = kw.Buffer(kw.Device.host(), kw.IndexVec(*a.shape), 8)
+    b.host_view()[:, : a.shape[1]] = a
+    return b
+
+
+def test_dgemm_paths_agree_bitwise_on_random_cases(gpu, oracle, monkeypatch):
+    rng = np.random.default_rng(20261018)
+    lib = L.lib()
+    q = kw.Queue(gpu, kw.QueueFlavor.Async)
+    for case in range(120):
+        m, n, k = (int(v) for v in rng.integers(1, 1400, size=3))
+        alpha = float(rng.choice([1.0, -0.5, 0.75, 2.0]))
+        beta = float(rng.choice([0.0, 1.0, -1.25, 0.5]))
+        a = rng.standard_normal((m, k))
+        b = rng.standard_normal((k, n))
+        c = rng.standard_normal((m, n))
+        tile = int(rng.choice([64, 128]))
+        wd = kw.gemmTiledWorkDiv(GPU, m, n, tile).to_c()
+        # resident reference launch
+        A, B, Cd = dev_mat(gpu, a), dev_mat(gpu, b), dev_mat(gpu, c)
+        L.check(lib.kw_dgemm(q.handle(), C.byref(wd), m, n, k, alpha, A.data(), A.leadingDim(), B.data(),
+                             B.leadingDim(), beta, Cd.data(), Cd.leadingDim()))
+        q.wait()
+        want = Cd.download()
+        if case % 8 == 0:  # the oracle on a subset (it is the slow part)
+            # signed inputs cancel, so the bound scales with the magnitudes summed, not |C_ref|
+            ref = oracle.gemm(alpha, beta, a, b, c)
+            scale = abs(alpha) * (np.abs(a) @ np.abs(b)) + abs(beta) * np.abs(c)
+            assert np.all(np.abs(want - ref) <= (k + 4) * U * scale), case
+        path = case % 4
+        monkeypatch.setenv("KW_E2E_MIN_INTENSITY", "0" if rng.random() < 0.5 else "400")
+        monkeypatch.setenv("KW_E2E_PANELS", str(int(rng.integers(1, 17))))
+        if path == 0:  # all host pinned (streamed or row panels)
+            Ah, Bh, Ch = host_mat(a), host_mat(b), host_mat(c)
+            L.check(lib.kw_dgemm(q.handle(), C.byref(wd), m, n, k, alpha, Ah.data(), Ah.leadingDim(), Bh.data(),
+                                 Bh.leadingDim(), beta, Ch.data(), Ch.leadingDim()))
+            q.wait()
+            got = Ch.host_view()[:, :n].copy()
+        elif path == 1:  # pageable numpy arrays
+            ap, bp, cp = a.copy(), b.copy(), c.copy()
+            L.check(lib.kw_dgemm(q.handle(), C.byref(wd), m, n, k, alpha, ap.ctypes.data, k, bp.ctypes.data, n,
+                                 beta, cp.ctypes.data, n))
+            q.wait()
+            got = cp
+        elif path == 2:  # mixed: B resident, A and C pinned host
+            Ah, Ch = host_mat(a), host_mat(c)
+            L.check(lib.kw_dgemm(q.handle(), C.byref(wd), m, n, k, alpha, Ah.data(), Ah.leadingDim(), B.data(),
+                                 B.leadingDim(), beta, Ch.data(), Ch.leadingDim()))
+            q.wait()
+            got = Ch.host_view()[:, :n].copy()
+        else:  # resident again on a fresh C: run-to-run determinism
+            C2 = dev_mat(gpu, c)
+            L.check(lib.kw_dgemm(q.handle(), C.byref(wd), m, n, k, alpha, A.data(), A.leadingDim(), B.data(),
+                                 B.leadingDim(), beta, C2.data(), C2.leadingDim()))
+            q.wait()
+            got = C2.download()
+        assert np.array_equal(got, want), (case, path, m, n, k, tile)
