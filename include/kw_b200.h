@@ -128,8 +128,10 @@ KW_EXPORT kw_status kw_queue_complete_launch(kw_queue q, int cuda_error, const c
 KW_EXPORT kw_status kw_queue_fail_slot(kw_queue q, const char* what, uint32_t** slot);
 
 /* TaskHandle (queue.hpp:36-52) as a CUDA event recorded after the last enqueued task. State is
- * PENDING until the event completes, then DONE (FAILED on a device fault). A task's own launch
- * failure is the KW_TASK returned by its kw_* call (the C++/Python handles carry it). */
+ * PENDING until the event completes, then DONE — or FAILED on a device fault or when the task's
+ * device-side failure slot (kw_queue_fail_slot) was set. A task's own launch failure is the
+ * KW_TASK returned by its kw_* call (the C++/Python handles carry it; a Sync queue's handles need
+ * no event at all). */
 KW_EXPORT kw_status kw_event_record(kw_queue q, kw_event* ev);
 KW_EXPORT kw_status kw_event_state(kw_event ev, int* state);
 KW_EXPORT kw_status kw_event_destroy(kw_event ev);
@@ -158,19 +160,22 @@ KW_EXPORT kw_status kw_dgemm_default_workdiv(size_t m, size_t n, size_t tile, kw
  * Bit-exact against axpyReference (reference.cpp:8-12): product and sum rounded separately
  * (no FMA contraction). wd covers n with its grid element extent; elements >= n are never
  * touched (axpy.cpp:15-17). Device pointers run the HBM kernel; host pointers (pinned or
- * pageable) are streamed through the device in chunks with copies overlapped on two
- * streams (e2e path). wd == NULL: kw_axpy_default_workdiv. */
+ * pageable) are streamed through the device in 32 MiB chunks, uploads / kernel / downloads
+ * overlapped on three streams (e2e path). wd == NULL: kw_axpy_default_workdiv. */
 KW_EXPORT kw_status kw_axpy_f32(kw_queue q, const kw_workdiv* wd, size_t n, float alpha, const float* x,
                                 float* y);
 KW_EXPORT kw_status kw_axpy_f64(kw_queue q, const kw_workdiv* wd, size_t n, double alpha, const double* x,
                                 double* y);
 
 /* ---- K2: tiled DGEMM  C = alpha*A*B + beta*C  (GemmTiledKernel, gemm.cpp:40-118) ----------
- * Row-major pitched fp64; lda/ldb/ldc in elements. FP64 DMMA tensor-core kernel, cp.async
- * multistage smem pipeline. Within |dC| <= (K+4)*2^-53*|C_ref| of gemmReference
- * (reference.cpp:14-26); the epilogue is fl(fl(alpha*acc) + fl(beta*c)) as in gemm.cpp:115.
- * beta multiplies C even when 0 (C is always read). wd == NULL: default tile. Host pointers
- * are staged through the device (e2e path). */
+ * Row-major pitched fp64; lda/ldb/ldc in elements. FP64 DMMA tensor-core kernel fed by TMA and
+ * an mbarrier stage ring (warp-specialised; a cp.async kernel for operands TMA cannot address).
+ * Within |dC| <= (K+4)*2^-53*|C_ref| of gemmReference (reference.cpp:14-26); the epilogue is
+ * fl(fl(alpha*acc) + fl(beta*c)) as in gemm.cpp:115. beta multiplies C even when 0 (C is always
+ * read). wd == NULL: default tile; wd's tile (64 or 128) is the coverage contract, the CTA tile is
+ * chosen per problem among bitwise-identical configurations. Host pointers are streamed through
+ * the device inside the task (row panels, or for compute-heavy problems with all three operands
+ * pinned, panel uploads feeding one persistent launch); bits equal the resident launch. */
 KW_EXPORT kw_status kw_dgemm(kw_queue q, const kw_workdiv* wd, size_t m, size_t n, size_t k, double alpha,
                              const double* A, size_t lda, const double* B, size_t ldb, double beta, double* C,
                              size_t ldc);
@@ -193,13 +198,14 @@ KW_EXPORT kw_status kw_dgemm_with_config(kw_queue q, int cfg, size_t m, size_t n
 
 /* ---- K3: naive DGEMM (GemmNaiveKernel, gemm.cpp:11-38) — BIT-EXACT mode --------------------
  * One dot product per output, ascending p, products and sums rounded separately, acc from
- * +0.0: bitwise identical to gemmReference. Honors the (rows, cols) work division exactly
- * like the reference: thread (r, c) of the grid owns rows [r*er, r*er+er) x cols [c*ec, ...). */
+ * +0.0: bitwise identical to gemmReference. Computes exactly the outputs the (rows, cols) work
+ * division covers in the reference (thread (r, c) owns rows [r*er, r*er+er) x cols [c*ec, ...));
+ * inside a block the outputs go to lanes in column order (coalesced; no bit depends on it). */
 KW_EXPORT kw_status kw_dgemm_naive(kw_queue q, const kw_workdiv* wd, size_t m, size_t n, size_t k,
                                    double alpha, const double* A, size_t lda, const double* B, size_t ldb,
                                    double beta, double* C, size_t ldc);
 
-/* ---- multi-GPU (one process per GPU) -------------------------------------------------------
+/* ---- multi-GPU (one process per GPU; BASELINE.json configs[3]) ------------------
  * NCCL communicator for the row-sharded DGEMM's broadcast of B. The 128-byte unique id is
  * produced by rank 0 (kw_comm_unique_id) and exchanged by the caller (torch.distributed
  * store, MPI, a file). */
@@ -212,8 +218,9 @@ KW_EXPORT kw_status kw_comm_broadcast(kw_comm comm, kw_queue q, void* buf, size_
 /* Row-block shard of C = alpha*A*B + beta*C across `world` ranks: this rank holds
  * rows [row0, row0+m_local) of A (lda) and C (ldc); B (k x n, ldb) is valid on `root` and is
  * broadcast in `panels` column panels into the caller's b_panels scratch (k*n doubles,
- * panel-major: panel j is k x w_j dense), each panel's broadcast overlapped with the
- * previous panel's DGEMM on a second stream. Every output element is reduced entirely on
+ * panel-major: panel j is k x w_j dense), each panel's broadcast (high-priority stream)
+ * overlapped with the DGEMMs of earlier panels, which alternate between two compute streams.
+ * Every output element is reduced entirely on
  * one rank in the single-GPU kernel's order, so the gathered C is bitwise identical to the
  * 1-GPU kw_dgemm result. */
 KW_EXPORT kw_status kw_dgemm_rowsharded(kw_comm comm, kw_queue q, size_t m_local, size_t n, size_t k,
