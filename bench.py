@@ -415,9 +415,15 @@ def run_dgemm(args, dist, kw, L, lib, dev, q, sampler) -> dict:
                 q.wait()
             e2e_s = time.perf_counter() - t0
             sampler.active = False
+            # the library's schedule choice (kw_dgemm.cu dgemm_streamed): >= 400 flop/B -> streamed
+            intensity = 2 * size ** 3 / (8 * 3 * size * size)
+            streamed = intensity >= float(os.environ.get("KW_E2E_MIN_INTENSITY", "400")) and \
+                os.environ.get("KW_E2E_STREAMED", "1") != "0"
             entry["e2e"] = {"value": round(2 * size ** 3 * e2e_steps / e2e_s / 1e12, 3), "unit": "TFLOP/s",
                             "steps": e2e_steps, "h2d_bytes_per_step": 3 * size * size * 8,
-                            "d2h_bytes_per_step": size * size * 8}
+                            "d2h_bytes_per_step": size * size * 8,
+                            "schedule": ("streamed: square-growth panel uploads into one persistent kernel"
+                                         if streamed else "row panels of A/C, B streamed in column panels")}
             bw_task = None
             if size == 8192:
                 # bit-exact tiled mode: separately rounded products/sums in ascending k
