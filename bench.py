@@ -407,7 +407,7 @@ def run_dgemm(args, dist, kw, L, lib, dev, q, sampler) -> dict:
                                   kw.GemmArgs(size, size, size, 1.25, 0.75, hA, hB, hC))
             q.enqueue(htask)
             q.wait()
-            e2e_steps = 3
+            e2e_steps = 5
             sampler.active = True
             t0 = time.perf_counter()
             for _ in range(e2e_steps):
