@@ -35,11 +35,13 @@ kw_status resource(const std::string& msg)
 kw_status cuda_fail(const char* what, cudaError_t e)
 {
     set_error(std::string(what) + ": " + cudaGetErrorString(e));
+    cudaGetLastError(); // reported here: must not resurface as the next task's launch error
     return KW_TASK;
 }
 
 kw_status task_fail(Queue* q, const std::string& msg)
 {
+    cudaGetLastError(); // recorded once here (a device fault stays sticky regardless)
     {
         std::lock_guard<std::mutex> lock(q->mu);
         if (q->failed++ == 0)
@@ -198,6 +200,11 @@ kw_status kw_device_props_get(int device, kw_device_props* props)
 {
     if (!props)
         return kw::usage("kw_device_props_get: null output");
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || device < 0 || device >= count) {
+        cudaGetLastError();
+        return kw::usage("kw_device_props_get: device index " + std::to_string(device) + " does not exist");
+    }
     cudaDeviceProp p;
     cudaError_t e = cudaGetDeviceProperties(&p, device);
     if (e != cudaSuccess)
@@ -222,6 +229,11 @@ kw_status kw_device_props_get(int device, kw_device_props* props)
 
 kw_status kw_device_synchronize(int device)
 {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || device < 0 || device >= count) {
+        cudaGetLastError();
+        return kw::usage("kw_device_synchronize: device index " + std::to_string(device) + " does not exist");
+    }
     kw::DeviceGuard g(device);
     cudaError_t e = cudaDeviceSynchronize();
     return e == cudaSuccess ? KW_OK : kw::cuda_fail("cudaDeviceSynchronize", e);

@@ -1,0 +1,82 @@
+"""The remaining C-ABI entry points on a GPU (tests/test_abi.py checks that every declared symbol
+is exported; this checks each one does what include/kw_b200.h says): version and device queries,
+pointer classification, queue flavor, the DGEMM configuration table, the L2 flush and the NCCL
+broadcast (world size 1)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from paper_1602_08477_b200 import _lib as L
+from paper_1602_08477_b200 import kernelweave as kw
+
+pytestmark = pytest.mark.gpu
+
+
+def test_version_and_device_queries(gpu):
+    lib = L.lib()
+    assert lib.kw_version().decode().strip()
+    n = C.c_int()
+    L.check(lib.kw_device_count(C.byref(n)))
+    assert n.value >= 1
+    props = L.kw_device_props()
+    L.check(lib.kw_device_props_get(0, C.byref(props)))
+    assert (props.cc_major, props.cc_minor) == (10, 0)  # sm_100a: this build's only target
+    assert props.sm_count == 148 and b"B200" in props.name
+    L.check(lib.kw_device_synchronize(0))
+    assert lib.kw_device_props_get(n.value + 3, C.byref(props)) == L.KW_USAGE
+    assert lib.kw_device_synchronize(n.value + 3) == L.KW_USAGE
+    # a failed query leaves nothing behind for the next task to trip over
+    q = kw.Queue(gpu, kw.QueueFlavor.Sync)
+    L.check(lib.kw_l2_flush(q.handle()))
+
+
+def test_pointer_kinds_and_queue_flavor(gpu):
+    lib = L.lib()
+    dev = kw.Buffer(gpu, kw.IndexVec(16), 8)
+    pinned = kw.Buffer(kw.Device.host(), kw.IndexVec(16), 8)
+    pageable = np.zeros(16)
+    for ptr, want in ((dev.data(), L.KW_MEM_DEVICE), (pinned.data(), L.KW_MEM_PINNED),
+                      (pageable.ctypes.data, L.KW_MEM_PAGEABLE)):
+        kind, d = C.c_int(), C.c_int()
+        L.check(lib.kw_pointer_kind(ptr, C.byref(kind), C.byref(d)))
+        assert kind.value == want
+    for flavor in (kw.QueueFlavor.Sync, kw.QueueFlavor.Async):
+        q = kw.Queue(gpu, flavor)
+        f = C.c_int()
+        L.check(lib.kw_queue_flavor(q.handle(), C.byref(f)))
+        assert f.value == flavor.value
+
+
+def test_dgemm_configuration_table(gpu):
+    lib = L.lib()
+    count = lib.kw_dgemm_config_count()
+    assert count >= 2
+    for cfg in range(count):
+        info = (C.c_int * 5)()
+        L.check(lib.kw_dgemm_config_info(cfg, info))
+        bm, bn, bk, threads, stages = list(info)
+        assert bm in (64, 128) and bn in (64, 128) and bk in (16, 32) and threads % 32 == 0 and stages >= 2
+    info = (C.c_int * 5)()
+    assert lib.kw_dgemm_config_info(count, info) == L.KW_USAGE
+
+
+def test_l2_flush_and_world1_broadcast(gpu):
+    lib = L.lib()
+    q = kw.Queue(gpu, kw.QueueFlavor.Async)
+    L.check(lib.kw_l2_flush(q.handle()))
+    q.wait()
+    uid = (C.c_char * 128)()
+    L.check(lib.kw_comm_unique_id(uid))
+    comm = C.c_void_p()
+    L.check(lib.kw_comm_init(C.byref(comm), 0, 1, 0, uid))
+    try:
+        buf = kw.Buffer(gpu, kw.IndexVec(1000), 8)
+        vals = np.arange(1000, dtype=np.float64)
+        buf.upload(vals)
+        L.check(lib.kw_comm_broadcast(comm, q.handle(), buf.data(), 8000, 0))
+        q.wait()
+        assert np.array_equal(buf.download(), vals)  # the root's own data is unchanged
+        assert lib.kw_comm_broadcast(comm, q.handle(), buf.data(), 8000, 1) == L.KW_USAGE  # no rank 1
+    finally:
+        L.check(lib.kw_comm_destroy(comm))
