@@ -8,6 +8,8 @@
 //   totalExtent / divideForBackend             core/src/work_div.cpp:53-119
 #include "kw_common.cuh"
 
+#include <cstdint>
+
 #include <cstring>
 #include <new>
 #include <vector>
@@ -250,19 +252,22 @@ kw_status kw_buffer_alloc(int device, uint32_t dim, const size_t extent[3], size
         return kw::usage("IndexVec: dimensionality must be 1, 2 or 3");
     if (elem_size == 0)
         return kw::usage("Buffer: element size must be positive");
-    if (row_align == 0 || (row_align & (row_align - 1)) != 0)
+    if (row_align == 0 || (row_align & (row_align - 1)) != 0 || row_align > (SIZE_MAX >> 2))
         return kw::usage("Buffer: row alignment must be a power of two");
     size_t rows = 1;
     for (uint32_t k = 0; k < dim; ++k) {
         if (extent[k] == 0)
             return kw::usage("Buffer: extent components must be positive");
-        if (k + 1 < dim)
-            rows *= extent[k];
+        if (k + 1 < dim && __builtin_mul_overflow(rows, extent[k], &rows))
+            return kw::resource("Buffer: size overflows the address space");
     }
-    const size_t row_bytes = extent[dim - 1] * elem_size;
+    size_t row_bytes = 0, bytes = 0;
+    if (__builtin_mul_overflow(extent[dim - 1], elem_size, &row_bytes) || row_bytes > (SIZE_MAX >> 1))
+        return kw::resource("Buffer: size overflows the address space");
     // 1-D buffers are dense; padding a vector has no locality benefit (buffer.cpp:36-37).
     const size_t pitch = dim == 1 ? row_bytes : (row_bytes + row_align - 1) / row_align * row_align;
-    const size_t bytes = rows * pitch;
+    if (__builtin_mul_overflow(rows, pitch, &bytes))
+        return kw::resource("Buffer: size overflows the address space");
     void* p = nullptr;
     cudaError_t e;
     if (device < 0) {

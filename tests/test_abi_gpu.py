@@ -80,3 +80,37 @@ def test_l2_flush_and_world1_broadcast(gpu):
         assert lib.kw_comm_broadcast(comm, q.handle(), buf.data(), 8000, 1) == L.KW_USAGE  # no rank 1
     finally:
         L.check(lib.kw_comm_destroy(comm))
+
+
+def test_failed_calls_leave_no_residue(gpu):
+    """Usage errors and failed CUDA calls are reported by the call that made them and never
+    resurface in a later, valid task (queue.hpp:86-93: one failure, reported once)."""
+    lib = L.lib()
+    q = kw.Queue(gpu, kw.QueueFlavor.Async)
+    x = kw.Buffer(gpu, kw.IndexVec(1024), 8)
+    y = kw.Buffer(gpu, kw.IndexVec(1024), 8)
+    x.upload(np.ones(1024))
+    y.upload(np.zeros(1024))
+    ptr, pitch = C.c_void_p(), C.c_size_t()
+    bad = [
+        lambda: lib.kw_buffer_alloc(4096, 1, L.sz3((8,)), 8, 64, C.byref(ptr), C.byref(pitch)),
+        lambda: lib.kw_buffer_alloc(0, 1, L.sz3((1 << 62,)), 8, 64, C.byref(ptr), C.byref(pitch)),  # too big
+        lambda: lib.kw_axpy_f64(q.handle(), C.byref(kw.WorkDiv(kw.IndexVec(1), kw.IndexVec(2048),
+                                                                kw.IndexVec(1)).to_c()), 1024, 1.0,
+                                x.data(), y.data()),
+        lambda: lib.kw_dgemm(q.handle(), None, 4, 4, 8, 1.0, x.data(), 4, x.data(), 4, 1.0, y.data(), 4),  # lda<k
+        lambda: lib.kw_copy(q.handle(), y.data(), 8, L.sz3((1024,)), x.data(), 8, L.sz3((1024,)), 1,
+                            L.sz3((2048,)), 8),  # extent beyond both buffers
+        lambda: lib.kw_device_synchronize(-1),
+        lambda: lib.kw_queue_create(99, 0, C.byref(ptr)),
+    ]
+    for i, call in enumerate(bad):
+        assert call() != L.KW_OK, i
+    # a valid task on the same queue, then wait(): clean
+    L.check(lib.kw_axpy_f64(q.handle(), None, 1024, 2.0, x.data(), y.data()))
+    q.wait()
+    assert (y.download() == 2.0).all()
+    q2 = kw.Queue(gpu, kw.QueueFlavor.Sync)
+    L.check(lib.kw_axpy_f64(q2.handle(), None, 1024, 1.0, x.data(), y.data()))
+    q2.wait()
+    assert (y.download() == 3.0).all()
