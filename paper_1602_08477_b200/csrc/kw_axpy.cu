@@ -21,6 +21,7 @@
 #include "kw_common.cuh"
 
 #include <climits>
+#include <cstdint>
 #include <cstdlib>
 
 namespace {
@@ -239,7 +240,9 @@ kw_status validate_wd(const kw_workdiv* wd, size_t n, size_t& blocks, uint32_t& 
     blocks = wd->blocks[0];
     threads = static_cast<uint32_t>(wd->threads[0]);
     elems = static_cast<uint32_t>(wd->elems[0]);
-    const size_t covered = blocks * threads * static_cast<size_t>(elems);
+    size_t covered = 0; // saturates: a division that large covers every index
+    if (__builtin_mul_overflow(blocks, static_cast<size_t>(threads) * elems, &covered))
+        covered = SIZE_MAX;
     limit = covered < n ? covered : n; // only covered indices are computed (axpy.cpp:12-17)
     return KW_OK;
 }
