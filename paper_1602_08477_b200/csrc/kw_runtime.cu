@@ -599,8 +599,12 @@ kw_status kw_copy(kw_queue qh, void* dst, size_t dst_pitch, const size_t dst_ext
     for (uint32_t k = 0; k < dim; ++k)
         if (extent[k] > dst_extent[k] || extent[k] > src_extent[k])
             return kw::usage("copy: extent exceeds a buffer extent");
-    const size_t line = extent[dim - 1] * elem_size;
-    if (dim > 1 && (dst_pitch < dst_extent[dim - 1] * elem_size || src_pitch < src_extent[dim - 1] * elem_size))
+    size_t line = 0, dst_row = 0, src_row = 0;
+    if (__builtin_mul_overflow(extent[dim - 1], elem_size, &line) ||
+        __builtin_mul_overflow(dst_extent[dim - 1], elem_size, &dst_row) ||
+        __builtin_mul_overflow(src_extent[dim - 1], elem_size, &src_row))
+        return kw::usage("copy: row size overflows the address space");
+    if (dim > 1 && (dst_pitch < dst_row || src_pitch < src_row))
         return kw::usage("copy: row pitch smaller than a row");
     for (uint32_t k = 0; k < dim; ++k)
         if (extent[k] == 0)
