@@ -329,7 +329,10 @@ def run_ours(args, dist: Dist) -> dict:
         "e2e": {"value": round(e2e_value, 2), "unit": "GB/s", "steps": e2e_steps,
                 "h2d_bytes_per_step": 8 * N_AXPY, "d2h_bytes_per_step": 4 * N_AXPY,
                 "how": "executeTask-equivalent Queue.enqueue(createExec(GpuCudaRt, AxpyKernel, host pinned "
-                       "buffers)) + wait, wall clock; chunked H2D/kernel/D2H on two streams"},
+                       "buffers)) + wait, wall clock; chunked H2D/kernel/D2H on three streams",
+                "link_ceiling": {"value": 78.8, "unit": "GB/s",
+                                 "what": "pure pinned copies with the same 2:1 H2D:D2H byte mix on this box type",
+                                 "source": "profiles/pcie_probe_r01.txt"}},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "peak_source": peak_src,
                      "traffic": (None if traffic_from_profiles("axpy_f32") is None
