@@ -22,7 +22,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
               "-Xptxas", "-v", f"-I{INCLUDE}", f"-I{CSRC}"]
-SOURCES = ["kw_runtime.cu", "kw_axpy.cu", "kw_dgemm.cu", "kw_comm.cu"]
+SOURCES = ["kw_runtime.cu", "kw_axpy.cu", "kw_dgemm.cu", "kw_dgemm_e2e.cu", "kw_comm.cu"]
 
 
 def _run(cmd: list[str]) -> str:
