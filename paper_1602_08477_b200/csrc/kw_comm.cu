@@ -5,8 +5,9 @@
 // AXPY shards by index range and needs no communication.
 //
 // Row-sharded DGEMM: rank r owns row block r of A and C. B (k x n) lives on the root and is
-// broadcast in column panels; panel j's broadcast (comm stream) overlaps panel j-1's DGEMM
-// (queue stream). Each C element is reduced entirely on one rank by the single-GPU kernel in
+// broadcast in column panels; panel j's broadcast (high-priority comm stream) overlaps the
+// DGEMMs of earlier panels, which alternate between the queue's two compute streams so no panel
+// ends in a partial wave. Each C element is reduced entirely on one rank by the single-GPU kernel in
 // the same k order, so gathering the C row blocks reproduces the 1-GPU result bit for bit.
 #include "kw_common.cuh"
 
