@@ -232,12 +232,12 @@ kw_status kw_dgemm_rowsharded(kw_comm c, kw_queue qh, size_t m_local, size_t n, 
     cudaError_t e = cudaEventRecord(c->start, q->stream); // B and C may come from earlier tasks
     if (e == cudaSuccess)
         e = cudaStreamWaitEvent(c->stream, c->start, 0);
-    // Panel launches alternate between the queue stream and its aux stream: panel j+1's CTAs
+    // Panel launches alternate between the queue stream and its second compute stream: panel j+1's CTAs
     // fill the SMs while panel j's last wave drains (disjoint C columns, same per-element
     // arithmetic — bits unchanged). A panel launch ends in a partial wave otherwise: one rank's
     // 2048..8192-row block lost 2-13 % (tools/rowshard_rank_probe.py).
     if (e == cudaSuccess)
-        e = cudaStreamWaitEvent(q->aux, c->start, 0);
+        e = cudaStreamWaitEvent(q->comp2, c->start, 0);
     ncclResult_t r = ncclSuccess;
     size_t off = 0;
     for (int j = 0; j < np && e == cudaSuccess && r == ncclSuccess; ++j) {
@@ -251,7 +251,7 @@ kw_status kw_dgemm_rowsharded(kw_comm c, kw_queue qh, size_t m_local, size_t n, 
         }
         if (e == cudaSuccess)
             e = cudaEventRecord(c->panel_ready[j], c->stream);
-        cudaStream_t cs = (j & 1) ? q->aux : q->stream;
+        cudaStream_t cs = (j & 1) ? q->comp2 : q->stream;
         if (e == cudaSuccess)
             e = cudaStreamWaitEvent(cs, c->panel_ready[j], 0);
         if (e == cudaSuccess && m_local > 0) {
@@ -262,9 +262,9 @@ kw_status kw_dgemm_rowsharded(kw_comm c, kw_queue qh, size_t m_local, size_t n, 
         off += k * wj;
     }
     if (e == cudaSuccess)
-        e = cudaEventRecord(q->ev_join, q->aux);
+        e = cudaEventRecord(q->ev_join2, q->comp2);
     if (e == cudaSuccess)
-        e = cudaStreamWaitEvent(q->stream, q->ev_join, 0);
+        e = cudaStreamWaitEvent(q->stream, q->ev_join2, 0);
     if (r != ncclSuccess)
         return kw::task_fail(q, std::string("ncclBroadcast: ") + ncclGetErrorString(r));
     if (e != cudaSuccess)
