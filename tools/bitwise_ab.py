@@ -1,5 +1,8 @@
-"""Interleaved A/B of bit-exact tiled DGEMM variants (KW_BW_VARIANT read per launch):
-python tools/bitwise_ab.py n variants rounds"""
+"""Interleaved A/B of bit-exact tiled DGEMM variants: python tools/bitwise_ab.py n variants rounds.
+The library reads no variant switch today — profiles/dgemm_bitwise_variants_r01.txt came from a
+temporary KW_BW_VARIANT hook in launch_bitwise (BwCfg<8,1,BK,STAGES> instantiations), removed
+once k-tile 32 x 2 stages was adopted; re-add such a hook to compare new variants. Also checks
+that every variant's output is bitwise equal to the first's."""
 import ctypes as C
 import json
 import os
