@@ -80,3 +80,27 @@ def test_dgemm_paths_agree_bitwise_on_random_cases(gpu, oracle, monkeypatch):
             q.wait()
             got = C2.download()
         assert np.array_equal(got, want), (case, path, m, n, k, tile)
+
+
+@pytest.mark.parametrize("m,n,k", [(1, 1, 100000), (100000, 1, 16), (16, 100000, 1), (3, 70000, 9),
+                                   (65537, 3, 33), (1, 8192, 8192), (8192, 1, 8192)])
+def test_extreme_shapes(gpu, oracle, m, n, k):
+    """Dot products, GEMV-like and outer-product shapes: resident launch within the
+    magnitude-scaled (K+4)u bound of gemmReference, and the pinned-host path equal to it."""
+    rng = np.random.default_rng(m * 7 + n * 3 + k)
+    lib = L.lib()
+    q = kw.Queue(gpu, kw.QueueFlavor.Async)
+    a, b, c = rng.standard_normal((m, k)), rng.standard_normal((k, n)), rng.standard_normal((m, n))
+    A, B, Cd = dev_mat(gpu, a), dev_mat(gpu, b), dev_mat(gpu, c)
+    L.check(lib.kw_dgemm(q.handle(), None, m, n, k, 0.75, A.data(), A.leadingDim(), B.data(), B.leadingDim(), -1.5,
+                         Cd.data(), Cd.leadingDim()))
+    q.wait()
+    got = Cd.download()
+    ref = oracle.gemm(0.75, -1.5, a, b, c)
+    scale = 0.75 * (np.abs(a) @ np.abs(b)) + 1.5 * np.abs(c)
+    assert np.all(np.abs(got - ref) <= (k + 4) * U * scale)
+    Ah, Bh, Ch = host_mat(a), host_mat(b), host_mat(c)
+    L.check(lib.kw_dgemm(q.handle(), None, m, n, k, 0.75, Ah.data(), Ah.leadingDim(), Bh.data(), Bh.leadingDim(),
+                         -1.5, Ch.data(), Ch.leadingDim()))
+    q.wait()
+    assert np.array_equal(Ch.host_view()[:, :n], got)
