@@ -105,6 +105,9 @@ def test_kwbench_native_backend_and_baseline_report(programs, tmp_path):
         recs = list(csv.DictReader(out.open()))
         assert {r["backend"] for r in recs} == backends, argv
         assert len(recs) == 3 * len(backends) and all(r["verified"] == "1" for r in recs), argv
+        from oracle import oracle as O
+        if O.ref_available():  # native rows still parse and re-serialise byte for byte in the reference
+            assert O.ref().kwref_csv_roundtrip(str(out).encode()) == len(recs), argv
         if "--baseline" in argv:
             base = argv[argv.index("--baseline") + 1]
             assert f"median time relative to {base}:" in p.stdout
