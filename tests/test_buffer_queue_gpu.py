@@ -338,3 +338,30 @@ def test_matrix_csv_round_trip_python_mirror(gpu, oracle):
             kw.readBufferCsv(io.StringIO(bad))
     with pytest.raises(kw.UsageError):
         kw.writeBufferCsv(kw.Buffer(HOST, kw.IndexVec(4), 8), io.StringIO())
+
+
+def test_3d_copy_property_over_random_extents_and_residencies(gpu):
+    """The 3-D counterpart of test_buffer.cpp:190-223: random (d0, d1, d2) extents and row
+    alignments on both sides, every residency pair; the copied box carries the source pattern,
+    every other byte of the destination (padding included) keeps its canary."""
+    rng = np.random.default_rng(303)
+    q = kw.Queue(gpu, kw.QueueFlavor.Sync)
+    aligns = (32, 64, 128, 256)
+    pairs = ((HOST, gpu), (gpu, HOST), (gpu, gpu), (HOST, HOST))
+    for it in range(40):
+        box = tuple(1 + int(v) for v in rng.integers(0, 9, size=3))
+        sext = tuple(b + int(rng.integers(0, 3)) for b in box)
+        dext = tuple(b + int(rng.integers(0, 3)) for b in box)
+        sdev, ddev = pairs[it % 4]
+        src = kw.Buffer(sdev, kw.IndexVec(*sext), 8, aligns[int(rng.integers(0, 4))])
+        dst = kw.Buffer(ddev, kw.IndexVec(*dext), 8, aligns[int(rng.integers(0, 4))])
+        put(src, pattern(sext))
+        fill(dst, 0x3C)
+        kw.copyBuffer(q, dst, src, kw.IndexVec(*box))
+        q.wait()
+        r = raw(dst).reshape(dext[0], dext[1], dst.rowPitch())
+        got = r[: box[0], : box[1], : box[2] * 8].copy().view(np.float64)
+        assert np.array_equal(got, pattern(sext)[: box[0], : box[1], : box[2]]), it
+        mask = np.ones_like(r, dtype=bool)
+        mask[: box[0], : box[1], : box[2] * 8] = False
+        assert (r[mask] == 0x3C).all(), it
