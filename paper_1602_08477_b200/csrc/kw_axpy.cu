@@ -18,6 +18,11 @@
 //   Elements >= n are never read or written (axpy.cpp:15-17 tail guard).
 //
 // Bytes per element (algorithmic): read X, read Y, write Y = 3*sizeof(T) (12 B for fp32).
+//
+// Launches use programmatic dependent launch (launch_pdl / griddep_enter): back-to-back steps
+// on a stream overlap one grid's launch with the previous grid's tail, and each grid still reads
+// Y only after the previous one's writes are visible. Host-resident operands (the e2e path) are
+// streamed through device scratch in 32 MiB chunks (run_staged).
 #include "kw_common.cuh"
 
 #include <climits>
