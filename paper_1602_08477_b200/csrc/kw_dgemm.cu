@@ -5,22 +5,25 @@
 //
 // K2 design (FP64 on Blackwell): tcgen05.mma has no f64 kind, so FP64 tensor work is the legacy
 // DMMA.8x8x4 (mma.sync.m8n8k4.f64). Measured on this pool's B200: DMMA 37.2 TFLOP/s vs DFMA
-// 34.1 TFLOP/s peak (tools/probe/probe.cu), and DMMA needs 8x fewer operand registers per FMA,
-// so the block tile is computed with DMMA fed from shared memory.
-//   * block tile BM x BN (128 x 128), k-tile BK = 16, 8 warps each owning a 64 x 32 warp tile
-//     = 8 x 4 DMMA accumulators (64 fp64 registers per lane);
-//   * global -> shared through a STAGES-deep cp.async (LDGSTS) ring, zero-filling ragged
-//     edges in hardware (src-size < cp-size), which is the reference's zero-padded staging
-//     (gemm.cpp:77-92) without any branch in the math loop;
-//   * shared layouts XOR-swizzled at 16-byte granularity so every fragment load (LDS.64, served
-//     per half-warp) touches 16 distinct banks: A[m][k] chunk (k/2) ^ ((m & 3) << 1);
-//     B[k][n] chunk (n/2) ^ ((k & 3) << 1) (ncu: 0 shared-load bank conflicts);
-//   * epilogue fl(fl(alpha*acc) + fl(beta*c)) exactly as gemm.cpp:115 / reference.cpp:24
-//     (C is always read, also for beta == 0);
-//   * blocks rasterised in groups of 8 tile-rows so co-resident CTAs share A and B panels in L2.
+// 34.1 TFLOP/s peak (tools/probe/probe.cu), and DMMA needs 8x fewer operand registers per FMA.
+//   * primary kernel dgemm_tma_kernel: warp-specialised — one producer lane streams k-tiles of
+//     A and B with TMA (cp.async.bulk.tensor, SWIZZLE_128B, hardware zero-fill of ragged edges)
+//     into an mbarrier-synchronised stage ring; consumer warps (64 x 32 warp tiles = 8 x 4 DMMA
+//     accumulators) wait `full`, run the DMMAs, release `empty`; no CTA barrier in the main loop;
+//     setmaxnreg moves registers from the producer warpgroup to the consumers;
+//   * a paired k-slot permutation puts two k-steps of an A fragment in one 16-byte chunk (one
+//     LDS.128), conflict-free under the swizzle; every tile shape ("paired" configs 14-17) feeds
+//     each output element the identical DMMA sequence, so the per-problem tile choice
+//     (pick_config: 64 x 128 at 2 CTAs/SM or 64 x 64 at 3) never changes a bit;
+//   * epilogue fl(fl(alpha*acc) + fl(beta*c)) exactly as gemm.cpp:115 / reference.cpp:24 (C is
+//     always read, also for beta == 0); tiles rasterised in groups of 8 tile-rows for L2 reuse;
+//   * the STREAMED instantiation additionally walks a tile list and waits on per-panel ready
+//     flags (host-operand e2e path, kw_dgemm_e2e.cu);
+//   * dgemm_dmma_kernel: the earlier cp.async (LDGSTS) + __syncthreads family, kept as the path
+//     for operands TMA cannot address (odd leading dimensions) and for the tile sweep.
 // Numerics: per output element the K products are accumulated in ascending k-tile order by
 // DMMA (fused multiply-add), hence |dC| <= (K+4)*2^-53*|C_ref| instead of bit equality
-// (SURVEY.md §7 "Hard parts" 6). K3 below is the bit-exact mode.
+// (SURVEY.md §7 "Hard parts" 6). K3 (naive) and K2-bitwise below are the bit-exact modes.
 #include "kw_common.cuh"
 #include "kw_dgemm_internal.cuh"
 
