@@ -390,6 +390,7 @@ kw_status axpy_entry(kw_queue qh, const kw_workdiv* wd, size_t n, T alpha, const
 {
     KW_CHECK_QUEUE(qh);
     KW_ENQUEUE_LOCK(qh);
+    KW_NVTX("kw axpy");
     auto* q = reinterpret_cast<kw::Queue*>(qh);
     kw_workdiv def;
     if (wd == nullptr) {

@@ -202,6 +202,7 @@ kw_status kw_dgemm_rowsharded(kw_comm c, kw_queue qh, size_t m_local, size_t n, 
 {
     KW_CHECK_QUEUE(qh);
     KW_ENQUEUE_LOCK(qh);
+    KW_NVTX("kw dgemm row-sharded");
     if (!c)
         return kw::usage("dgemm_rowsharded: null communicator");
     auto* q = reinterpret_cast<kw::Queue*>(qh);

@@ -6,6 +6,7 @@
 #include "kw_b200.h"
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <atomic>
 #include <cstdio>
@@ -117,6 +118,15 @@ int pointer_kind(const void* p, int* device);
 
 inline size_t ceil_div(size_t a, size_t b) { return (a + b - 1) / b; }
 
+// NVTX range around one library call (Nsight Systems timelines; header-only NVTX3, a no-op
+// unless a tool is attached) — the tracing hook SURVEY.md §2 lists for the B200 build.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 } // namespace kw
 
 #define KW_CHECK_QUEUE(q)                                                                          \
@@ -131,3 +141,4 @@ inline size_t ceil_div(size_t a, size_t b) { return (a + b - 1) / b; }
 // lock is the FIFO order, and the host-staging scratch/events of one queue are never shared by
 // two in-flight enqueues.
 #define KW_ENQUEUE_LOCK(q) std::lock_guard<std::mutex> kw_enqueue_guard_(reinterpret_cast<kw::Queue*>(q)->enqueue)
+#define KW_NVTX(name) kw::NvtxRange kw_nvtx_range_(name)

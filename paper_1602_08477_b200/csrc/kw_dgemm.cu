@@ -1226,6 +1226,7 @@ kw_status kw_dgemm(kw_queue qh, const kw_workdiv* wd, size_t m, size_t n, size_t
 {
     KW_CHECK_QUEUE(qh);
     KW_ENQUEUE_LOCK(qh);
+    KW_NVTX("kw dgemm");
     auto* q = reinterpret_cast<kw::Queue*>(qh);
     kw_status st = validate_gemm(m, n, k, A, lda, B, ldb, C, ldc);
     if (st != KW_OK)
@@ -1266,6 +1267,7 @@ kw_status kw_dgemm_bitwise(kw_queue qh, const kw_workdiv* wd, size_t m, size_t n
 {
     KW_CHECK_QUEUE(qh);
     KW_ENQUEUE_LOCK(qh);
+    KW_NVTX("kw dgemm (bit-exact mode)");
     auto* q = reinterpret_cast<kw::Queue*>(qh);
     kw_status st = validate_gemm(m, n, k, A, lda, B, ldb, C, ldc);
     if (st != KW_OK)
@@ -1334,6 +1336,7 @@ kw_status kw_dgemm_naive(kw_queue qh, const kw_workdiv* wd, size_t m, size_t n, 
 {
     KW_CHECK_QUEUE(qh);
     KW_ENQUEUE_LOCK(qh);
+    KW_NVTX("kw dgemm (naive)");
     auto* q = reinterpret_cast<kw::Queue*>(qh);
     kw_status st = validate_gemm(m, n, k, A, lda, B, ldb, C, ldc);
     if (st != KW_OK)

@@ -28,6 +28,7 @@ kw_status dgemm_staged(kw::Queue* q, int tile, size_t m, size_t n, size_t k, dou
                        size_t lda, const double* B, size_t ldb, double beta, double* C, size_t ldc, bool a_dev,
                        bool b_dev, bool c_dev)
 {
+    KW_NVTX("kw dgemm e2e: row panels");
     const size_t ldbs = round2(n), ldas = round2(k == 0 ? 1 : k), ldcs = round2(n);
     const size_t row_bytes = (ldas + ldcs) * sizeof(double);
     // Panel height: about m/16 in whole 64-row tiles (the launcher sizes its CTA tile to the
@@ -209,6 +210,7 @@ const StreamMemOps& stream_mem_ops()
 kw_status dgemm_streamed(kw::Queue* q, int tile, size_t m, size_t n, size_t k, double alpha, const double* A,
                          size_t lda, const double* B, size_t ldb, double beta, double* C, size_t ldc, bool* used)
 {
+    KW_NVTX("kw dgemm e2e: streamed");
     *used = false;
     const char* env = std::getenv("KW_E2E_STREAMED");
     if ((env && env[0] == '0') || k == 0 || m > INT_MAX || n > INT_MAX || k > INT_MAX)

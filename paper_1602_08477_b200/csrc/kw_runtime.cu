@@ -421,6 +421,7 @@ kw_status kw_queue_destroy(kw_queue qh)
 
 kw_status kw_queue_wait(kw_queue qh)
 {
+    KW_NVTX("kw queue wait");
     if (!qh)
         return kw::usage("null queue");
     auto* q = reinterpret_cast<Queue*>(qh);
@@ -589,6 +590,7 @@ kw_status kw_copy(kw_queue qh, void* dst, size_t dst_pitch, const size_t dst_ext
 {
     KW_CHECK_QUEUE(qh);
     KW_ENQUEUE_LOCK(qh);
+    KW_NVTX("kw copy");
     auto* q = reinterpret_cast<Queue*>(qh);
     if (dim < 1 || dim > 3)
         return kw::usage("copy: buffer and extent dimensionalities must match");
