@@ -7,6 +7,7 @@
 #include "check.hpp"
 
 #include <algorithm>
+#include <cmath>
 #include <chrono>
 #include <cstring>
 #include <random>
@@ -559,6 +560,142 @@ TEST_CASE("paper's one-to-one tiled DGEMM: functor vs native CUDA, same bits, >=
         CHECK(same);
         CHECK(native / functor >= 0.94); // the paper reports >= 94 % for this translation on K20
     }
+}
+
+// The paper's performance-portability experiment: ONE single-source tiled
+// DGEMM kernel using every level of the hierarchy — grid of blocks, 16 x 16 threads per block,
+// E x E elements per thread (getWorkDiv<Thread, Elems>), shared-memory tiles — measured against
+// the architecture's FP64 peak (≈ 20 % on K20/K80/Xeon/Opteron in the paper).
+template <int E>
+struct PaperHierarchicalGemm {
+    static constexpr int T = 16, BK = 16, BM = T * E;
+    static constexpr std::size_t sharedMemBytes = static_cast<std::size_t>(2 * BM * (BK + 1)) * sizeof(double);
+    __device__ void operator()(const AccContext& acc, std::size_t n, double alpha, double beta, BufferView a,
+                               BufferView b, BufferView c) const
+    {
+        const IndexVec elems = workdiv::getWorkDiv<Thread, Elems>(acc); // (E, E) by construction
+        const IndexVec blk = idx::getIdx<Grid, Blocks>(acc);
+        const IndexVec thr = idx::getIdx<Block, Threads>(acc);
+        if (elems.get(0) != static_cast<std::size_t>(E) || elems.get(1) != static_cast<std::size_t>(E)) {
+            failTask(acc, 1);
+            return;
+        }
+        double* sa = allocSharedMem<double>(acc, BM * (BK + 1)); // [BM][BK+1], padded
+        double* sb = allocSharedMem<double>(acc, BK * (BM + 1)); // [BK][BN+1]
+        const int ty = static_cast<int>(thr.get(0)), tx = static_cast<int>(thr.get(1)), tid = ty * T + tx;
+        const std::size_t row0 = blk.get(0) * BM, col0 = blk.get(1) * BM;
+        const double* A = a.rowData<double>(0);
+        const double* B = b.rowData<double>(0);
+        const std::size_t lda = a.leadingDim<double>(), ldb = b.leadingDim<double>();
+        double accum[E][E];
+#pragma unroll
+        for (int i = 0; i < E; ++i)
+#pragma unroll
+            for (int j = 0; j < E; ++j)
+                accum[i][j] = 0.0;
+        for (std::size_t k0 = 0; k0 < n; k0 += BK) {
+            for (int e = tid; e < BM * BK; e += T * T) { // A tile: BM rows x BK
+                const int r = e / BK, kk = e % BK;
+                const std::size_t gr = row0 + r, gk = k0 + kk;
+                sa[r * (BK + 1) + kk] = gr < n && gk < n ? A[gr * lda + gk] : 0.0;
+            }
+            for (int e = tid; e < BK * BM; e += T * T) { // B tile: BK rows x BN
+                const int kk = e / BM, col = e % BM;
+                const std::size_t gk = k0 + kk, gc = col0 + col;
+                sb[kk * (BM + 1) + col] = gk < n && gc < n ? B[gk * ldb + gc] : 0.0;
+            }
+            syncBlockThreads(acc);
+#pragma unroll
+            for (int kk = 0; kk < BK; ++kk) {
+                double av[E], bv[E];
+#pragma unroll
+                for (int i = 0; i < E; ++i)
+                    av[i] = sa[(ty + T * i) * (BK + 1) + kk];
+#pragma unroll
+                for (int j = 0; j < E; ++j)
+                    bv[j] = sb[kk * (BM + 1) + tx + T * j];
+#pragma unroll
+                for (int i = 0; i < E; ++i)
+#pragma unroll
+                    for (int j = 0; j < E; ++j)
+                        accum[i][j] = fma(av[i], bv[j], accum[i][j]);
+            }
+            syncBlockThreads(acc);
+        }
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+            const std::size_t r = row0 + ty + T * i;
+            if (r >= n)
+                continue;
+            double* crow = c.rowData<double>(r);
+#pragma unroll
+            for (int j = 0; j < E; ++j) {
+                const std::size_t col = col0 + tx + T * j;
+                if (col < n)
+                    crow[col] = alpha * accum[i][j] + beta * crow[col];
+            }
+        }
+    }
+};
+KW_DEVICE_FUNCTOR(PaperHierarchicalGemm<4>)
+KW_DEVICE_FUNCTOR(PaperHierarchicalGemm<8>)
+
+template <int E>
+double run_hierarchical(std::size_t n, Buffer& a, Buffer& b, Buffer& c)
+{
+    const WorkDiv wd(IndexVec((n + 16 * E - 1) / (16 * E), (n + 16 * E - 1) / (16 * E)), IndexVec(16, 16), IndexVec(E, E));
+    executeTask(kBk, wd, PaperHierarchicalGemm<E>{}, n, 1.0, 0.0, view(a), view(b), view(c));
+    std::vector<double> t;
+    for (int r = 0; r < 3; ++r) {
+        const auto t0 = std::chrono::steady_clock::now();
+        executeTask(kBk, wd, PaperHierarchicalGemm<E>{}, n, 1.0, 0.0, view(a), view(b), view(c));
+        t.push_back(std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+    }
+    std::sort(t.begin(), t.end());
+    return 2.0 * n * n * n / t[1] / 1e12;
+}
+
+TEST_CASE("paper's single-source hierarchical DGEMM functor: fraction of FP64 peak (PAPER.md:740-753)")
+{
+    const std::size_t n = 4096;
+    Buffer ha(Device::host(), IndexVec(n, n), 8), hb(Device::host(), IndexVec(n, n), 8);
+    std::mt19937_64 rng(4096);
+    for (std::size_t r = 0; r < n; ++r)
+        for (std::size_t col = 0; col < n; ++col) {
+            ha.rowData<double>(r)[col] = static_cast<double>(rng() >> 11) * 0x1.0p-53 * 10.0;
+            hb.rowData<double>(r)[col] = static_cast<double>(rng() >> 11) * 0x1.0p-53 * 10.0;
+        }
+    Buffer a(kGpu, IndexVec(n, n), 8), b(kGpu, IndexVec(n, n), 8), c(kGpu, IndexVec(n, n), 8), ref(kGpu, IndexVec(n, n), 8);
+    {
+        Queue q(kGpu, QueueFlavor::Sync);
+        copyBuffer(q, a, ha, ha.extent());
+        copyBuffer(q, b, hb, hb.extent());
+        kw_memset(q.native(), ref.data(), 0, ref.storageBytes());
+    }
+    executeTask(kBk, kernels::gemmTiledWorkDiv(kBk, n, n, 128), kernels::GemmTiledKernel{},
+                kernels::GemmArgs{n, n, n, 1.0, 0.0, &a, &b, &ref});
+    const double peak = 37.22; // nominal FP64 (DMMA measured 37.16, DFMA 34.1: tools/probe/probe.cu)
+    double best = 0.0;         // the paper picks the division per architecture: the best one counts
+    for (int e : {4, 8}) {
+        const double tf = e == 4 ? run_hierarchical<4>(n, a, b, c) : run_hierarchical<8>(n, a, b, c);
+        // same product as the library's DGEMM within both kernels' (K+4)u bounds
+        Buffer hc(Device::host(), IndexVec(n, n), 8), hr(Device::host(), IndexVec(n, n), 8);
+        Queue q(kGpu, QueueFlavor::Sync);
+        copyBuffer(q, hc, c, c.extent());
+        copyBuffer(q, hr, ref, ref.extent());
+        double worst = 0.0;
+        for (std::size_t r = 0; r < n; r += 97)
+            for (std::size_t col = 0; col < n; ++col) {
+                const double x = hc.rowData<double>(r)[col], y = hr.rowData<double>(r)[col];
+                worst = std::max(worst, std::fabs(x - y) / (std::fabs(y) * (2.0 * (n + 4)) * 0x1.0p-53));
+            }
+        std::printf("  single-source hierarchical DGEMM n=%zu, 16x16 threads x %dx%d elements: %.2f TFLOP/s = %.1f %% of "
+                    "FP64 peak (paper: ~20 %%); max err / 2(K+4)u = %.3f\n",
+                    n, e, e, tf, 100.0 * tf / peak, worst);
+        CHECK(worst <= 1.0);
+        best = std::max(best, tf / peak);
+    }
+    CHECK(best >= 0.20);
 }
 
 TEST_CASE("criterion 08 analogue: a generic functor runs within 1.5x of the native kernel (acceptance.cpp:546-587)")
