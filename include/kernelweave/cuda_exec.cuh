@@ -229,12 +229,14 @@ struct DeviceLauncher {
         static thread_local std::size_t cachedResident = 0;
         if (cachedThreads != threads || cachedDev != dev) {
             int perSm = 0, sms = 0;
-            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perSm, functorKernel<Kernel, Args...>, threads, smem) !=
-                    cudaSuccess ||
-                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+            if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) {
                 cudaGetLastError();
+                sms = 148;
+            }
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perSm, functorKernel<Kernel, Args...>, threads, smem) !=
+                cudaSuccess) {
+                cudaGetLastError(); // e.g. a block that cannot fit: the launch itself reports it
                 perSm = 1;
-                sms = 1;
             }
             cachedResident = static_cast<std::size_t>(perSm > 0 ? perSm : 1) * static_cast<std::size_t>(sms);
             cachedThreads = threads;
