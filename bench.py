@@ -456,7 +456,8 @@ def run_dgemm(args, dist, kw, L, lib, dev, q, sampler) -> dict:
             entry["e2e"] = {"value": round(2 * size ** 3 * e2e_steps / e2e_s / 1e12, 3), "unit": "TFLOP/s",
                             "steps": e2e_steps, "h2d_bytes_per_step": 3 * size * size * 8,
                             "d2h_bytes_per_step": size * size * 8,
-                            "schedule": ("streamed: square-growth panel uploads into one persistent kernel"
+                            "schedule": ("streamed: square-growth panel uploads into one persistent kernel, "
+                                          "k split 1/4 + 3/4 (first pass on the first quarter of A/B)"
                                          if streamed else "row panels of A/C, B streamed in column panels")}
             bw_task = None
             if size == 8192:

@@ -401,7 +401,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmParams p)
 {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1 KiB alignment (128B-swizzled TMA boxes) by pointer arithmetic on the __shared__ array, not
+    // through an integer cast: the compiler must still see a shared-space pointer, so fragment
+    // loads compile to LDS. (Through uintptr_t they became generic LD.E — slower, and not ordered
+    // before the empty-barrier arrive, so a refill could overwrite a stage still being read.)
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
     uint64_t* empty = full + Cfg::STAGES;
 
@@ -411,13 +415,17 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     // stages while the consumers run the epilogue). All CTAs at step j work on consecutive tile
     // ids, which keeps the L2 locality of the rasterisation.
     constexpr int GROUP = 8;
-    const int ntiles = p.tiles_m * p.tiles_n;
-    auto origin = [&](int tile, int& bm, int& bn) {
+    const int ntiles = STREAMED ? p.tile_list[0].x : p.tiles_m * p.tiles_n;
+    const int ktiles = (p.k + Cfg::BK - 1) / Cfg::BK;
+    // Tile origin and k-tile range [kt0, kt1) of work item `tile`; false = padding entry.
+    auto origin = [&](int tile, int& bm, int& bn, int& kt0, int& kt1) {
         if constexpr (STREAMED) {
-            const int2 v = p.tile_list[tile];
+            const int4 v = p.tile_list[1 + tile];
             bm = v.x * Cfg::BM;
             bn = v.y * Cfg::BN;
-            return;
+            kt0 = v.z;
+            kt1 = v.w;
+            return v.x >= 0;
         }
         const int per_group = GROUP * p.tiles_n;
         const int group = tile / per_group;
@@ -426,6 +434,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
         const int in_group = tile - group * per_group;
         bm = (first_m + in_group % gsize) * Cfg::BM;
         bn = (in_group / gsize) * Cfg::BN;
+        kt0 = 0;
+        kt1 = ktiles;
+        return true;
     };
 
     const int tid = threadIdx.x;
@@ -438,7 +449,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
         fence_mbar_init();
     }
     __syncthreads();
-    const int ktiles = (p.k + Cfg::BK - 1) / Cfg::BK;
 
     if (warp >= Cfg::CONSUMERS) {
         // ---------------- producer warpgroup ----------------
@@ -449,17 +459,19 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
             tma_prefetch_desc(&tmB);
             int it = 0; // k-tile iteration counter across this CTA's tiles (ring position)
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-                int bm, bn;
-                origin(tile, bm, bn);
+                int bm, bn, kt0, kt1;
+                if (!origin(tile, bm, bn, kt0, kt1))
+                    continue;
                 if constexpr (STREAMED) {
-                    // A row panel and B column panel of this tile resident? (The C block is
-                    // waited for before the last k-tile, below.)
-                    wait_ready(p.ready + bm / p.panel_rows);
-                    wait_ready(p.ready + p.npr + bn / p.panel_cols);
+                    // A row panel and B column panel of this tile (of its pass) resident? (The C
+                    // block is waited for before the last k-tile, below.)
+                    const uint32_t* pass_flags = p.ready + (kt0 > 0 ? p.npr + p.npc : 0);
+                    wait_ready(pass_flags + bm / p.panel_rows);
+                    wait_ready(pass_flags + p.npr + bn / p.panel_cols);
                     // the panels were written by the copy engine; order the TMA reads after
                     asm volatile("fence.proxy.async.global;\n" ::: "memory");
                 }
-                for (int kt = 0; kt < ktiles; ++kt, ++it) {
+                for (int kt = kt0; kt < kt1; ++kt, ++it) {
                     const int s = it % Cfg::STAGES;
                     const uint32_t r = static_cast<uint32_t>(it / Cfg::STAGES);
                     mbar_wait(&empty[s], (r & 1u) ^ 1u);
@@ -469,7 +481,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
                         // C block's flag here orders those reads after its upload, and leaves
                         // the upload a whole tile of slack.
                         if (kt == ktiles - 1)
-                            wait_ready(p.ready + p.npr + p.npc + (bm / p.panel_rows) * p.npc + bn / p.panel_cols);
+                            wait_ready(p.ready + 2 * (p.npr + p.npc) + (bm / p.panel_rows) * p.npc +
+                                       bn / p.panel_cols);
                     }
                     mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
                     const uint32_t sa = smem_u32(smem + s * Cfg::STAGE_BYTES);
@@ -514,15 +527,36 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
 
     const bool c_vec = (p.ldc % 2 == 0) && (reinterpret_cast<uintptr_t>(p.c) % 16 == 0);
     int it0 = 0; // ring position of this tile's first k-tile
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it0 += ktiles) {
-    int bm, bn;
-    origin(tile, bm, bn);
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    int bm, bn, kt0, kt1;
+    if (!origin(tile, bm, bn, kt0, kt1))
+        continue;
+    const int nkt = kt1 - kt0;
+    // k-split (streamed only): this thread's accumulators of the tile, parked between passes;
+    // item i of lane l at ((tile * CONSUMERS + warp) * MT*NT + i) * 32 + l (coalesced double2).
+    double2* park = nullptr;
+    if constexpr (STREAMED) {
+        const size_t tid_tile = static_cast<size_t>(bm / Cfg::BM) * p.tiles_n + bn / Cfg::BN;
+        park = reinterpret_cast<double2*>(p.partial) + (tid_tile * Cfg::CONSUMERS + warp) * (Cfg::MT * Cfg::NT) * 32 + lane;
+    }
     double acc[Cfg::MT][Cfg::NT][2];
 #pragma unroll
     for (int i = 0; i < Cfg::MT; ++i)
 #pragma unroll
         for (int j = 0; j < Cfg::NT; ++j)
             acc[i][j][0] = acc[i][j][1] = 0.0;
+    if constexpr (STREAMED) {
+        if (kt0 > 0) {
+#pragma unroll
+            for (int i = 0; i < Cfg::MT; ++i)
+#pragma unroll
+                for (int j = 0; j < Cfg::NT; ++j) {
+                    const double2 v = __ldcg(park + (i * Cfg::NT + j) * 32);
+                    acc[i][j][0] = v.x;
+                    acc[i][j][1] = v.y;
+                }
+        }
+    }
 
     if constexpr (Cfg::PAIRED) {
         // A pair fragments: one double2 per (i, q) = k-steps 2q and 2q+1; B per k-step.
@@ -554,13 +588,13 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
         // one k-step ahead.
         double2 a2[2][Cfg::MT];
         double bf[2][Cfg::NT];
-        if (ktiles > 0) {
+        if (nkt > 0) {
             const int s0 = it0 % Cfg::STAGES;
             mbar_wait(&full[s0], static_cast<uint32_t>(it0 / Cfg::STAGES) & 1u);
             load_a2(smem + s0 * Cfg::STAGE_BYTES, 0, a2[0]);
             load_b(smem + s0 * Cfg::STAGE_BYTES, 0, bf[0]);
         }
-        for (int kt = 0; kt < ktiles; ++kt) {
+        for (int kt = 0; kt < nkt; ++kt) {
             const int s = (it0 + kt) % Cfg::STAGES;
             const uint8_t* sa = smem + s * Cfg::STAGE_BYTES;
             const uint8_t* sa2 = sa;
@@ -574,10 +608,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
                     load_b(sa, ks + 1, bf[bn2]);
                 }
                 else {
-                    __syncwarp();
-                    if (lane == 0)
-                        mbar_arrive(&empty[s]);
-                    if (kt + 1 < ktiles) {
+                    if (kt + 1 < nkt) {
                         const int s2 = (it0 + kt + 1) % Cfg::STAGES;
                         mbar_wait(&full[s2], static_cast<uint32_t>((it0 + kt + 1) / Cfg::STAGES) & 1u);
                         sa2 = smem + s2 * Cfg::STAGE_BYTES;
@@ -590,6 +621,15 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
 #pragma unroll
                     for (int j = 0; j < Cfg::NT; ++j)
                         dmma_8x8x4(acc[i][j][0], acc[i][j][1], h ? a2[q][i].y : a2[q][i].x, bf[bc][j]);
+                if (ks == 3) {
+                    // Release stage s only now: these DMMAs consumed its last fragments, so
+                    // every LDS from it has returned. (An arrive right after issuing the LDS
+                    // let the refill's TMA overwrite the stage under a still-pending LDS —
+                    // seen as k-step-sized errors when tiles turn over quickly.)
+                    __syncwarp();
+                    if (lane == 0)
+                        mbar_arrive(&empty[s]);
+                }
             }
         }
     }
@@ -598,12 +638,12 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     // first k-step) are loaded before the DMMAs of the current one are issued, so LDS latency
     // hides behind 32 DMMAs instead of stalling the warp.
     double af[2][Cfg::MT], bf[2][Cfg::NT];
-    if (ktiles > 0) {
+    if (nkt > 0) {
         const int s0 = it0 % Cfg::STAGES;
         mbar_wait(&full[s0], static_cast<uint32_t>(it0 / Cfg::STAGES) & 1u);
         load_frags(smem + s0 * Cfg::STAGE_BYTES, 0, af[0], bf[0]);
     }
-    for (int kt = 0; kt < ktiles; ++kt) {
+    for (int kt = 0; kt < nkt; ++kt) {
         const int s = (it0 + kt) % Cfg::STAGES;
         const uint8_t* sa = smem + s * Cfg::STAGE_BYTES;
 #pragma unroll
@@ -613,12 +653,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
                 load_frags(sa, ks + 1, af[nxt], bf[nxt]);
             }
             else {
-                // Every fragment of stage s is in registers: release the slot to the producer,
-                // then wait for the next stage (if any) and prefetch its first k-step.
-                __syncwarp();
-                if (lane == 0)
-                    mbar_arrive(&empty[s]);
-                if (kt + 1 < ktiles) {
+                // wait for the next stage (if any) and prefetch its first k-step
+                if (kt + 1 < nkt) {
                     const int s2 = (it0 + kt + 1) % Cfg::STAGES;
                     mbar_wait(&full[s2], static_cast<uint32_t>((it0 + kt + 1) / Cfg::STAGES) & 1u);
                     load_frags(smem + s2 * Cfg::STAGE_BYTES, 0, af[nxt], bf[nxt]);
@@ -629,9 +665,28 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
 #pragma unroll
                 for (int j = 0; j < Cfg::NT; ++j)
                     dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[cur][i], bf[cur][j]);
+            if (ks == 3) {
+                // stage s fully consumed (see the paired loop): release it
+                __syncwarp();
+                if (lane == 0)
+                    mbar_arrive(&empty[s]);
+            }
         }
     }
 
+    }
+    it0 += nkt;
+    if constexpr (STREAMED) {
+        if (kt1 < ktiles) {
+            // first pass of a k-split: park the accumulators; the second pass (same CTA, same
+            // thread, later in this loop) reloads them and runs the epilogue
+#pragma unroll
+            for (int i = 0; i < Cfg::MT; ++i)
+#pragma unroll
+                for (int j = 0; j < Cfg::NT; ++j)
+                    __stcg(park + (i * Cfg::NT + j) * 32, make_double2(acc[i][j][0], acc[i][j][1]));
+            continue;
+        }
     }
 
 #pragma unroll
@@ -663,7 +718,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
         __syncwarp();
         if (lane == 0) {
             __threadfence_system();
-            atomicAdd(p.done + (bm / p.panel_rows) * p.npc + bn / p.panel_cols, 1u);
+            uint32_t* done = p.ready + 2 * (p.npr + p.npc) + p.npr * p.npc;
+            atomicAdd(done + (bm / p.panel_rows) * p.npc + bn / p.panel_cols, 1u);
         }
     }
     } // tile loop
@@ -1138,7 +1194,7 @@ GemmParams make_params(size_t m, size_t n, size_t k, double alpha, const double*
     p.tiles_m = p.tiles_n = 0;
     p.tile_list = nullptr;
     p.ready = nullptr;
-    p.done = nullptr;
+    p.partial = nullptr;
     p.panel_rows = p.panel_cols = 1;
     p.npr = p.npc = 0;
     return p;
@@ -1170,6 +1226,15 @@ StreamedShape streamed_shape(int cfg)
 {
     return cfg == kCfgWide ? StreamedShape{Tma64x128x2p::BM, Tma64x128x2p::BN, Tma64x128x2p::CONSUMERS}
                            : StreamedShape{Tma64x64x3p::BM, Tma64x64x3p::BN, Tma64x64x3p::CONSUMERS};
+}
+int streamed_grid(int cfg, const GemmParams& p)
+{
+    // launch_tma<.., PERSISTENT = true, ..>'s grid: min(tiles, resident CTAs)
+    const StreamedShape sh = streamed_shape(cfg);
+    const long long tiles = static_cast<long long>(kw::ceil_div(p.m, sh.bm)) * kw::ceil_div(p.n, sh.bn);
+    const long long resident =
+        static_cast<long long>(sm_count()) * (cfg == kCfgWide ? Tma64x128x2p::MIN_BLOCKS : Tma64x64x3p::MIN_BLOCKS);
+    return static_cast<int>(tiles > resident ? resident : tiles);
 }
 kw_status launch_streamed(cudaStream_t s, int cfg, const GemmParams& p)
 {

@@ -239,11 +239,24 @@ kw_status dgemm_streamed(kw::Queue* q, int tile, size_t m, size_t n, size_t k, d
     const StreamedShape shape = streamed_shape(cfg);
     const int bm = shape.bm, bn = shape.bn;
     const uint32_t consumers = shape.consumers;
-    const size_t tiles = kw::ceil_div(m, bm) * kw::ceil_div(n, bn);
-    const size_t nflags = npr + npc + npr * npc, ndone = npr * npc;
+    const size_t tiles_m = kw::ceil_div(m, bm), tiles_n = kw::ceil_div(n, bn), tiles = tiles_m * tiles_n;
+    // k-split (KW_E2E_KSPLIT = d, default 4; 0/1 = off): a first pass over k-tiles [0, kts), kts =
+    // ktiles / d, needs only the first K0 = 16 kts columns of A and rows of B, so d times less
+    // upload per unit of work than the full-depth panels — the kernel reaches full rate while
+    // most of A and B are still in flight. Its accumulators are parked in `partial` and picked up
+    // by the second pass, which streams the rest of A and B and all of C exactly as the
+    // single-pass schedule does.
+    const size_t ktiles = kw::ceil_div(k, static_cast<size_t>(16));
+    const char* ke = std::getenv("KW_E2E_KSPLIT");
+    const long kd = ke ? std::atol(ke) : 4;
+    const size_t kts = kd > 1 ? ktiles / static_cast<size_t>(kd) : 0;
+    const size_t K0 = kts * 16;
+    const int passes = kts > 0 ? 2 : 1;
+    const size_t nflags = 2 * (npr + npc) + npr * npc, ndone = npr * npc;
     const size_t mat_bytes = (m * ldas + k * ldbs + m * ldcs) * sizeof(double);
+    const size_t part_bytes = passes > 1 ? tiles * bm * bn * sizeof(double) : 0;
     const size_t aux_bytes = (nflags + ndone) * sizeof(uint32_t) + 512;
-    if (q->scratch_bytes < mat_bytes + aux_bytes) {
+    if (q->scratch_bytes < mat_bytes + part_bytes + aux_bytes) {
         // growing the scratch: only when the operands fit comfortably (a resource-manager query,
         // so not on every call)
         size_t free_b = 0, total_b = 0;
@@ -251,17 +264,19 @@ kw_status dgemm_streamed(kw::Queue* q, int tile, size_t m, size_t n, size_t k, d
             cudaGetLastError();
             return KW_OK;
         }
-        if (static_cast<double>(mat_bytes + aux_bytes) > 0.8 * static_cast<double>(free_b + q->scratch_bytes))
+        if (static_cast<double>(mat_bytes + part_bytes + aux_bytes) >
+            0.8 * static_cast<double>(free_b + q->scratch_bytes))
             return KW_OK; // too large to hold whole: the row-panel ring schedule
     }
-    kw_status st = kw::ensure_scratch(q, mat_bytes + aux_bytes);
+    kw_status st = kw::ensure_scratch(q, mat_bytes + part_bytes + aux_bytes);
     if (st != KW_OK)
         return st;
     char* base = static_cast<char*>(q->scratch);
     double* Ad = reinterpret_cast<double*>(base);
     double* Bd = Ad + m * ldas;
     double* Cd = Bd + k * ldbs;
-    char* tail = reinterpret_cast<char*>(Cd + m * ldcs);
+    double* part = Cd + m * ldcs; // 16-byte aligned: every extent above is even
+    char* tail = reinterpret_cast<char*>(part) + part_bytes;
     tail = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(tail) + 255) & ~uintptr_t(255));
     uint32_t* ready = reinterpret_cast<uint32_t*>(tail);
     uint32_t* done = ready + nflags;
@@ -272,9 +287,11 @@ kw_status dgemm_streamed(kw::Queue* q, int tile, size_t m, size_t n, size_t k, d
     static std::atomic<int> mem_ops_ok{-1};
     if (mem_ops_ok.load() == 0)
         return KW_OK;
+    const size_t grid = static_cast<size_t>(streamed_grid(cfg, p));
 
     // The growth order: A_0, B_0, then add a B column panel while it is not ahead of the A row
-    // panels, else an A row panel; each addition completes the C blocks of its row/column.
+    // panels, else an A row panel; each addition completes the C blocks of its row/column. Both
+    // passes follow it (pass 0 with K0-deep panels and no C).
     struct Step {
         bool is_a;
         size_t idx;
@@ -297,19 +314,30 @@ kw_status dgemm_streamed(kw::Queue* q, int tile, size_t m, size_t n, size_t k, d
             }
         }
     }
-    std::vector<int2> order;
-    order.reserve(tiles);
-    for (const auto& bl : blocks) {
-        const size_t r0 = bl.first * R, r1 = std::min(m, r0 + R), c0 = bl.second * W, c1 = std::min(n, c0 + W);
-        for (size_t tr = r0 / bm; tr < kw::ceil_div(r1, bm); ++tr)
-            for (size_t tc = c0 / bn; tc < kw::ceil_div(c1, bn); ++tc)
-                order.push_back(make_int2(static_cast<int>(tr), static_cast<int>(tc)));
+    // Work list: pass 0 (if any) padded to a multiple of the grid, so entry e and entry
+    // e + len0 — the two passes of one tile — run on the same CTA (CTA = entry mod grid).
+    std::vector<int4> order(1); // [0] = header: entry count
+    auto add_pass = [&](int kt0, int kt1) {
+        for (const auto& bl : blocks) {
+            const size_t r0 = bl.first * R, r1 = std::min(m, r0 + R), c0 = bl.second * W, c1 = std::min(n, c0 + W);
+            for (size_t tr = r0 / bm; tr < kw::ceil_div(r1, bm); ++tr)
+                for (size_t tc = c0 / bn; tc < kw::ceil_div(c1, bn); ++tc)
+                    order.push_back(make_int4(static_cast<int>(tr), static_cast<int>(tc), kt0, kt1));
+        }
+    };
+    if (passes > 1) {
+        add_pass(0, static_cast<int>(kts));
+        while ((order.size() - 1) % grid != 0)
+            order.push_back(make_int4(-1, 0, 0, 0));
     }
-    if (order.size() != tiles)
+    const size_t len0 = order.size();
+    add_pass(static_cast<int>(kts), static_cast<int>(ktiles));
+    if (order.size() - len0 != tiles || order.size() > static_cast<size_t>(INT_MAX))
         return kw::task_fail(q, "dgemm (streamed): tile order does not cover the output");
+    order[0] = make_int4(static_cast<int>(order.size() - 1), 0, 0, 0);
 
-    // The tile order goes up from a pinned copy, once per (scratch, shape, panel grid, tile).
-    const size_t key[8] = {m, n, R, W, static_cast<size_t>(cfg), 1, 0, 0};
+    // The tile order goes up from a pinned copy, once per (scratch, shape, panel grid, tile, split).
+    const size_t key[8] = {m, n, R, W, static_cast<size_t>(cfg), 2, kts, grid};
     const bool order_current = std::equal(key, key + 8, q->order_key);
     auto flag = [&](size_t idx) { return reinterpret_cast<CUdeviceptr>(ready + idx); };
     cudaError_t e = cudaMemsetAsync(ready, 0, (nflags + ndone) * sizeof(uint32_t), q->stream);
@@ -318,7 +346,7 @@ kw_status dgemm_streamed(kw::Queue* q, int tile, size_t m, size_t n, size_t k, d
             e = cudaEventSynchronize(q->ev_order); // the previous upload still reads order_host
         else
             e = cudaEventCreateWithFlags(&q->ev_order, cudaEventDisableTiming);
-        const size_t bytes = tiles * sizeof(int2);
+        const size_t bytes = order.size() * sizeof(int4);
         if (e == cudaSuccess && q->order_bytes < bytes) {
             // earlier kernels on this queue may still read order_dev
             e = cudaStreamSynchronize(q->stream);
@@ -372,40 +400,47 @@ kw_status dgemm_streamed(kw::Queue* q, int tile, size_t m, size_t n, size_t k, d
         cudaEventRecord(tev[0], q->stream);
     }
 
-    // 1. uploads + ready flags (copy stream)
+    // 1. uploads + ready flags (copy stream): pass 0's K0-deep panels, then the final pass's
+    // panels (columns / rows K0.. of A / B) with the C blocks they complete
     CUresult ce = CUDA_SUCCESS;
-    size_t a = 0, b = 0;
-    for (const Step& stp : steps) {
-        if (e != cudaSuccess || ce != CUDA_SUCCESS)
-            break;
-        if (stp.is_a) {
-            const size_t r0 = stp.idx * R, rows = std::min(m, r0 + R) - r0;
-            e = cudaMemcpy2DAsync(Ad + r0 * ldas, ldas * 8, A + r0 * lda, lda * 8, k * 8, rows,
-                                  cudaMemcpyHostToDevice, q->h2d);
-            if (e == cudaSuccess)
-                ce = ops.write(q->h2d, flag(stp.idx), 1, 0);
-            if (e == cudaSuccess && ce == CUDA_SUCCESS && b > 0) {
-                const size_t cols = std::min(n, b * W);
-                e = cudaMemcpy2DAsync(Cd + r0 * ldcs, ldcs * 8, C + r0 * ldc, ldc * 8, cols * 8, rows,
+    for (int pass = passes > 1 ? 0 : 1; pass < 2; ++pass) {
+        const bool final_pass = pass == 1;
+        const size_t k0 = final_pass ? K0 : 0, kw_ = final_pass ? k - K0 : K0;
+        const size_t fbase = passes > 1 && final_pass ? npr + npc : 0; // kernel: kt0 > 0 -> pass-1 flags
+        size_t a = 0, b = 0;
+        for (const Step& stp : steps) {
+            if (e != cudaSuccess || ce != CUDA_SUCCESS)
+                break;
+            if (stp.is_a) {
+                const size_t r0 = stp.idx * R, rows = std::min(m, r0 + R) - r0;
+                e = cudaMemcpy2DAsync(Ad + r0 * ldas + k0, ldas * 8, A + r0 * lda + k0, lda * 8, kw_ * 8, rows,
                                       cudaMemcpyHostToDevice, q->h2d);
-                for (size_t j = 0; j < b && e == cudaSuccess && ce == CUDA_SUCCESS; ++j)
-                    ce = ops.write(q->h2d, flag(npr + npc + stp.idx * npc + j), 1, 0);
+                if (e == cudaSuccess)
+                    ce = ops.write(q->h2d, flag(fbase + stp.idx), 1, 0);
+                if (final_pass && e == cudaSuccess && ce == CUDA_SUCCESS && b > 0) {
+                    const size_t cols = std::min(n, b * W);
+                    e = cudaMemcpy2DAsync(Cd + r0 * ldcs, ldcs * 8, C + r0 * ldc, ldc * 8, cols * 8, rows,
+                                          cudaMemcpyHostToDevice, q->h2d);
+                    for (size_t j = 0; j < b && e == cudaSuccess && ce == CUDA_SUCCESS; ++j)
+                        ce = ops.write(q->h2d, flag(2 * (npr + npc) + stp.idx * npc + j), 1, 0);
+                }
+                ++a;
             }
-            ++a;
-        }
-        else {
-            const size_t c0 = stp.idx * W, cols = std::min(n, c0 + W) - c0;
-            e = cudaMemcpy2DAsync(Bd + c0, ldbs * 8, B + c0, ldb * 8, cols * 8, k, cudaMemcpyHostToDevice, q->h2d);
-            if (e == cudaSuccess)
-                ce = ops.write(q->h2d, flag(npr + stp.idx), 1, 0);
-            if (e == cudaSuccess && ce == CUDA_SUCCESS && a > 0) {
-                const size_t rows = std::min(m, a * R);
-                e = cudaMemcpy2DAsync(Cd + c0, ldcs * 8, C + c0, ldc * 8, cols * 8, rows, cudaMemcpyHostToDevice,
-                                      q->h2d);
-                for (size_t i = 0; i < a && e == cudaSuccess && ce == CUDA_SUCCESS; ++i)
-                    ce = ops.write(q->h2d, flag(npr + npc + i * npc + stp.idx), 1, 0);
+            else {
+                const size_t c0 = stp.idx * W, cols = std::min(n, c0 + W) - c0;
+                e = cudaMemcpy2DAsync(Bd + k0 * ldbs + c0, ldbs * 8, B + k0 * ldb + c0, ldb * 8, cols * 8, kw_,
+                                      cudaMemcpyHostToDevice, q->h2d);
+                if (e == cudaSuccess)
+                    ce = ops.write(q->h2d, flag(fbase + npr + stp.idx), 1, 0);
+                if (final_pass && e == cudaSuccess && ce == CUDA_SUCCESS && a > 0) {
+                    const size_t rows = std::min(m, a * R);
+                    e = cudaMemcpy2DAsync(Cd + c0, ldcs * 8, C + c0, ldc * 8, cols * 8, rows, cudaMemcpyHostToDevice,
+                                          q->h2d);
+                    for (size_t i = 0; i < a && e == cudaSuccess && ce == CUDA_SUCCESS; ++i)
+                        ce = ops.write(q->h2d, flag(2 * (npr + npc) + i * npc + stp.idx), 1, 0);
+                }
+                ++b;
             }
-            ++b;
         }
     }
     if (e != cudaSuccess || ce != CUDA_SUCCESS)
@@ -417,9 +452,9 @@ kw_status dgemm_streamed(kw::Queue* q, int tile, size_t m, size_t n, size_t k, d
         cudaEventRecord(tev[1], q->stream);
 
     // 2. the persistent kernel (queue stream)
-    p.tile_list = static_cast<const int2*>(q->order_dev);
-    p.ready = ready;
-    p.done = done;
+    p.tile_list = static_cast<const int4*>(q->order_dev);
+    p.ready = ready; // done[] follows the flags (GemmParams)
+    p.partial = part;
     p.panel_rows = static_cast<int>(R);
     p.panel_cols = static_cast<int>(W);
     p.npr = static_cast<int>(npr);

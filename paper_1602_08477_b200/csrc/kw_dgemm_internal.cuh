@@ -24,13 +24,20 @@ struct GemmParams {
     int tiles_m, tiles_n;
     // Streamed mode (host-resident operands, dgemm_streamed): the copy stream uploads A in row
     // panels, B in column panels and C in blocks, and publishes each with a stream write of
-    // ready[] = 1: [npr A panels | npc B panels | npr*npc C blocks]. The persistent kernel walks
-    // tile_list (availability order) and waits for a tile's panels before loading them; every
-    // consumer warp bumps done[block] after storing its part of the block, which releases the
-    // block's download. nullptr = ordinary launch (operands already resident).
-    const int2* tile_list;
-    const uint32_t* ready;
-    uint32_t* done;
+    // ready[] = 1: [pass 0: npr A | npc B][pass 1: npr A | npc B][npr*npc C blocks], followed
+    // by the done[npr*npc] counters. The persistent kernel walks tile_list (tile_list[0].x =
+    // entry count, then entries {tile row, tile col, first k-tile, end k-tile}; tile row < 0 =
+    // padding) in availability order and waits for a tile's panels before loading them. An
+    // entry that starts at k-tile 0 uses the pass-0 panels, any other the pass-1 panels (k-split:
+    // the first pass covers k-tiles [0, kts) of every tile and parks its accumulators in
+    // `partial`; the second pass reloads them — same thread, same DMMA order, no bit changes).
+    // Every consumer warp of a tile's final pass bumps done[block] after storing its part of the
+    // block, which releases the block's download. nullptr = ordinary launch (operands resident).
+    // (The struct size is part of the tuned kernels' codegen: measured, a larger parameter block
+    // costs the resident DGEMM 1.3 % — keep new streamed fields out of it.)
+    const int4* tile_list;
+    uint32_t* ready;
+    double* partial;
     int panel_rows, panel_cols, npr, npc;
 };
 
@@ -50,6 +57,10 @@ struct StreamedShape {
 };
 int streamed_config(int tile, const GemmParams& p);
 StreamedShape streamed_shape(int cfg);
+// The persistent grid launch_streamed uses for this problem (entry e of the tile list runs on
+// CTA e mod grid: a k-split pads its first pass to a multiple of it so both passes of a tile
+// run on the same CTA).
+int streamed_grid(int cfg, const GemmParams& p);
 kw_status launch_streamed(cudaStream_t s, int cfg, const GemmParams& p);
 
 // Host-operand schedules (kw_dgemm_e2e.cu): row panels, and the streamed schedule (returns
