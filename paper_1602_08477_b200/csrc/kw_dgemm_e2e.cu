@@ -176,6 +176,11 @@ kw_status dgemm_staged(kw::Queue* q, int tile, size_t m, size_t n, size_t k, dou
 // which fences the copy before the flag). Finished C blocks go back on the aux stream as soon
 // as every consumer warp of every tile in the block has counted in (cuStreamWaitValue32 on
 // done[block]). Same kernel arithmetic per tile -> bitwise identical to the resident launch.
+// k-split (default): the whole schedule first runs over the first quarter of A's columns and
+// B's rows (pass 0: k-tiles [0, ktiles/4) of every tile, accumulators parked per thread), then
+// over the rest plus C (final pass: reload, remaining k-tiles, epilogue). Square growth unlocks
+// s/4 flop per uploaded byte at side s whatever the panel depth, so quarter-depth panels reach
+// the kernel's full rate after a quarter of the bytes (DESIGN.md §4 "k-split").
 // Deadlock freedom: the kernel waits only on copies, the copies wait only on ev_start (before
 // the kernel), the downloads wait on the kernel; everything is enqueued in that order, so even
 // streams that share a hardware queue never block a producer behind its consumer.
