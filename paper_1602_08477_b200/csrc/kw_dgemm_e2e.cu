@@ -245,7 +245,8 @@ kw_status dgemm_streamed(kw::Queue* q, int tile, size_t m, size_t n, size_t k, d
     const int bm = shape.bm, bn = shape.bn;
     const uint32_t consumers = shape.consumers;
     const size_t tiles_m = kw::ceil_div(m, bm), tiles_n = kw::ceil_div(n, bn), tiles = tiles_m * tiles_n;
-    // k-split (KW_E2E_KSPLIT = d, default 4; 0/1 = off): a first pass over k-tiles [0, kts), kts =
+    // k-split (KW_E2E_KSPLIT = d; default 4 from 600 flop/B — 8192^3 is 683 — and off below,
+    // where it measured 0.5-1 % slower at 5120-6144; 0/1 = off): a first pass over k-tiles [0, kts), kts =
     // ktiles / d, needs only the first K0 = 16 kts columns of A and rows of B, so d times less
     // upload per unit of work than the full-depth panels — the kernel reaches full rate while
     // most of A and B are still in flight. Its accumulators are parked in `partial` and picked up
@@ -253,7 +254,7 @@ kw_status dgemm_streamed(kw::Queue* q, int tile, size_t m, size_t n, size_t k, d
     // single-pass schedule does.
     const size_t ktiles = kw::ceil_div(k, static_cast<size_t>(16));
     const char* ke = std::getenv("KW_E2E_KSPLIT");
-    const long kd = ke ? std::atol(ke) : 4;
+    const long kd = ke ? std::atol(ke) : (intensity >= 600.0 ? 4 : 0);
     const size_t kts = kd > 1 ? ktiles / static_cast<size_t>(kd) : 0;
     const size_t K0 = kts * 16;
     const int passes = kts > 0 ? 2 : 1;

@@ -29,7 +29,7 @@ def run(n):
         ts.append(time.perf_counter() - t)
     med = statistics.median(ts)
     tag = (f"streamed={os.environ.get('KW_E2E_STREAMED', '1')} panels={os.environ.get('KW_E2E_PANELS', '12')} "
-           f"ksplit={os.environ.get('KW_E2E_KSPLIT', '4')}")
+           f"ksplit={os.environ.get('KW_E2E_KSPLIT', 'auto')}")
     print(f"{tag} conn={os.environ.get('CUDA_DEVICE_MAX_CONNECTIONS', '-')} n={n} {med*1e3:.1f} ms {2*n**3/med/1e12:.2f} TFLOP/s steps " + " ".join(f"{t*1e3:.1f}" for t in ts))
 
 
