@@ -9,7 +9,9 @@
 //   * primary kernel dgemm_tma_kernel: warp-specialised — one producer lane streams k-tiles of
 //     A and B with TMA (cp.async.bulk.tensor, SWIZZLE_128B, hardware zero-fill of ragged edges)
 //     into an mbarrier-synchronised stage ring; consumer warps (64 x 32 warp tiles = 8 x 4 DMMA
-//     accumulators) wait `full`, run the DMMAs, release `empty`; no CTA barrier in the main loop;
+//     accumulators) wait `full`, run the DMMAs, release `empty` once the DMMAs of the stage's last
+//     k-step are issued (not earlier: a pending LDS must not race the refill's TMA); no CTA
+//     barrier in the main loop;
 //     setmaxnreg moves registers from the producer warpgroup to the consumers;
 //   * a paired k-slot permutation puts two k-steps of an A fragment in one 16-byte chunk (one
 //     LDS.128), conflict-free under the swizzle; every tile shape ("paired" configs 14-17) feeds
@@ -18,7 +20,8 @@
 //   * epilogue fl(fl(alpha*acc) + fl(beta*c)) exactly as gemm.cpp:115 / reference.cpp:24 (C is
 //     always read, also for beta == 0); tiles rasterised in groups of 8 tile-rows for L2 reuse;
 //   * the STREAMED instantiation additionally walks a tile list and waits on per-panel ready
-//     flags (host-operand e2e path, kw_dgemm_e2e.cu);
+//     flags (host-operand e2e path, kw_dgemm_e2e.cu); list entries carry a k-tile range, so a
+//     tile can run as two passes whose accumulators are parked in global memory in between;
 //   * dgemm_dmma_kernel: the earlier cp.async (LDGSTS) + __syncthreads family, kept as the path
 //     for operands TMA cannot address (odd leading dimensions) and for the tile sweep.
 // Numerics: per output element the K products are accumulated in ascending k-tile order by
