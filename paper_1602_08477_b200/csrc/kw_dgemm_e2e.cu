@@ -74,6 +74,14 @@ kw_status dgemm_staged(kw::Queue* q, int tile, size_t m, size_t n, size_t k, dou
     }
     char* slots = base + ((b_bytes + 255) / 256) * 256;
     const size_t npanels = kw::ceil_div(m, R);
+    // KW_E2E_TRACE: CUDA-event timeline (start, B resident, last upload, last compute, last download)
+    const bool trace = std::getenv("KW_E2E_TRACE") != nullptr;
+    cudaEvent_t tev[5] = {};
+    if (trace) {
+        for (auto& ev : tev)
+            cudaEventCreate(&ev);
+        cudaEventRecord(tev[0], q->stream);
+    }
     for (size_t pi = 0; pi < npanels && e == cudaSuccess; ++pi) {
         const int s = static_cast<int>(pi % ring);
         const size_t r0 = pi * R, rows = m - r0 < R ? m - r0 : R;
@@ -126,6 +134,8 @@ kw_status dgemm_staged(kw::Queue* q, int tile, size_t m, size_t n, size_t k, dou
                 if (st != KW_OK)
                     return st;
             }
+            if (trace)
+                cudaEventRecord(tev[1], q->h2d);
         }
         else {
             if (stream_b && pi == 1) {
@@ -152,6 +162,11 @@ kw_status dgemm_staged(kw::Queue* q, int tile, size_t m, size_t n, size_t k, dou
             e = cudaEventRecord(q->ev_free[s], comp);
         }
     }
+    if (trace && e == cudaSuccess) {
+        cudaEventRecord(tev[2], q->h2d);
+        cudaEventRecord(tev[3], (npanels & 1) ? q->stream : q->comp2); // stream of the last panel
+        cudaEventRecord(tev[4], q->aux);
+    }
     if (e == cudaSuccess) {
         e = cudaEventRecord(q->ev_join, q->aux);
         if (e == cudaSuccess)
@@ -160,6 +175,17 @@ kw_status dgemm_staged(kw::Queue* q, int tile, size_t m, size_t n, size_t k, dou
             e = cudaEventRecord(q->ev_join2, q->comp2);
         if (e == cudaSuccess)
             e = cudaStreamWaitEvent(q->stream, q->ev_join2, 0);
+    }
+    if (trace && e == cudaSuccess) {
+        cudaEventSynchronize(tev[4]);
+        cudaStreamSynchronize(q->stream);
+        float t[5] = {};
+        for (int i = 1; i < 5; ++i)
+            cudaEventElapsedTime(&t[i], tev[0], tev[i]);
+        std::fprintf(stderr, "[kw trace] row panels: %zu x %zu rows | B resident %.2f | last upload %.2f | last compute %.2f | "
+                     "last download %.2f ms\n", npanels, R, t[1], t[2], t[3], t[4]);
+        for (auto& ev : tev)
+            cudaEventDestroy(ev);
     }
     if (e != cudaSuccess)
         return kw::task_fail(q, std::string("dgemm (host-staged): ") + cudaGetErrorString(e));
