@@ -763,6 +763,23 @@ bool make_map(CUtensorMap* map, const double* base, size_t rows, size_t cols, si
 }
 
 
+// 2-D row-major fp64 matrix as a TMA map with an unswizzled (box_cols x box_rows) box: the box
+// lands dense in shared memory, row after row.
+bool make_map_dense(CUtensorMap* map, const double* base, size_t rows, size_t cols, size_t ld, uint32_t box_cols,
+                    uint32_t box_rows)
+{
+    PFN_encodeTiled enc = encode_fn();
+    if (!enc)
+        return false;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * sizeof(double))};
+    const cuuint32_t box[2] = {box_cols, box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <class Cfg, bool PERSISTENT = false, bool STREAMED = false>
 kw_status launch_tma(cudaStream_t s, const GemmParams& p0);
 
@@ -993,6 +1010,125 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS) dgemm_bitwise_k
     }
 }
 
+// Bit-exact mode, warp-specialised: the same per-element arithmetic as dgemm_bitwise_kernel
+// (acc = dadd(acc, dmul(a, b)) over k ascending from +0.0, padded k never summed, two-rounding
+// epilogue), but the k-tiles arrive by TMA in an mbarrier ring filled by one producer lane, so the
+// 8 consumer warps never meet at a block barrier: a warp waiting for a stage leaves the FP64 pipe
+// to the other warp of its sub-partition. Consumer warp w owns rows w + 8i (i < 16) and lane l
+// columns l + 32j (j < 4): the A operand of a k-step is one broadcast address per warp (no bank
+// conflicts on a dense TMA box), B is 32 consecutive doubles.
+struct BwTmaCfg {
+    static constexpr int BM = 128, BN = 128, BK = 32, STAGES = 3, CONSUMERS = 8;
+    static constexpr int MI = 16, NJ = 4; // per-thread outputs: MI rows x NJ columns
+    static constexpr int THREADS = 32 * (CONSUMERS + 4);
+    static constexpr int PRODUCER_REGS = 40, CONSUMER_REGS = 232; // 4*40 + 8*232 <= 12 * 168
+    static constexpr uint32_t A_BYTES = BM * BK * 8, B_BYTES = BK * BN * 8, STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr size_t SMEM = 1024 + static_cast<size_t>(STAGES) * STAGE_BYTES + 2 * STAGES * sizeof(uint64_t);
+    static_assert(4 * PRODUCER_REGS + CONSUMERS * CONSUMER_REGS <= 12 * 168, "register pool overcommitted");
+};
+
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, 1)
+    dgemm_bitwise_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                             GemmParams p)
+{
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+    uint64_t* empty = full + Cfg::STAGES;
+    constexpr int GROUP = 8;
+    const int tile = blockIdx.x;
+    const int per_group = GROUP * p.tiles_n;
+    const int group = tile / per_group;
+    const int first_m = group * GROUP;
+    const int gsize = (p.tiles_m - first_m) < GROUP ? (p.tiles_m - first_m) : GROUP;
+    const int in_group = tile - group * per_group;
+    const int bm = (first_m + in_group % gsize) * Cfg::BM;
+    const int bn = (in_group / gsize) * Cfg::BN;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < Cfg::STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], Cfg::CONSUMERS);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int ktiles = (p.k + Cfg::BK - 1) / Cfg::BK;
+
+    if (warp >= Cfg::CONSUMERS) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(Cfg::PRODUCER_REGS));
+        if (warp == Cfg::CONSUMERS && lane == 0) {
+            tma_prefetch_desc(&tmA);
+            tma_prefetch_desc(&tmB);
+            for (int kt = 0; kt < ktiles; ++kt) {
+                const int s = kt % Cfg::STAGES;
+                mbar_wait(&empty[s], (static_cast<uint32_t>(kt / Cfg::STAGES) & 1u) ^ 1u);
+                mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
+                const uint32_t sa = smem_u32(smem + s * Cfg::STAGE_BYTES);
+                tma_load_2d(sa, &tmA, kt * Cfg::BK, bm, &full[s]);
+                tma_load_2d(sa + Cfg::A_BYTES, &tmB, bn, kt * Cfg::BK, &full[s]);
+            }
+        }
+        return;
+    }
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(Cfg::CONSUMER_REGS));
+
+    double acc[Cfg::MI][Cfg::NJ];
+#pragma unroll
+    for (int i = 0; i < Cfg::MI; ++i)
+#pragma unroll
+        for (int j = 0; j < Cfg::NJ; ++j)
+            acc[i][j] = 0.0;
+    for (int kt = 0; kt < ktiles; ++kt) {
+        const int s = kt % Cfg::STAGES;
+        mbar_wait(&full[s], static_cast<uint32_t>(kt / Cfg::STAGES) & 1u);
+        const double* a_s = reinterpret_cast<const double*>(smem + s * Cfg::STAGE_BYTES) + warp * Cfg::BK;
+        const double* b_s = reinterpret_cast<const double*>(smem + s * Cfg::STAGE_BYTES + Cfg::A_BYTES) + lane;
+        const int kend = (p.k - kt * Cfg::BK) < Cfg::BK ? (p.k - kt * Cfg::BK) : Cfg::BK; // no padded terms
+        auto kstep = [&](int kk) {
+            double a[Cfg::MI], b[Cfg::NJ];
+#pragma unroll
+            for (int i = 0; i < Cfg::MI; ++i)
+                a[i] = a_s[i * 8 * Cfg::BK + kk];
+#pragma unroll
+            for (int j = 0; j < Cfg::NJ; ++j)
+                b[j] = b_s[kk * Cfg::BN + 32 * j];
+#pragma unroll
+            for (int i = 0; i < Cfg::MI; ++i)
+#pragma unroll
+                for (int j = 0; j < Cfg::NJ; ++j)
+                    acc[i][j] = __dadd_rn(acc[i][j], __dmul_rn(a[i], b[j])); // never contracted to DFMA
+        };
+        if (kend == Cfg::BK) {
+#pragma unroll 4
+            for (int kk = 0; kk < Cfg::BK; ++kk)
+                kstep(kk);
+        }
+        else {
+            for (int kk = 0; kk < kend; ++kk)
+                kstep(kk);
+        }
+        // every value read from stage s has been consumed by the arithmetic above
+        __syncwarp();
+        if (lane == 0)
+            mbar_arrive(&empty[s]);
+    }
+#pragma unroll
+    for (int i = 0; i < Cfg::MI; ++i) {
+        const int row = bm + warp + 8 * i;
+        if (row >= p.m)
+            continue;
+        double* crow = p.c + row * p.ldc;
+#pragma unroll
+        for (int j = 0; j < Cfg::NJ; ++j) {
+            const int col = bn + lane + 32 * j;
+            if (col < p.n)
+                crow[col] = __dadd_rn(__dmul_rn(p.alpha, acc[i][j]), __dmul_rn(p.beta, crow[col]));
+        }
+    }
+}
+
 template <class Cfg>
 kw_status launch_bitwise_cfg(cudaStream_t s, const GemmParams& p0)
 {
@@ -1014,7 +1150,36 @@ kw_status launch_bitwise_cfg(cudaStream_t s, const GemmParams& p0)
     return KW_OK;
 }
 
-kw_status launch_bitwise(cudaStream_t s, const GemmParams& p) { return launch_bitwise_cfg<Bw128>(s, p); }
+kw_status launch_bitwise_tma(cudaStream_t s, const GemmParams& p0)
+{
+    using Cfg = BwTmaCfg;
+    GemmParams p = p0;
+    p.tiles_m = static_cast<int>(kw::ceil_div(p.m, Cfg::BM));
+    p.tiles_n = static_cast<int>(kw::ceil_div(p.n, Cfg::BN));
+    const long long tiles = static_cast<long long>(p.tiles_m) * p.tiles_n;
+    if (tiles > INT_MAX)
+        return kw::usage("dgemm: problem too large for the tile grid");
+    CUtensorMap ma, mb;
+    if (!make_map_dense(&ma, p.a, p.m, p.k, p.lda, Cfg::BK, Cfg::BM) ||
+        !make_map_dense(&mb, p.b, p.k, p.n, p.ldb, Cfg::BN, Cfg::BK))
+        return launch_bitwise_cfg<Bw128>(s, p0);
+    const kw_status st = ensure_smem(reinterpret_cast<const void*>(dgemm_bitwise_tma_kernel<Cfg>), Cfg::SMEM,
+                                     "dgemm_bitwise: cudaFuncSetAttribute");
+    if (st != KW_OK)
+        return st;
+    dgemm_bitwise_tma_kernel<Cfg><<<static_cast<unsigned>(tiles), Cfg::THREADS, Cfg::SMEM, s>>>(ma, mb, p);
+    kw::g_launches.fetch_add(1, std::memory_order_relaxed);
+    return KW_OK;
+}
+
+kw_status launch_bitwise(cudaStream_t s, const GemmParams& p)
+{
+    const char* e = std::getenv("KW_BW_TMA");
+    const bool tma = !(e && e[0] == '0') && p.k > 0 && (p.lda * 8) % 16 == 0 && (p.ldb * 8) % 16 == 0 &&
+                     reinterpret_cast<uintptr_t>(p.a) % 16 == 0 && reinterpret_cast<uintptr_t>(p.b) % 16 == 0 &&
+                     encode_fn() != nullptr;
+    return tma ? launch_bitwise_tma(s, p) : launch_bitwise_cfg<Bw128>(s, p);
+}
 
 kw_status validate_gemm(size_t m, size_t n, size_t k, const double* A, size_t lda, const double* B, size_t ldb,
                         const double* C, size_t ldc)
