@@ -346,9 +346,13 @@ def tiled_bitwise(dev, alpha, beta, a, b, c, align=64):
     return Cb.download()
 
 
-def test_tiled_bitwise_mode_is_bit_exact(gpu, oracle, golden):
+@pytest.mark.parametrize("bw_tma", ["1", "0"])
+def test_tiled_bitwise_mode_is_bit_exact(gpu, oracle, golden, bw_tma, monkeypatch):
     """GemmTiledKernel in bitwise mode reproduces the reference bit for bit — the reference's
-    own contract tiled == naive == gemmReference (test_kernels.cpp:184-279)."""
+    own contract tiled == naive == gemmReference (test_kernels.cpp:184-279) — with the
+    warp-specialised TMA kernel (default) and with the cp.async kernel (KW_BW_TMA=0, also the
+    path for odd leading dimensions, align 8 below)."""
+    monkeypatch.setenv("KW_BW_TMA", bw_tma)
     for case in (4, 5):
         c = golden["workloads"][case]
         alpha, beta, a, b, cin = oracle.workload_gemm(c["n"], c["seed"], "gemm-tiled")
