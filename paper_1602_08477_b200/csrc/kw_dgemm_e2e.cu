@@ -435,6 +435,23 @@ kw_status dgemm_streamed(kw::Queue* q, int tile, size_t m, size_t n, size_t k, d
     // 1. uploads + ready flags (copy stream): pass 0's K0-deep panels, then the final pass's
     // panels (columns / rows K0.. of A / B) with the C blocks they complete
     CUresult ce = CUDA_SUCCESS;
+    // The C region a step completes: row panel idx x the first `count` column panels (A step) or
+    // column panel idx x the first `count` row panels (B step).
+    auto upload_c = [&](bool is_a, size_t idx, size_t count) {
+        if (is_a) {
+            const size_t r0 = idx * R, rows = std::min(m, r0 + R) - r0, cols = std::min(n, count * W);
+            e = cudaMemcpy2DAsync(Cd + r0 * ldcs, ldcs * 8, C + r0 * ldc, ldc * 8, cols * 8, rows,
+                                  cudaMemcpyHostToDevice, q->h2d);
+            for (size_t j = 0; j < count && e == cudaSuccess && ce == CUDA_SUCCESS; ++j)
+                ce = ops.write(q->h2d, flag(2 * (npr + npc) + idx * npc + j), 1, 0);
+        }
+        else {
+            const size_t c0 = idx * W, cols = std::min(n, c0 + W) - c0, rows = std::min(m, count * R);
+            e = cudaMemcpy2DAsync(Cd + c0, ldcs * 8, C + c0, ldc * 8, cols * 8, rows, cudaMemcpyHostToDevice, q->h2d);
+            for (size_t i = 0; i < count && e == cudaSuccess && ce == CUDA_SUCCESS; ++i)
+                ce = ops.write(q->h2d, flag(2 * (npr + npc) + i * npc + idx), 1, 0);
+        }
+    };
     for (int pass = passes > 1 ? 0 : 1; pass < 2; ++pass) {
         const bool final_pass = pass == 1;
         const size_t k0 = final_pass ? K0 : 0, kw_ = final_pass ? k - K0 : K0;
@@ -449,14 +466,6 @@ kw_status dgemm_streamed(kw::Queue* q, int tile, size_t m, size_t n, size_t k, d
                                       cudaMemcpyHostToDevice, q->h2d);
                 if (e == cudaSuccess)
                     ce = ops.write(q->h2d, flag(fbase + stp.idx), 1, 0);
-                if (final_pass && e == cudaSuccess && ce == CUDA_SUCCESS && b > 0) {
-                    const size_t cols = std::min(n, b * W);
-                    e = cudaMemcpy2DAsync(Cd + r0 * ldcs, ldcs * 8, C + r0 * ldc, ldc * 8, cols * 8, rows,
-                                          cudaMemcpyHostToDevice, q->h2d);
-                    for (size_t j = 0; j < b && e == cudaSuccess && ce == CUDA_SUCCESS; ++j)
-                        ce = ops.write(q->h2d, flag(2 * (npr + npc) + stp.idx * npc + j), 1, 0);
-                }
-                ++a;
             }
             else {
                 const size_t c0 = stp.idx * W, cols = std::min(n, c0 + W) - c0;
@@ -464,15 +473,16 @@ kw_status dgemm_streamed(kw::Queue* q, int tile, size_t m, size_t n, size_t k, d
                                       cudaMemcpyHostToDevice, q->h2d);
                 if (e == cudaSuccess)
                     ce = ops.write(q->h2d, flag(fbase + npr + stp.idx), 1, 0);
-                if (final_pass && e == cudaSuccess && ce == CUDA_SUCCESS && a > 0) {
-                    const size_t rows = std::min(m, a * R);
-                    e = cudaMemcpy2DAsync(Cd + c0, ldcs * 8, C + c0, ldc * 8, cols * 8, rows, cudaMemcpyHostToDevice,
-                                          q->h2d);
-                    for (size_t i = 0; i < a && e == cudaSuccess && ce == CUDA_SUCCESS; ++i)
-                        ce = ops.write(q->h2d, flag(2 * (npr + npc) + i * npc + stp.idx), 1, 0);
-                }
-                ++b;
             }
+            const size_t count = stp.is_a ? b : a; // blocks this step completes
+            if (stp.is_a)
+                ++a;
+            else
+                ++b;
+            // the final pass's C blocks go up right behind the panel that completes them (one step
+            // later measured 0.6 % slower at 8192^3, neutral elsewhere)
+            if (final_pass && count > 0 && e == cudaSuccess && ce == CUDA_SUCCESS)
+                upload_c(stp.is_a, stp.idx, count);
         }
     }
     if (e != cudaSuccess || ce != CUDA_SUCCESS)
