@@ -82,11 +82,16 @@ def test_dgemm_paths_agree_bitwise_on_random_cases(gpu, oracle, monkeypatch):
         assert np.array_equal(got, want), (case, path, m, n, k, tile)
 
 
+@pytest.mark.parametrize("schedule", ["default", "streamed-ksplit"])
 @pytest.mark.parametrize("m,n,k", [(1, 1, 100000), (100000, 1, 16), (16, 100000, 1), (3, 70000, 9),
                                    (65537, 3, 33), (1, 8192, 8192), (8192, 1, 8192)])
-def test_extreme_shapes(gpu, oracle, m, n, k):
+def test_extreme_shapes(gpu, oracle, m, n, k, schedule, monkeypatch):
     """Dot products, GEMV-like and outer-product shapes: resident launch within the
-    magnitude-scaled (K+4)u bound of gemmReference, and the pinned-host path equal to it."""
+    magnitude-scaled (K+4)u bound of gemmReference, and the pinned-host path equal to it — with
+    the default schedule choice and with the streamed two-pass k-split forced."""
+    if schedule == "streamed-ksplit":
+        monkeypatch.setenv("KW_E2E_MIN_INTENSITY", "0")
+        monkeypatch.setenv("KW_E2E_KSPLIT", "2")
     rng = np.random.default_rng(m * 7 + n * 3 + k)
     lib = L.lib()
     q = kw.Queue(gpu, kw.QueueFlavor.Async)
