@@ -142,7 +142,7 @@ private:
         if (m_flavor == QueueFlavor::Sync)
             return TaskHandle(nullptr, st == KW_TASK, msg, true);
         kw_event ev = nullptr;
-        if (kw_event_record(m_q, &ev) != KW_OK)
+        if (kw_task_marker(m_q, &ev) != KW_OK)
             ev = nullptr;
         return TaskHandle(ev, st == KW_TASK, msg);
     }

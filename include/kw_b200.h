@@ -133,6 +133,9 @@ KW_EXPORT kw_status kw_queue_fail_slot(kw_queue q, const char* what, uint32_t** 
  * KW_TASK returned by its kw_* call (the C++/Python handles carry it; a Sync queue's handles need
  * no event at all). */
 KW_EXPORT kw_status kw_event_record(kw_queue q, kw_event* ev);
+/* The same completion marker without a timestamp (cheaper to record and to wait on): what the
+ * C++ and Python TaskHandles of an Async queue use. kw_event_elapsed_ms rejects it. */
+KW_EXPORT kw_status kw_task_marker(kw_queue q, kw_event* ev);
 KW_EXPORT kw_status kw_event_state(kw_event ev, int* state);
 KW_EXPORT kw_status kw_event_destroy(kw_event ev);
 /* Milliseconds between two recorded events of the same device (timing helper). */

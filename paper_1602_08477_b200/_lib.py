@@ -54,6 +54,7 @@ SIGNATURES = {
     "kw_queue_complete_launch": (st, [vp, C.c_int, C.c_char_p]),
     "kw_queue_fail_slot": (st, [vp, C.c_char_p, C.POINTER(C.POINTER(C.c_uint32))]),
     "kw_event_record": (st, [vp, C.POINTER(vp)]),
+    "kw_task_marker": (st, [vp, C.POINTER(vp)]),
     "kw_event_state": (st, [vp, C.POINTER(C.c_int)]),
     "kw_event_destroy": (st, [vp]),
     "kw_event_elapsed_ms": (st, [vp, vp, C.POINTER(C.c_float)]),

@@ -177,6 +177,7 @@ struct kw_event_s {
     cudaEvent_t ev;
     Queue* q;
     std::shared_ptr<kw::FailSlot> slot; // device-side failure slot of the task, if any
+    bool timing = true;                 // false: kw_task_marker (no timestamp)
 };
 
 extern "C" {
@@ -514,30 +515,38 @@ kw_status kw_queue_fail_slot(kw_queue qh, const char* what, uint32_t** slot)
 
 // ---- task events --------------------------------------------------------------------------
 
-kw_status kw_event_record(kw_queue qh, kw_event* out)
+namespace {
+kw_status record_event(kw_queue qh, kw_event* out, bool timing)
 {
     KW_CHECK_QUEUE(qh);
     KW_ENQUEUE_LOCK(qh);
     if (!out)
-        return kw::usage("kw_event_record: null output");
+        return kw::usage(timing ? "kw_event_record: null output" : "kw_task_marker: null output");
     auto* q = reinterpret_cast<Queue*>(qh);
     kw::DeviceGuard g(q->device);
-    auto* ev = new kw_event_s{q->device, nullptr, q, nullptr};
+    auto* ev = new kw_event_s{q->device, nullptr, q, nullptr, timing};
     {
         std::lock_guard<std::mutex> lock(q->mu);
         ev->slot = std::move(q->last_slot);
         q->last_slot.reset();
     }
-    cudaError_t e = cudaEventCreate(&ev->ev);
+    cudaError_t e = timing ? cudaEventCreate(&ev->ev) : cudaEventCreateWithFlags(&ev->ev, cudaEventDisableTiming);
     if (e == cudaSuccess)
         e = cudaEventRecord(ev->ev, q->stream);
     if (e != cudaSuccess) {
+        if (ev->ev)
+            cudaEventDestroy(ev->ev);
         delete ev;
         return kw::cuda_fail("event record", e);
     }
     *out = ev;
     return KW_OK;
 }
+} // namespace
+
+kw_status kw_event_record(kw_queue qh, kw_event* out) { return record_event(qh, out, true); }
+
+kw_status kw_task_marker(kw_queue qh, kw_event* out) { return record_event(qh, out, false); }
 
 kw_status kw_event_state(kw_event ev, int* state)
 {
@@ -575,6 +584,8 @@ kw_status kw_event_elapsed_ms(kw_event a, kw_event b, float* ms)
 {
     if (!a || !b || !ms)
         return kw::usage("kw_event_elapsed_ms: null argument");
+    if (!a->timing || !b->timing)
+        return kw::usage("kw_event_elapsed_ms: task markers carry no timestamp (use kw_event_record)");
     kw::DeviceGuard g(a->device);
     cudaError_t e = cudaEventSynchronize(b->ev);
     if (e == cudaSuccess)

@@ -553,7 +553,7 @@ class Queue:
             if self._flavor == QueueFlavor.Sync:  # completed inside the call: no event needed
                 return TaskHandle(None, failed)
             ev = C.c_void_p()
-            if L.lib().kw_event_record(self._h, C.byref(ev)) != L.KW_OK:
+            if L.lib().kw_task_marker(self._h, C.byref(ev)) != L.KW_OK:
                 return TaskHandle(None, TaskError(1, L.last_error()))
             return TaskHandle(ev.value, failed)
 

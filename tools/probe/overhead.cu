@@ -63,6 +63,11 @@ int main()
         kw_event_record(aq.native(), &ev);
         kw_event_destroy(ev);
     }));
+    std::printf("kw_task_marker + destroy              : %6.2f us\n", per_call_us([&] {
+        kw_event ev = nullptr;
+        kw_task_marker(aq.native(), &ev);
+        kw_event_destroy(ev);
+    }));
     std::printf("C-ABI kw_axpy_f64 (Sync queue)        : %6.2f us\n", per_call_us([&] {
         kw_axpy_f64(sq.native(), &w, n, 0.5, xd, yd);
     }));
