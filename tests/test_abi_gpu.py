@@ -114,3 +114,30 @@ def test_failed_calls_leave_no_residue(gpu):
     L.check(lib.kw_axpy_f64(q2.handle(), None, 1024, 1.0, x.data(), y.data()))
     q2.wait()
     assert (y.download() == 3.0).all()
+
+
+def test_task_markers_and_timed_events(gpu):
+    """kw_task_marker (what TaskHandles use) completes like kw_event_record but carries no
+    timestamp: kw_event_elapsed_ms accepts two recorded events and rejects a marker."""
+    lib = L.lib()
+    q = kw.Queue(gpu, kw.QueueFlavor.Async)
+    x = kw.Buffer(gpu, kw.IndexVec(1 << 20), 4)
+    y = kw.Buffer(gpu, kw.IndexVec(1 << 20), 4)
+    x.upload(np.ones(1 << 20, np.float32))
+    y.upload(np.ones(1 << 20, np.float32))
+    e0, mk, e1 = C.c_void_p(), C.c_void_p(), C.c_void_p()
+    L.check(lib.kw_event_record(q.handle(), C.byref(e0)))
+    L.check(lib.kw_axpy_f32(q.handle(), None, 1 << 20, 2.0, x.data(), y.data()))
+    L.check(lib.kw_task_marker(q.handle(), C.byref(mk)))
+    L.check(lib.kw_event_record(q.handle(), C.byref(e1)))
+    L.check(lib.kw_queue_wait(q.handle()))
+    state = C.c_int()
+    L.check(lib.kw_event_state(mk, C.byref(state)))
+    assert state.value == L.KW_TASK_DONE
+    ms = C.c_float()
+    L.check(lib.kw_event_elapsed_ms(e0, e1, C.byref(ms)))
+    assert ms.value >= 0.0
+    assert lib.kw_event_elapsed_ms(e0, mk, C.byref(ms)) == L.KW_USAGE
+    for ev in (e0, mk, e1):
+        L.check(lib.kw_event_destroy(ev))
+    assert np.array_equal(y.download(), np.full(1 << 20, 3.0, np.float32))
