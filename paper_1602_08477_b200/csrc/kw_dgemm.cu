@@ -1606,8 +1606,17 @@ kw_status kw_dgemm_naive(kw_queue qh, const kw_workdiv* wd, size_t m, size_t n, 
         return kw::usage("dgemm_naive: operands must be device buffers");
     dim3 grid(static_cast<unsigned>(wd->blocks[1]), static_cast<unsigned>(wd->blocks[0]));
     dim3 block(static_cast<unsigned>(wd->threads[1]), static_cast<unsigned>(wd->threads[0]));
-    dgemm_naive_kernel<<<grid, block, 0, q->stream>>>(make_params(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc),
-                                                       static_cast<int>(wd->elems[0]), static_cast<int>(wd->elems[1]));
+    int er = static_cast<int>(wd->elems[0]), ec = static_cast<int>(wd->elems[1]);
+    // A reference thread's er x ec chunk becomes er x ec CUDA threads when the block's outputs fit
+    // one CUDA block: the same block tile, one output per CUDA thread (the kernel hands a block's
+    // outputs to its threads in column order, so this only changes how many threads share them).
+    const size_t tile_rows = wd->threads[0] * wd->elems[0], tile_cols = wd->threads[1] * wd->elems[1];
+    if (tile_rows * tile_cols <= 1024) {
+        block = dim3(static_cast<unsigned>(tile_cols), static_cast<unsigned>(tile_rows));
+        er = ec = 1;
+    }
+    dgemm_naive_kernel<<<grid, block, 0, q->stream>>>(make_params(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc), er,
+                                                       ec);
     kw::g_launches.fetch_add(1, std::memory_order_relaxed);
     return kw::after_enqueue(q, "dgemm_naive");
 }

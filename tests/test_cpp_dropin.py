@@ -130,3 +130,23 @@ def test_criterion10_pessimization_analogue(programs, tmp_path):
     degraded = [float(r["seconds"]) for r in recs if r["tile"] == "1"]
     assert tuned and degraded
     assert statistics.median(degraded) / statistics.median(tuned) >= 2.0
+
+
+@pytest.mark.gpu
+def test_criterion08_zero_overhead_analogue(programs, tmp_path):
+    """acceptance.cpp:546-585 on the GPU: the library back-end's median time over the native
+    CUDA kernels' (kwbench --baseline native) is at most 1.5x for AXPY at n = 2^20 and for the
+    naive GEMM at 256 and 512, each with a tuned division (the reference picks one per kernel)."""
+    import csv
+    import statistics
+    exe = str(programs["kwbench"])
+    for argv in (["--kernel", "axpy", "--sizes", "1048576"], ["--kernel", "gemm-naive", "--sizes", "256,512"]):
+        out = tmp_path / "c08.csv"
+        p = subprocess.run([exe, *argv, "--backend", "all", "--baseline", "native", "--reps", "21", "--csv", str(out)],
+                           capture_output=True, text=True, timeout=600)
+        assert p.returncode == 0, (argv, p.stdout, p.stderr)
+        recs = list(csv.DictReader(out.open()))
+        for n in {r["n"] for r in recs}:
+            lib = statistics.median(float(r["seconds"]) for r in recs if r["n"] == n and r["backend"] == "gpu")
+            nat = statistics.median(float(r["seconds"]) for r in recs if r["n"] == n and r["backend"] == "native")
+            assert lib / nat <= 1.5, (argv, n, lib / nat)

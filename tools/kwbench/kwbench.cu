@@ -89,6 +89,7 @@ struct Config {
     int reps = 5;
     std::uint64_t seed = 42;
     std::size_t tile = 128, tpb = 512, ept = 4;
+    bool tpb_set = false, ept_set = false; // gemm-naive has its own tuned default division
     bool verify = false, pessimize = false, f32 = false;
     std::string csv, baseline;
     std::vector<std::string> backends; // resolved from --backend (+ the baseline if missing)
@@ -162,10 +163,14 @@ Config parse(int argc, char** argv)
             c.seed = std::strtoull(val().c_str(), nullptr, 10);
         else if (a == "--tile")
             c.tile = std::strtoull(val().c_str(), nullptr, 10);
-        else if (a == "--tpb")
+        else if (a == "--tpb") {
             c.tpb = std::strtoull(val().c_str(), nullptr, 10);
-        else if (a == "--ept")
+            c.tpb_set = true;
+        }
+        else if (a == "--ept") {
             c.ept = std::strtoull(val().c_str(), nullptr, 10);
+            c.ept_set = true;
+        }
         else if (a == "--dtype") {
             const std::string d = val();
             if (d != "f32" && d != "f64")
@@ -205,6 +210,15 @@ Config parse(int argc, char** argv)
     for (std::size_t n : c.sizes)
         if (n == 0)
             throw UsageError("sizes must be at least 1");
+    // A tuned division per kernel, as acceptance.cpp:567-579 picks one for its gemm instances:
+    // gemm-naive defaults to 16 threads x 16 elements (a 16 x 16 output block per CUDA block, one
+    // output per CUDA thread); axpy keeps 512 x 4.
+    if (c.kernel == "gemm-naive") {
+        if (!c.tpb_set)
+            c.tpb = 16;
+        if (!c.ept_set)
+            c.ept = 16;
+    }
     if (c.tile == 0 || c.tpb == 0 || c.ept == 0)
         throw UsageError("tile, tpb and ept must be at least 1");
     if (c.pessimize && c.kernel == "axpy")
