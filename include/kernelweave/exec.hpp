@@ -31,7 +31,7 @@ void executeTask(BackendKind backend, const WorkDiv& wd, const Kernel& kernel, c
     ExecTask task = createExec(backend, wd, kernel, args...);
     Queue& q = detail::defaultQueue(detail::Launcher<Kernel, Args...>::device(args...));
     q.enqueue(std::move(task));
-    q.wait();
+    q.report(); // the Sync queue already completed the task: no second stream round trip
 }
 
 } // namespace kernelweave

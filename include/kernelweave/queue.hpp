@@ -123,6 +123,9 @@ public:
     /// Blocks until everything enqueued so far completed; throws TaskError for failures since
     /// the last report (queue.cpp:99-131). Idempotent.
     void wait() { detail::check(kw_queue_wait(m_q)); }
+    /// Sync queues: throws the TaskError of failed tasks since the last report without a stream
+    /// round trip (their tasks completed inside enqueue).
+    void report() { detail::check(kw_queue_report(m_q)); }
     void shutdown() { detail::check(kw_queue_shutdown(m_q)); }
 
     Device device() const noexcept { return m_device; }

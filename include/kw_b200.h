@@ -108,6 +108,10 @@ KW_EXPORT kw_status kw_memset(kw_queue q, void* ptr, int value, size_t bytes);
 KW_EXPORT kw_status kw_queue_create(int device, int flavor, kw_queue* q);
 KW_EXPORT kw_status kw_queue_destroy(kw_queue q);
 KW_EXPORT kw_status kw_queue_wait(kw_queue q);
+/* Sync queues only: the TaskError for failures since the last report, without a stream round
+ * trip (every task on a Sync queue completed inside its own call; after a failure it drains the
+ * stream first, like kw_queue_wait). What executeTask uses. KW_USAGE on an Async queue. */
+KW_EXPORT kw_status kw_queue_report(kw_queue q);
 KW_EXPORT kw_status kw_queue_device(kw_queue q, int* device);
 KW_EXPORT kw_status kw_queue_flavor(kw_queue q, int* flavor);
 KW_EXPORT kw_status kw_queue_stream(kw_queue q, void** cuda_stream);

@@ -47,6 +47,7 @@ SIGNATURES = {
     "kw_queue_create": (st, [C.c_int, C.c_int, C.POINTER(vp)]),
     "kw_queue_destroy": (st, [vp]),
     "kw_queue_wait": (st, [vp]),
+    "kw_queue_report": (st, [vp]),
     "kw_queue_device": (st, [vp, C.POINTER(C.c_int)]),
     "kw_queue_flavor": (st, [vp, C.POINTER(C.c_int)]),
     "kw_queue_stream": (st, [vp, C.POINTER(vp)]),

@@ -444,6 +444,22 @@ kw_status kw_queue_wait(kw_queue qh)
     return KW_TASK;
 }
 
+kw_status kw_queue_report(kw_queue qh)
+{
+    if (!qh)
+        return kw::usage("null queue");
+    auto* q = reinterpret_cast<Queue*>(qh);
+    if (q->flavor != KW_QUEUE_SYNC)
+        return kw::usage("kw_queue_report: only a Sync queue's tasks are complete when their call returns");
+    {
+        std::lock_guard<std::mutex> lock(q->mu);
+        if (q->failed == 0)
+            return KW_OK;
+    }
+    // a failed task may have left work behind it: drain before reporting, as kw_queue_wait does
+    return kw_queue_wait(qh);
+}
+
 kw_status kw_queue_device(kw_queue qh, int* device)
 {
     if (!qh || !device)

@@ -560,6 +560,11 @@ class Queue:
     def wait(self) -> None:
         _raise_for(L.lib().kw_queue_wait(self._h))
 
+    def report(self) -> None:
+        """Sync queues: raise TaskError for failures since the last report, without a stream
+        round trip (the tasks completed inside enqueue)."""
+        _raise_for(L.lib().kw_queue_report(self._h))
+
     def shutdown(self) -> None:
         _raise_for(L.lib().kw_queue_shutdown(self._h))
 
@@ -754,4 +759,4 @@ def executeTask(backend: BackendKind, wd: WorkDiv, kernel, *args) -> None:
     out = args[0].y if isinstance(args[0], AxpyArgs) else args[0].c
     q = _default_queue(out.device())
     q.enqueue(task)
-    q.wait()
+    q.report()

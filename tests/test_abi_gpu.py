@@ -141,3 +141,25 @@ def test_task_markers_and_timed_events(gpu):
     for ev in (e0, mk, e1):
         L.check(lib.kw_event_destroy(ev))
     assert np.array_equal(y.download(), np.full(1 << 20, 3.0, np.float32))
+
+
+def test_queue_report_on_sync_queues(gpu):
+    """kw_queue_report (what executeTask uses): OK after successful Sync tasks, TaskError (once)
+    after a failed one, KW_USAGE on an Async queue."""
+    lib = L.lib()
+    sq = kw.Queue(gpu, kw.QueueFlavor.Sync)
+    x = kw.Buffer(gpu, kw.IndexVec(1024), 8)
+    y = kw.Buffer(gpu, kw.IndexVec(1024), 8)
+    x.upload(np.ones(1024))
+    y.upload(np.ones(1024))
+    L.check(lib.kw_axpy_f64(sq.handle(), None, 1024, 2.0, x.data(), y.data()))
+    assert lib.kw_queue_report(sq.handle()) == L.KW_OK
+    assert np.array_equal(y.download(), np.full(1024, 3.0))
+    # a task failure on the Sync queue (an illegal division) is reported, then cleared
+    bad = kw.WorkDiv(kw.IndexVec(1), kw.IndexVec(2048), kw.IndexVec(1)).to_c()
+    st = lib.kw_axpy_f64(sq.handle(), C.byref(bad), 1024, 2.0, x.data(), y.data())
+    if st == L.KW_TASK:
+        assert lib.kw_queue_report(sq.handle()) == L.KW_TASK
+    assert lib.kw_queue_report(sq.handle()) == L.KW_OK
+    aq = kw.Queue(gpu, kw.QueueFlavor.Async)
+    assert lib.kw_queue_report(aq.handle()) == L.KW_USAGE
