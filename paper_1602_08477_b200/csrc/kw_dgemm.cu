@@ -427,7 +427,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
             bm = v.x * Cfg::BM;
             bn = v.y * Cfg::BN;
             kt0 = v.z;
-            kt1 = v.w;
+            kt1 = v.w & 0x07ffffff; // bits 27..30: the entry's pass (its set of panel flags)
             return v.x >= 0;
         }
         const int per_group = GROUP * p.tiles_n;
@@ -468,7 +468,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
                 if constexpr (STREAMED) {
                     // A row panel and B column panel of this tile (of its pass) resident? (The C
                     // block is waited for before the last k-tile, below.)
-                    const uint32_t* pass_flags = p.ready + (kt0 > 0 ? p.npr + p.npc : 0);
+                    const uint32_t* pass_flags =
+                        p.ready + (p.tile_list[1 + tile].w >> 27) * (p.npr + p.npc);
                     wait_ready(pass_flags + bm / p.panel_rows);
                     wait_ready(pass_flags + p.npr + bn / p.panel_cols);
                     // the panels were written by the copy engine; order the TMA reads after
@@ -484,8 +485,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
                         // C block's flag here orders those reads after its upload, and leaves
                         // the upload a whole tile of slack.
                         if (kt == ktiles - 1)
-                            wait_ready(p.ready + 2 * (p.npr + p.npc) + (bm / p.panel_rows) * p.npc +
-                                       bn / p.panel_cols);
+                            wait_ready(p.ready + p.tile_list[0].y * (p.npr + p.npc) +
+                                       (bm / p.panel_rows) * p.npc + bn / p.panel_cols);
                     }
                     mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
                     const uint32_t sa = smem_u32(smem + s * Cfg::STAGE_BYTES);
@@ -721,7 +722,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
         __syncwarp();
         if (lane == 0) {
             __threadfence_system();
-            uint32_t* done = p.ready + 2 * (p.npr + p.npc) + p.npr * p.npc;
+            uint32_t* done = p.ready + p.tile_list[0].y * (p.npr + p.npc) + p.npr * p.npc;
             atomicAdd(done + (bm / p.panel_rows) * p.npc + bn / p.panel_cols, 1u);
         }
     }

@@ -281,10 +281,31 @@ kw_status dgemm_streamed(kw::Queue* q, int tile, size_t m, size_t n, size_t k, d
     const size_t ktiles = kw::ceil_div(k, static_cast<size_t>(16));
     const char* ke = std::getenv("KW_E2E_KSPLIT");
     const long kd = ke ? std::atol(ke) : (intensity >= 600.0 ? 4 : 0);
-    const size_t kts = kd > 1 ? ktiles / static_cast<size_t>(kd) : 0;
-    const size_t K0 = kts * 16;
-    const int passes = kts > 0 ? 2 : 1;
-    const size_t nflags = 2 * (npr + npc) + npr * npc, ndone = npr * npc;
+    // Pass boundaries in k-tiles: [0, ktiles/d, ktiles], or KW_E2E_KPASSES = cumulative
+    // percentages of the k-tiles ("25,50" -> [0, 25 %, 50 %, 100 %]); empty passes dropped.
+    std::vector<size_t> bounds{0};
+    if (const char* kp = std::getenv("KW_E2E_KPASSES")) {
+        for (const char* c = kp; *c;) {
+            char* end = nullptr;
+            const long pct = std::strtol(c, &end, 10);
+            if (end == c)
+                break;
+            if (pct > 0 && pct < 100)
+                bounds.push_back(ktiles * static_cast<size_t>(pct) / 100);
+            c = *end == ',' ? end + 1 : end;
+        }
+    }
+    else if (kd > 1) {
+        bounds.push_back(ktiles / static_cast<size_t>(kd));
+    }
+    bounds.push_back(ktiles);
+    std::sort(bounds.begin(), bounds.end());
+    bounds.erase(std::unique(bounds.begin(), bounds.end()), bounds.end());
+    if (bounds.size() > 16) // the entry's pass index has 4 bits
+        bounds.erase(bounds.begin() + 15, bounds.end() - 1);
+    const size_t npass = bounds.size() - 1;
+    const int passes = static_cast<int>(npass);
+    const size_t nflags = npass * (npr + npc) + npr * npc, ndone = npr * npc;
     const size_t mat_bytes = (m * ldas + k * ldbs + m * ldcs) * sizeof(double);
     const size_t part_bytes = passes > 1 ? tiles * bm * bn * sizeof(double) : 0;
     const size_t aux_bytes = (nflags + ndone) * sizeof(uint32_t) + 512;
@@ -322,8 +343,8 @@ kw_status dgemm_streamed(kw::Queue* q, int tile, size_t m, size_t n, size_t k, d
     const size_t grid = static_cast<size_t>(streamed_grid(cfg, p));
 
     // The growth order: A_0, B_0, then add a B column panel while it is not ahead of the A row
-    // panels, else an A row panel; each addition completes the C blocks of its row/column. Both
-    // passes follow it (pass 0 with K0-deep panels and no C).
+    // panels, else an A row panel; each addition completes the C blocks of its row/column. Every
+    // pass follows it with its own k-range of the panels; only the last carries C.
     struct Step {
         bool is_a;
         size_t idx;
@@ -346,30 +367,35 @@ kw_status dgemm_streamed(kw::Queue* q, int tile, size_t m, size_t n, size_t k, d
             }
         }
     }
-    // Work list: pass 0 (if any) padded to a multiple of the grid, so entry e and entry
-    // e + len0 — the two passes of one tile — run on the same CTA (CTA = entry mod grid).
-    std::vector<int4> order(1); // [0] = header: entry count
-    auto add_pass = [&](int kt0, int kt1) {
+    // Work list: header [0] = {entry count, pass count}, then every pass in the same block order;
+    // entry = {tile row, tile col, first k-tile, end k-tile | pass << 27}. Each pass but the last
+    // is padded to a multiple of the grid, so a tile's entries all run on one CTA (entry mod grid).
+    std::vector<int4> order(1);
+    size_t len_last = 0;
+    for (size_t ps = 0; ps < npass; ++ps) {
+        const int kt0 = static_cast<int>(bounds[ps]), kt1 = static_cast<int>(bounds[ps + 1]);
+        const size_t before = order.size();
         for (const auto& bl : blocks) {
             const size_t r0 = bl.first * R, r1 = std::min(m, r0 + R), c0 = bl.second * W, c1 = std::min(n, c0 + W);
             for (size_t tr = r0 / bm; tr < kw::ceil_div(r1, bm); ++tr)
                 for (size_t tc = c0 / bn; tc < kw::ceil_div(c1, bn); ++tc)
-                    order.push_back(make_int4(static_cast<int>(tr), static_cast<int>(tc), kt0, kt1));
+                    order.push_back(make_int4(static_cast<int>(tr), static_cast<int>(tc), kt0,
+                                              kt1 | static_cast<int>(ps << 27)));
         }
-    };
-    if (passes > 1) {
-        add_pass(0, static_cast<int>(kts));
-        while ((order.size() - 1) % grid != 0)
-            order.push_back(make_int4(-1, 0, 0, 0));
+        len_last = order.size() - before;
+        if (ps + 1 < npass)
+            while ((order.size() - 1) % grid != 0)
+                order.push_back(make_int4(-1, 0, 0, 0));
     }
-    const size_t len0 = order.size();
-    add_pass(static_cast<int>(kts), static_cast<int>(ktiles));
-    if (order.size() - len0 != tiles || order.size() > static_cast<size_t>(INT_MAX))
+    if (len_last != tiles || order.size() > static_cast<size_t>(INT_MAX))
         return kw::task_fail(q, "dgemm (streamed): tile order does not cover the output");
-    order[0] = make_int4(static_cast<int>(order.size() - 1), 0, 0, 0);
+    order[0] = make_int4(static_cast<int>(order.size() - 1), static_cast<int>(npass), 0, 0);
 
-    // The tile order goes up from a pinned copy, once per (scratch, shape, panel grid, tile, split).
-    const size_t key[8] = {m, n, R, W, static_cast<size_t>(cfg), 2, kts, grid};
+    // The tile order goes up from a pinned copy, once per (scratch, shape, panel grid, tile, passes).
+    size_t bhash = 1469598103934665603ull;
+    for (size_t b : bounds)
+        bhash = (bhash ^ b) * 1099511628211ull;
+    const size_t key[8] = {m, n, R, W, static_cast<size_t>(cfg), npass, bhash, grid};
     const bool order_current = std::equal(key, key + 8, q->order_key);
     auto flag = [&](size_t idx) { return reinterpret_cast<CUdeviceptr>(ready + idx); };
     cudaError_t e = cudaMemsetAsync(ready, 0, (nflags + ndone) * sizeof(uint32_t), q->stream);
@@ -432,8 +458,8 @@ kw_status dgemm_streamed(kw::Queue* q, int tile, size_t m, size_t n, size_t k, d
         cudaEventRecord(tev[0], q->stream);
     }
 
-    // 1. uploads + ready flags (copy stream): pass 0's K0-deep panels, then the final pass's
-    // panels (columns / rows K0.. of A / B) with the C blocks they complete
+    // 1. uploads + ready flags (copy stream): pass by pass, the panels' k-range of A (columns) and
+    // B (rows); the last pass also uploads the C blocks each panel completes
     CUresult ce = CUDA_SUCCESS;
     // The C region a step completes: row panel idx x the first `count` column panels (A step) or
     // column panel idx x the first `count` row panels (B step).
@@ -443,19 +469,19 @@ kw_status dgemm_streamed(kw::Queue* q, int tile, size_t m, size_t n, size_t k, d
             e = cudaMemcpy2DAsync(Cd + r0 * ldcs, ldcs * 8, C + r0 * ldc, ldc * 8, cols * 8, rows,
                                   cudaMemcpyHostToDevice, q->h2d);
             for (size_t j = 0; j < count && e == cudaSuccess && ce == CUDA_SUCCESS; ++j)
-                ce = ops.write(q->h2d, flag(2 * (npr + npc) + idx * npc + j), 1, 0);
+                ce = ops.write(q->h2d, flag(npass * (npr + npc) + idx * npc + j), 1, 0);
         }
         else {
             const size_t c0 = idx * W, cols = std::min(n, c0 + W) - c0, rows = std::min(m, count * R);
             e = cudaMemcpy2DAsync(Cd + c0, ldcs * 8, C + c0, ldc * 8, cols * 8, rows, cudaMemcpyHostToDevice, q->h2d);
             for (size_t i = 0; i < count && e == cudaSuccess && ce == CUDA_SUCCESS; ++i)
-                ce = ops.write(q->h2d, flag(2 * (npr + npc) + i * npc + idx), 1, 0);
+                ce = ops.write(q->h2d, flag(npass * (npr + npc) + i * npc + idx), 1, 0);
         }
     };
-    for (int pass = passes > 1 ? 0 : 1; pass < 2; ++pass) {
-        const bool final_pass = pass == 1;
-        const size_t k0 = final_pass ? K0 : 0, kw_ = final_pass ? k - K0 : K0;
-        const size_t fbase = passes > 1 && final_pass ? npr + npc : 0; // kernel: kt0 > 0 -> pass-1 flags
+    for (size_t ps = 0; ps < npass; ++ps) {
+        const bool final_pass = ps + 1 == npass;
+        const size_t k0 = bounds[ps] * 16, kw_ = std::min(k, bounds[ps + 1] * 16) - k0;
+        const size_t fbase = ps * (npr + npc);
         size_t a = 0, b = 0;
         for (const Step& stp : steps) {
             if (e != cudaSuccess || ce != CUDA_SUCCESS)

@@ -24,15 +24,15 @@ struct GemmParams {
     int tiles_m, tiles_n;
     // Streamed mode (host-resident operands, dgemm_streamed): the copy stream uploads A in row
     // panels, B in column panels and C in blocks, and publishes each with a stream write of
-    // ready[] = 1: [pass 0: npr A | npc B][pass 1: npr A | npc B][npr*npc C blocks], followed
-    // by the done[npr*npc] counters. The persistent kernel walks tile_list (tile_list[0].x =
-    // entry count, then entries {tile row, tile col, first k-tile, end k-tile}; tile row < 0 =
-    // padding) in availability order and waits for a tile's panels before loading them. An
-    // entry that starts at k-tile 0 uses the pass-0 panels, any other the pass-1 panels (k-split:
-    // the first pass covers k-tiles [0, kts) of every tile and parks its accumulators in
-    // `partial`; the second pass reloads them — same thread, same DMMA order, no bit changes).
-    // Every consumer warp of a tile's final pass bumps done[block] after storing its part of the
-    // block, which releases the block's download. nullptr = ordinary launch (operands resident).
+    // ready[] = 1: [pass 0: npr A | npc B] ... [pass P-1: npr A | npc B][npr*npc C blocks],
+    // followed by the done[npr*npc] counters. The persistent kernel walks tile_list
+    // (tile_list[0] = {entry count, P}, then entries {tile row, tile col, first k-tile, end
+    // k-tile | pass << 27}; tile row < 0 = padding) in availability order and waits for a tile's
+    // panels of the entry's pass before loading them. A tile runs as P entries over consecutive
+    // k-ranges (k-split): all but the last park their accumulators in `partial`, all but the
+    // first reload them — same thread, same DMMA order, no bit changes. Every consumer warp of a
+    // tile's last entry bumps done[block] after storing its part of the block, which releases
+    // the block's download. nullptr = ordinary launch (operands resident).
     // (The struct size is part of the tuned kernels' codegen: measured, a larger parameter block
     // costs the resident DGEMM 1.3 % — keep new streamed fields out of it.)
     const int4* tile_list;

@@ -223,18 +223,22 @@ def test_host_buffers_are_staged(gpu, oracle):
 
 
 @pytest.mark.parametrize("panels,ksplit", [("1", "4"), ("3", "4"), ("8", "4"), ("16", "4"), ("1", "0"), ("8", "0"),
-                                           ("3", "2"), ("1", "3"), ("16", "64")])
+                                           ("3", "2"), ("1", "3"), ("16", "64"), ("3", "p20,45,70"), ("8", "p50")])
 def test_streamed_host_schedule_is_bitwise_the_resident_launch(gpu, panels, ksplit, monkeypatch):
     """The streamed e2e schedule (pinned A, B, C: panels uploaded in square-growth order, one
     persistent kernel waiting on per-panel ready flags, C blocks downloaded as they complete)
     gives the bits of the device-resident launch for ragged shapes, both tile contracts, several
     panel grids and back-to-back enqueues on one queue (flags are reset per call) — single pass
     (KW_E2E_KSPLIT=0) and k-split (a first pass over the first 1/d of the k-tiles whose
-    accumulators are parked and reloaded; d = 64 degenerates to a single pass at small k)."""
+    accumulators are parked and reloaded; d = 64 degenerates to a single pass at small k; "pX,Y"
+    = passes at cumulative k-tile percentages, KW_E2E_KPASSES)."""
     monkeypatch.setenv("KW_E2E_PANELS", panels)
-    monkeypatch.setenv("KW_E2E_KSPLIT", ksplit)
+    if ksplit.startswith("p"):  # several passes at cumulative k-tile percentages
+        monkeypatch.setenv("KW_E2E_KPASSES", ksplit[1:])
+    else:
+        monkeypatch.setenv("KW_E2E_KSPLIT", ksplit)
     monkeypatch.setenv("KW_E2E_MIN_INTENSITY", "0")  # small shapes: force the streamed schedule
-    rng = np.random.default_rng(int(panels) + 40 + 100 * int(ksplit))
+    rng = np.random.default_rng(int(panels) + 40 + 100 * len(ksplit))
     host = kw.Device.host()
     q = kw.Queue(gpu, kw.QueueFlavor.Async)
     for (m, n, k), tile in (((1500, 700, 333), 128), ((64, 64, 64), 128), ((129, 4100, 17), 128),

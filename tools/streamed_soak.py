@@ -28,6 +28,10 @@ def main():
         m, n, k = (int(v) for v in rng.integers(300, 3000, size=3))
         os.environ["KW_E2E_PANELS"] = str(int(rng.integers(2, 17)))
         os.environ["KW_E2E_KSPLIT"] = str(int(rng.choice([0, 2, 3, 4, 8, 64])))
+        os.environ.pop("KW_E2E_KPASSES", None)
+        if rng.random() < 0.4:  # several passes: random cumulative percentages
+            cuts = sorted(int(v) for v in rng.integers(1, 100, size=int(rng.integers(1, 5))))
+            os.environ["KW_E2E_KPASSES"] = ",".join(str(v) for v in cuts)
         a, b, c = rng.standard_normal((m, k)), rng.standard_normal((k, n)), rng.standard_normal((m, n))
         A, B, Cd = (kw.Buffer(gpu, kw.IndexVec(*x.shape), 8) for x in (a, b, c))
         for buf, x in ((A, a), (B, b), (Cd, c)):
@@ -42,7 +46,8 @@ def main():
         q.wait()
         if not np.array_equal(Ch.host_view()[:, :n], Cd.download()):
             bad += 1
-            print("MISMATCH", case, m, n, k, os.environ["KW_E2E_PANELS"], os.environ["KW_E2E_KSPLIT"], flush=True)
+            print("MISMATCH", case, m, n, k, os.environ["KW_E2E_PANELS"], os.environ["KW_E2E_KSPLIT"],
+                  os.environ.get("KW_E2E_KPASSES"), flush=True)
     print(f"{cases} streamed cases, {bad} mismatches, {time.time() - t0:.1f} s")
     return 1 if bad else 0
 
