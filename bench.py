@@ -269,8 +269,9 @@ def run_ours(args, dist: Dist) -> dict:
     hy.host_view()[:] = ys
     del x_all, y_all
     htask = kw.createExec(GPU, wd, kw.AxpyKernel(), kw.AxpyArgs(n, float(alpha), hx, hy))
-    q.enqueue(htask)
-    q.wait()
+    for _ in range(2):  # first host-buffer passes on a fresh box run slow (page state); keep them untimed
+        q.enqueue(htask)
+        q.wait()
     dist.barrier()
     sampler.active = True
     t0 = time.perf_counter()
@@ -695,7 +696,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--tpb", type=int, default=512)
     ap.add_argument("--ept", type=int, default=4)
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--dgemm-steps", type=int, default=10)
     ap.add_argument("--panels", type=int, default=8)
     ap.add_argument("--dgemm-timeout", type=float, default=300.0,
