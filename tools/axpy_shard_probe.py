@@ -1,7 +1,10 @@
 """AXPY per-GPU throughput at the shard sizes of the strong-scaling run (n = 2^28 / P for
 P = 1, 2, 4, 8): 400 back-to-back launches with the default division, CUDA-event timed, the way
 bench.py times one rank. Every shard is > L2 (126 MB) so each launch streams from HBM.
-Usage: python tools/axpy_shard_probe.py [tpb,ept ...]"""
+Usage: python tools/axpy_shard_probe.py [tpb,ept ...]
+KW_PROBE_ALT=1 alternates two disjoint (X, Y) pairs launch by launch, so no step can find the
+previous step's operands in L2 (separates a tail effect from cross-launch L2 retention)."""
+import os
 import ctypes as C
 import json
 import sys
@@ -21,6 +24,12 @@ def main():
     x, y = kw.Buffer(dev, kw.IndexVec(full), 4), kw.Buffer(dev, kw.IndexVec(full), 4)
     x.fill_raw(0x3F)
     y.fill_raw(0x3F)
+    pairs = [(x, y)]
+    if os.environ.get("KW_PROBE_ALT") == "1":
+        x2, y2 = kw.Buffer(dev, kw.IndexVec(full), 4), kw.Buffer(dev, kw.IndexVec(full), 4)
+        x2.fill_raw(0x3F)
+        y2.fill_raw(0x3F)
+        pairs.append((x2, y2))
     for P in (1, 2, 4, 8):
         n = full // P
         for d in divs:
@@ -31,8 +40,9 @@ def main():
             e0, e1 = C.c_void_p(), C.c_void_p()
             reps = 400
             lib.kw_event_record(q.handle(), C.byref(e0))
-            for _ in range(reps):
-                L.check(lib.kw_axpy_f32(q.handle(), wd, n, 1.0000001, x.data(), y.data()))
+            for i in range(reps):
+                xs, ys = pairs[i % len(pairs)]
+                L.check(lib.kw_axpy_f32(q.handle(), wd, n, 1.0000001, xs.data(), ys.data()))
             lib.kw_event_record(q.handle(), C.byref(e1))
             q.wait()
             ms = C.c_float()
