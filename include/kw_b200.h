@@ -224,9 +224,11 @@ KW_EXPORT kw_status kw_comm_broadcast(kw_comm comm, kw_queue q, void* buf, size_
 
 /* Row-block shard of C = alpha*A*B + beta*C across `world` ranks: this rank holds
  * rows [row0, row0+m_local) of A (lda) and C (ldc); B (k x n, ldb) is valid on `root` and is
- * broadcast in `panels` column panels into the caller's b_panels scratch (k*n doubles,
- * panel-major: panel j is k x w_j dense), each panel's broadcast (high-priority stream)
- * overlapped with the DGEMMs of earlier panels, which alternate between two compute streams.
+ * broadcast in `panels` column panels into the caller's b_panels scratch
+ * (kw_dgemm_rowsharded_scratch doubles, panel-major: panel j is k x w_j with leading dimension
+ * w_j rounded up to 8 — the Buffer pitch rule, so every panel is TMA-addressable), each panel's
+ * broadcast (high-priority stream; every rank, world 1 included, runs ncclBroadcast) overlapped
+ * with the DGEMMs of earlier panels, which alternate between two compute streams.
  * Every output element is reduced entirely on
  * one rank in the single-GPU kernel's order, so the gathered C is bitwise identical to the
  * 1-GPU kw_dgemm result. */
@@ -234,6 +236,8 @@ KW_EXPORT kw_status kw_dgemm_rowsharded(kw_comm comm, kw_queue q, size_t m_local
                                         double alpha, const double* A, size_t lda, const double* B, size_t ldb,
                                         double beta, double* C, size_t ldc, double* b_panels, int panels,
                                         int root);
+/* Doubles the b_panels scratch of kw_dgemm_rowsharded must hold for (n, k, panels). */
+KW_EXPORT kw_status kw_dgemm_rowsharded_scratch(size_t n, size_t k, int panels, size_t* elems);
 
 /* ---- measurement helpers (bench / tests) --------------------------------------------------- */
 /* Writes a device scratch buffer larger than L2 (flush between timed iterations). */

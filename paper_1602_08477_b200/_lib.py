@@ -82,6 +82,7 @@ SIGNATURES = {
     "kw_comm_broadcast": (st, [vp, vp, vp, size_t, C.c_int]),
     "kw_dgemm_rowsharded": (st, [vp, vp, size_t, size_t, size_t, C.c_double, vp, size_t, vp, size_t, C.c_double,
                                  vp, size_t, vp, C.c_int, C.c_int]),
+    "kw_dgemm_rowsharded_scratch": (st, [size_t, size_t, C.c_int, C.POINTER(size_t)]),
     "kw_l2_flush": (st, [vp]),
     "kw_launch_count": (C.c_uint64, []),
 }

@@ -40,7 +40,8 @@ def _stale(target: Path, deps: list[Path]) -> bool:
 
 
 def build_lib(force: bool = False, verbose: bool = False) -> Path:
-    """Compile csrc/*.cu for sm_100a and link libkw_b200.so (links NCCL for the broadcast)."""
+    """Compile csrc/*.cu for sm_100a and link libkw_b200.so. NCCL is not linked: kw_comm.cu
+    dlopens libnccl.so.2 at first use (the copy torch already loaded, when there is one)."""
     BUILD.mkdir(exist_ok=True)
     headers = list(CSRC.glob("*.cuh")) + [INCLUDE / "kw_b200.h"]
     objs = []
@@ -52,11 +53,14 @@ def build_lib(force: bool = False, verbose: bool = False) -> Path:
         if force or _stale(o, [s] + headers):
             jobs.append([NVCC, *ARCH, *NVCC_FLAGS, "-c", str(s), "-o", str(o)])
     if jobs:
+        logs = []
         with cf.ThreadPoolExecutor(max_workers=len(jobs)) as ex:
-            for out in ex.map(_run, jobs):
+            for cmd, out in zip(jobs, ex.map(_run, jobs)):
                 if verbose:
                     print(out)
-                (BUILD / "ptxas.log").open("a").write(out)
+                logs.append(f"== {Path(cmd[-3]).name}\n{out}")
+        # ptxas -v of the objects rebuilt by this call (overwritten, not appended)
+        (BUILD / "ptxas.log").write_text("".join(logs))
     if force or jobs or _stale(LIB, objs):
         _run([NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart", "-ldl"])
     return LIB

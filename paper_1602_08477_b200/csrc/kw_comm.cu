@@ -98,6 +98,15 @@ kw_status nccl_fail(const char* what, ncclResult_t r)
     return KW_TASK;
 }
 
+// Column panel width (a multiple of the 128-column tile) and the panel's leading dimension in the
+// panel-major scratch (sharding.dgemm_panels mirrors both).
+size_t panel_width(size_t n, int panels)
+{
+    const size_t tile = 128;
+    return kw::ceil_div(kw::ceil_div(n, static_cast<size_t>(panels)), tile) * tile;
+}
+size_t panel_ld(size_t wj) { return (wj + 7) & ~static_cast<size_t>(7); }
+
 kw_status ensure_events(kw_comm_s* c, int n)
 {
     while (static_cast<int>(c->panel_ready.size()) < n) {
@@ -196,6 +205,22 @@ kw_status kw_comm_broadcast(kw_comm c, kw_queue qh, void* buf, size_t bytes, int
     return kw::after_enqueue(q, "broadcast");
 }
 
+kw_status kw_dgemm_rowsharded_scratch(size_t n, size_t k, int panels, size_t* elems)
+{
+    if (!elems)
+        return kw::usage("kw_dgemm_rowsharded_scratch: null output");
+    if (panels < 1)
+        return kw::usage("dgemm_rowsharded: panels must be >= 1");
+    size_t total = 0;
+    if (n > 0) {
+        const size_t w = panel_width(n, panels);
+        for (size_t n0 = 0; n0 < n; n0 += w)
+            total += k * panel_ld(n - n0 < w ? n - n0 : w);
+    }
+    *elems = total;
+    return KW_OK;
+}
+
 kw_status kw_dgemm_rowsharded(kw_comm c, kw_queue qh, size_t m_local, size_t n, size_t k, double alpha,
                               const double* A, size_t lda, const double* B, size_t ldb, double beta, double* C,
                               size_t ldc, double* b_panels, int panels, int root)
@@ -223,8 +248,7 @@ kw_status kw_dgemm_rowsharded(kw_comm c, kw_queue qh, size_t m_local, size_t n, 
     if (m_local > 0 && ldc < n)
         return kw::usage("dgemm_rowsharded: ldc smaller than n");
     // Panel widths: multiples of the 128-column tile so every panel starts on a tile boundary.
-    const size_t tile = 128;
-    size_t w = kw::ceil_div(kw::ceil_div(n, static_cast<size_t>(panels)), tile) * tile;
+    const size_t w = panel_width(n, panels);
     const int np = static_cast<int>(kw::ceil_div(n, w));
     kw::DeviceGuard g(q->device);
     kw_status st = ensure_events(c, np);
@@ -243,12 +267,18 @@ kw_status kw_dgemm_rowsharded(kw_comm c, kw_queue qh, size_t m_local, size_t n, 
     size_t off = 0;
     for (int j = 0; j < np && e == cudaSuccess && r == ncclSuccess; ++j) {
         const size_t n0 = static_cast<size_t>(j) * w, wj = n - n0 < w ? n - n0 : w;
-        double* panel = b_panels + off; // k x wj dense
+        // k x wj panel at the Buffer pitch rule (leading dimension a multiple of 8 doubles): an
+        // odd-width last panel stays TMA-addressable, so it runs the same kernel (and k grouping)
+        // as the resident 1-GPU launch — a dense odd pitch would drop to the cp.async kernel.
+        const size_t ldp = panel_ld(wj);
+        double* panel = b_panels + off;
         if (k > 0) {
             if (c->rank == root)
-                e = cudaMemcpy2DAsync(panel, wj * 8, B + n0, ldb * 8, wj * 8, k, cudaMemcpyDeviceToDevice, c->stream);
-            if (e == cudaSuccess && c->world > 1)
-                r = ncclBroadcast(panel, panel, k * wj * sizeof(double), ncclChar, root, c->comm, c->stream);
+                e = cudaMemcpy2DAsync(panel, ldp * 8, B + n0, ldb * 8, wj * 8, k, cudaMemcpyDeviceToDevice, c->stream);
+            // Every rank, world 1 included, runs the broadcast: a single-rank ncclBroadcast is legal
+            // and keeps the one-GPU path the code path of the multi-GPU one.
+            if (e == cudaSuccess)
+                r = ncclBroadcast(panel, panel, k * ldp * sizeof(double), ncclChar, root, c->comm, c->stream);
         }
         if (e == cudaSuccess)
             e = cudaEventRecord(c->panel_ready[j], c->stream);
@@ -256,11 +286,11 @@ kw_status kw_dgemm_rowsharded(kw_comm c, kw_queue qh, size_t m_local, size_t n, 
         if (e == cudaSuccess)
             e = cudaStreamWaitEvent(cs, c->panel_ready[j], 0);
         if (e == cudaSuccess && m_local > 0) {
-            st = kw::dgemm_device(cs, 128, m_local, wj, k, alpha, A, lda, panel, wj, beta, C + n0, ldc);
+            st = kw::dgemm_device(cs, 128, m_local, wj, k, alpha, A, lda, panel, ldp, beta, C + n0, ldc);
             if (st != KW_OK)
                 return kw::task_fail(q, kw::last_error());
         }
-        off += k * wj;
+        off += k * ldp;
     }
     if (e == cudaSuccess)
         e = cudaEventRecord(q->ev_join2, q->comp2);

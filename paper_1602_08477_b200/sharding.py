@@ -4,8 +4,9 @@ AXPY: contiguous index ranges, boundaries on 16-byte multiples; no collective â€
 is independent, so the sharded result is bit-identical to one GPU by construction.
 
 DGEMM: rank r owns row block r of A and C (boundaries on the 128-row tile); B lives on the root
-and is broadcast (ncclBroadcast over NVLink) in column panels, panel j packed dense (k x w_j) in
-the panel-major scratch, each panel's broadcast overlapped with the previous panel's DGEMM.
+and is broadcast (ncclBroadcast over NVLink) in column panels, panel j stored k x w_j at leading
+dimension round8(w_j) in the panel-major scratch (the Buffer pitch rule, so an odd-width last
+panel stays TMA-addressable), each panel's broadcast overlapped with the previous panel's DGEMM.
 `dgemm_panels` is the exact layout kw_dgemm_rowsharded uses (kw_comm.cu), so host code and
 tests can reproduce it.
 """
@@ -37,7 +38,8 @@ class Panel:
     index: int
     n0: int          # first column of B / C
     width: int       # columns in this panel
-    offset: int      # element offset of the dense k x width panel in the panel-major scratch
+    offset: int      # element offset of the k x width panel in the panel-major scratch
+    ld: int = 0      # its leading dimension: width rounded up to 8 doubles (Buffer pitch rule)
 
 
 def dgemm_panels(n: int, k: int, panels: int, tile: int = 128) -> list[Panel]:
@@ -49,6 +51,12 @@ def dgemm_panels(n: int, k: int, panels: int, tile: int = 128) -> list[Panel]:
     for j in range(ceil_div(n, w)):
         n0 = j * w
         wj = min(w, n - n0)
-        out.append(Panel(j, n0, wj, off))
-        off += k * wj
+        ld = ceil_div(wj, 8) * 8
+        out.append(Panel(j, n0, wj, off, ld))
+        off += k * ld
     return out
+
+
+def dgemm_panel_scratch(n: int, k: int, panels: int, tile: int = 128) -> int:
+    """Doubles of panel-major scratch kw_dgemm_rowsharded needs (kw_dgemm_rowsharded_scratch)."""
+    return sum(k * p.ld for p in dgemm_panels(n, k, panels, tile))

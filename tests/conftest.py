@@ -12,6 +12,7 @@ sys.path.insert(0, str(ROOT))
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA GPU (B200); parity tests through the C-ABI")
+    config.addinivalue_line("markers", "multigpu: one NCCL rank per visible GPU; skipped below 2 GPUs")
 
 
 @pytest.fixture(scope="session")

@@ -182,22 +182,42 @@ def test_row_panels_and_column_panels_are_bitwise_invariant(gpu, oracle):
     assert np.array_equal(full, cols)
 
 
-def test_rowsharded_single_rank_pipeline(gpu, oracle):
-    """kw_dgemm_rowsharded with world = 1 (NCCL single-rank communicator) exercises the
-    panel-broadcast pipeline on one GPU and must equal kw_dgemm bit for bit."""
+@pytest.mark.parametrize("n,panels", [(1000, 3), (1001, 3), (1001, 8), (127, 2), (2049, 5)])
+def test_rowsharded_single_rank_pipeline(gpu, oracle, n, panels):
+    """kw_dgemm_rowsharded with world = 1 (NCCL single-rank communicator): every panel goes
+    through ncclBroadcast (a single-rank broadcast is executed, not skipped), then the panel
+    DGEMMs on two compute streams. Must equal kw_dgemm bit for bit — including odd n, where the
+    last panel has an odd width and a padded leading dimension (a dense odd pitch
+    would drop that panel to the non-TMA kernel and change its k grouping)."""
+    from paper_1602_08477_b200 import sharding as S
     rng = np.random.default_rng(5)
-    m, n, k = 256, 1000, 200
+    m, k = 256, 200
     a, b, c = rng.random((m, k)) * 10, rng.random((k, n)) * 10, rng.random((m, n)) * 10
     want = tiled(gpu, 1.1, 0.9, a, b, c)
     uid = (C.c_char * 128)()
     assert L.lib().kw_comm_unique_id(uid) == 0
     comm = C.c_void_p()
     assert L.lib().kw_comm_init(C.byref(comm), 0, 1, 0, uid) == 0, L.last_error()
+    elems = C.c_size_t()
+    assert L.lib().kw_dgemm_rowsharded_scratch(n, k, panels, C.byref(elems)) == 0
+    assert elems.value == S.dgemm_panel_scratch(n, k, panels)
     A, B, Cb = mat(gpu, a), mat(gpu, b), mat(gpu, c)
-    panels = kw.Buffer(gpu, kw.IndexVec(k * n), 8)
+    scratch = kw.Buffer(gpu, kw.IndexVec(elems.value), 8)
     q = kw.Queue(gpu, kw.QueueFlavor.Async)
     st = L.lib().kw_dgemm_rowsharded(comm, q.handle(), m, n, k, 1.1, A.data(), A.leadingDim(), B.data(),
-                                     B.leadingDim(), 0.9, Cb.data(), Cb.leadingDim(), panels.data(), 3, 0)
+                                     B.leadingDim(), 0.9, Cb.data(), Cb.leadingDim(), scratch.data(), panels, 0)
+    assert st == 0, L.last_error()
+    q.wait()
+    assert np.array_equal(Cb.download(), want)
+    # the scratch holds exactly the broadcast panels at their padded pitch
+    got = scratch.download()
+    for p in S.dgemm_panels(n, k, panels):
+        blk = got[p.offset:p.offset + k * p.ld].reshape(k, p.ld)[:, :p.width]
+        assert np.array_equal(blk, b[:, p.n0:p.n0 + p.width])
+    # a second call on the same communicator (events reused) gives the same bits from pristine C
+    Cb.upload(c)
+    st = L.lib().kw_dgemm_rowsharded(comm, q.handle(), m, n, k, 1.1, A.data(), A.leadingDim(), B.data(),
+                                     B.leadingDim(), 0.9, Cb.data(), Cb.leadingDim(), scratch.data(), panels, 0)
     assert st == 0, L.last_error()
     q.wait()
     assert np.array_equal(Cb.download(), want)

@@ -42,22 +42,24 @@ def _worker(rank, world, port, q):
         axpy_ok = np.array_equal(full, O.axpy(alpha, x, y))
 
         # ---- DGEMM: row blocks + panel-major broadcast of B from rank 0
-        m, nn, k = 300, 520, 77
+        m, nn, k = 300, 521, 77  # odd n: the last panel's leading dimension is padded
         rng = np.random.default_rng(5)
         a = rng.random((m, k)) * 10
         c = rng.random((m, nn)) * 10
         b_root = rng.random((k, nn)) * 10 if rank == 0 else None
         r0, r1 = S.dgemm_rows(m, world, rank)
         panels = S.dgemm_panels(nn, k, 3)
-        scratch = torch.zeros(k * nn, dtype=torch.float64)
+        scratch = torch.zeros(S.dgemm_panel_scratch(nn, k, 3), dtype=torch.float64)
         for p in panels:
-            view = scratch[p.offset:p.offset + k * p.width]
+            view = scratch[p.offset:p.offset + k * p.ld]
             if rank == 0:
-                view.copy_(torch.from_numpy(np.ascontiguousarray(b_root[:, p.n0:p.n0 + p.width]).reshape(-1)))
+                padded = np.zeros((k, p.ld))
+                padded[:, :p.width] = b_root[:, p.n0:p.n0 + p.width]
+                view.copy_(torch.from_numpy(padded.reshape(-1)))
             dist.broadcast(view, src=0)
         cl = c[r0:r1].copy()
         for p in panels:
-            bp = scratch[p.offset:p.offset + k * p.width].numpy().reshape(k, p.width)
+            bp = scratch[p.offset:p.offset + k * p.ld].numpy().reshape(k, p.ld)[:, :p.width]
             cl[:, p.n0:p.n0 + p.width] = O.gemm(1.3, 0.7, a[r0:r1], bp, c[r0:r1, p.n0:p.n0 + p.width], threads=1)
         blocks = [None] * world
         dist.all_gather_object(blocks, (r0, cl))
@@ -106,5 +108,10 @@ def test_panel_layout_matches_the_c_abi_rule():
     ps = S.dgemm_panels(16384, 16384, 8)
     assert [p.width for p in ps] == [2048] * 8
     assert ps[-1].offset + 16384 * ps[-1].width == 16384 * 16384
+    assert S.dgemm_panel_scratch(16384, 16384, 8) == 16384 * 16384
     ps = S.dgemm_panels(1000, 200, 3)
     assert [p.width for p in ps] == [384, 384, 232] and [p.n0 for p in ps] == [0, 384, 768]
+    ps = S.dgemm_panels(1001, 200, 3)
+    assert [p.width for p in ps] == [384, 384, 233] and [p.ld for p in ps] == [384, 384, 240]
+    assert [p.offset for p in ps] == [0, 200 * 384, 2 * 200 * 384]
+    assert S.dgemm_panel_scratch(1001, 200, 3) == 200 * (384 + 384 + 240)
