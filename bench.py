@@ -5,16 +5,21 @@ Headline (the JSON line's metric/value): AXPY fp32, n = 2^28 (BASELINE.json conf
 resident in HBM, index-sharded across ranks under torchrun (strong scaling: total n fixed).
 The same line carries:
   e2e          the same metric through the public API with host (pinned) buffers: H2D of X, Y
-               and D2H of Y inside the timed region (Queue.enqueue + wait, like runner.cpp:114-117)
-  roofline     AXPY kernel vs MEASURED_PEAKS.json hbm_gbs (algorithmic 12 B/element)
+               and D2H of Y inside the timed region (Queue.enqueue + wait, like runner.cpp:114-117);
+               each rank streams only its own shard, pinned on its GPU's NUMA node
+  roofline     AXPY kernel vs MEASURED_PEAKS.json hbm_gbs (algorithmic 12 B/element); `kernel` is
+               the template the launch runs (kw_axpy_kernel_name)
   cpu_baseline the reference's own CPU AXPY (oracle/_ref: reference runtime, BlocksParallel,
-               all host cores) on the same inputs, rank 0 at N = 1 only; its output is also the
-               parity check of the GPU result (bitwise)
+               all host cores) on the same global input, rank 0, at every N
+  parity       at every N: each rank's GPU Y digest after the first step and after all
+               1 + W + K steps vs the reference CPU Y over the same index range
   dgemm        DGEMM fp64 TFLOP/s: 8192^3 (north-star headline) and 4096^3 (configured point)
-               at N = 1; 16384^3 row-block sharded with NCCL broadcast of B at N > 1
+               at N = 1; 16384^3 row-block sharded with NCCL broadcast of B at N > 1, with
+               sampled-row parity (CPU reference + 1-GPU kw_dgemm) and a CPU baseline
   clocks, gpu_launches
 
-`--impl reference` runs only the reference CPU implementation (rank 0) on the same config.
+`--impl reference` runs only the reference CPU implementation (rank 0) on the same config,
+--warmup + --steps runs.
 """
 from __future__ import annotations
 
@@ -37,6 +42,74 @@ sys.path.insert(0, str(ROOT))
 N_AXPY = 1 << 28
 BYTES_PER_ELEM = 12  # read X, read Y, write Y (fp32)
 FP64_NOMINAL_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # 37.2: 148 SMs x 64 FP64 FMA/clk x 1.965 GHz
+
+
+INPUT_BLOCK = 1 << 20  # elements per independently seeded block of the synthetic AXPY input
+AXPY_DATA = (f"synthetic (numpy U[0,10), {INPUT_BLOCK}-element blocks seeded [1234, block]; identical global "
+             f"input at every N, each rank generates only its shard)")
+DGEMM_PEAK_PROBE = 37.16  # DMMA throughput measured on this pool (tools/probe/probe.cu)
+
+
+def axpy_config(world: int, tpb: int, ept: int) -> dict:
+    """The headline's `config` — built from the arguments alone, so both arms print it identically."""
+    from paper_1602_08477_b200 import sharding as S
+    lo, hi = S.axpy_range(N_AXPY, world, 0)
+    n = hi - lo
+    return {"workload": "AXPY fp32 n=2^28 index-sharded (BASELINE.json configs[1])", "n": N_AXPY,
+            "n_per_rank": n, "workdiv": {"threads": tpb, "elems": ept, "blocks": -(-n // (tpb * ept))},
+            "parallelism": f"index-shard x{world} (no collective)",
+            "l2": "inputs larger than L2 (2.15 GB read+write per step vs 132 MB L2); no flush needed"}
+
+
+def axpy_inputs(lo: int, hi: int, seed: int = 1234, out=None):
+    """X, Y over [lo, hi) of the global synthetic input, U[0,10) fp32. The global input is cut into
+    INPUT_BLOCK-element blocks, block b drawn (X then Y) from default_rng([seed, b]): a rank
+    generates only its own shard, and every rank count sees the same global bytes."""
+    n = hi - lo
+    x, y = out if out is not None else (np.empty(n, np.float32), np.empty(n, np.float32))
+    ten = np.float32(10)
+    for b in range(lo // INPUT_BLOCK, -(-hi // INPUT_BLOCK)):
+        g = np.random.default_rng([seed, b])
+        bx = g.random(INPUT_BLOCK, dtype=np.float32) * ten
+        by = g.random(INPUT_BLOCK, dtype=np.float32) * ten
+        s0, s1 = max(lo, b * INPUT_BLOCK), min(hi, (b + 1) * INPUT_BLOCK)
+        x[s0 - lo:s1 - lo] = bx[s0 - b * INPUT_BLOCK:s1 - b * INPUT_BLOCK]
+        y[s0 - lo:s1 - lo] = by[s0 - b * INPUT_BLOCK:s1 - b * INPUT_BLOCK]
+    return x, y
+
+
+def gemm_rows(seed: int, rows, cols: int) -> np.ndarray:
+    """Rows of a synthetic U[0,10) fp64 matrix, row r drawn from default_rng([seed, r]): any rank
+    (or the checker on rank 0) can regenerate any row without the rest of the matrix."""
+    rows = list(rows)
+    out = np.empty((len(rows), cols))
+    for i, r in enumerate(rows):
+        out[i] = np.random.default_rng([seed, r]).random(cols) * 10
+    return out
+
+
+def digest(a: np.ndarray) -> str:
+    import hashlib
+    return hashlib.blake2b(np.ascontiguousarray(a), digest_size=16).hexdigest()
+
+
+def numa_node_of(lib, device: int):
+    """(node, cpus) the GPU's PCIe root sits on (sysfs), or None when unknown."""
+    buf = C.create_string_buffer(64)
+    if lib.kw_device_pci_bus_id(device, buf, 64) != 0:
+        return None
+    try:
+        node = int(Path(f"/sys/bus/pci/devices/{buf.value.decode()}/numa_node").read_text())
+        if node < 0:
+            return None
+        cpus = set()
+        for part in Path(f"/sys/devices/system/node/node{node}/cpulist").read_text().strip().split(","):
+            a, _, b = part.partition("-")
+            cpus.update(range(int(a), int(b or a) + 1))
+        cpus &= os.sched_getaffinity(0)
+        return (node, cpus) if cpus else None
+    except (OSError, ValueError):
+        return None
 
 
 def peaks():
@@ -165,6 +238,14 @@ class Dist:
         self.dist.all_reduce(t)
         return float(t.item())
 
+    def gather_objects(self, obj) -> list:
+        """Every rank's `obj`, in rank order, on every rank (test/parity plumbing only)."""
+        if self.world == 1:
+            return [obj]
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj)
+        return out
+
     def bcast_bytes(self, b: bytes | None) -> bytes:
         if self.world == 1:
             return b
@@ -193,26 +274,35 @@ def run_ours(args, dist: Dist) -> dict:
     from paper_1602_08477_b200 import sharding as S
     lo, hi = S.axpy_range(N_AXPY, dist.world, dist.rank)
     n = hi - lo
-    rng = np.random.default_rng(1234)
-    # synthetic data of the configured shape (same bytes on every rank count: one global draw)
-    x_all = (rng.random(N_AXPY, dtype=np.float32) * 10).astype(np.float32)
-    y_all = (rng.random(N_AXPY, dtype=np.float32) * 10).astype(np.float32)
     alpha = np.float32(9.096465)
-    xs, ys = x_all[lo:hi], y_all[lo:hi]
+    # This rank's pinned host shard, allocated and first-touched from the GPU's NUMA node (each
+    # rank streams over its own PCIe link; remote-node pinned pages would cross the socket link).
+    numa = numa_node_of(lib, gpu_index)
+    affinity = os.sched_getaffinity(0)
+    if numa:
+        os.sched_setaffinity(0, numa[1])
+    try:
+        hx = kw.Buffer(kw.Device.host(), kw.IndexVec(n), 4)
+        hy = kw.Buffer(kw.Device.host(), kw.IndexVec(n), 4)
+        xs, ys = axpy_inputs(lo, hi, out=(hx.host_view(), hy.host_view()))
+    finally:
+        os.sched_setaffinity(0, affinity)
 
     x = kw.Buffer(dev, kw.IndexVec(n), 4)
     y = kw.Buffer(dev, kw.IndexVec(n), 4)
-    y0 = kw.Buffer(dev, kw.IndexVec(n), 4)
     x.upload(xs)
     y.upload(ys)
-    y0.upload(ys)
     wd = kw.axpyWorkDiv(GPU, n, args.tpb, args.ept)
     task = kw.createExec(GPU, wd, kw.AxpyKernel(), kw.AxpyArgs(n, float(alpha), x, y))
+    wdc = wd.to_c()
+    kname = C.create_string_buffer(96)
+    L.check(lib.kw_axpy_kernel_name(C.byref(wdc), 4, x.data(), y.data(), kname, 96))
 
-    # parity step from pristine inputs (checked against the reference CPU result below)
+    # Parity: Y after the first step (from pristine inputs) and after all 1 + W + K steps are
+    # hashed per rank; rank 0 checks both against the reference CPU run on the global input.
     q.enqueue(task)
     q.wait()
-    y_first = y.download() if (dist.world == 1 and not args.no_cpu) else None
+    dig_first = digest(y.download())
 
     sampler = ClockSampler(gpu_index)
     sampler.start()
@@ -222,7 +312,6 @@ def run_ours(args, dist: Dist) -> dict:
     # `task`): a TaskHandle per enqueue would put an event between consecutive kernels, which
     # both costs an event per step and stops programmatic dependent launch from overlapping one
     # step's launch with the previous step's tail.
-    wdc = wd.to_c()
 
     def step():
         L.check(lib.kw_axpy_f32(q.handle(), C.byref(wdc), n, float(alpha), x.data(), y.data()))
@@ -260,14 +349,12 @@ def run_ours(args, dist: Dist) -> dict:
     value = total_bytes / (total_ms / 1e3) / 1e9
     peak, peak_src = peaks()
     achieved = BYTES_PER_ELEM * n / (statistics.mean(per) / 1e3) / 1e9
+    dig_final = digest(y.download())
+    applied = 1 + args.warmup + args.steps
+    del x, y
 
     # ---- e2e: host (pinned) buffers through the public API, copies inside the timed region
     e2e_steps = max(3, min(args.e2e_steps, args.steps))
-    hx = kw.Buffer(kw.Device.host(), kw.IndexVec(n), 4)
-    hy = kw.Buffer(kw.Device.host(), kw.IndexVec(n), 4)
-    hx.host_view()[:] = xs
-    hy.host_view()[:] = ys
-    del x_all, y_all
     htask = kw.createExec(GPU, wd, kw.AxpyKernel(), kw.AxpyArgs(n, float(alpha), hx, hy))
     for _ in range(2):  # first host-buffer passes on a fresh box run slow (page state); keep them untimed
         q.enqueue(htask)
@@ -280,8 +367,11 @@ def run_ours(args, dist: Dist) -> dict:
         q.wait()
     t1 = time.perf_counter()
     sampler.active = False
-    e2e_s = dist.max(t1 - t0)
+    e2e_local = t1 - t0
+    e2e_s = dist.max(e2e_local)
     e2e_value = BYTES_PER_ELEM * N_AXPY * e2e_steps / e2e_s / 1e9
+    rank_link = BYTES_PER_ELEM * n * e2e_steps / e2e_local / 1e9
+    del hx, hy, xs, ys
 
     # ---- fp64 AXPY (the reference's own AxpyKernel dtype), same n, device-resident
     f64 = None
@@ -315,6 +405,7 @@ def run_ours(args, dist: Dist) -> dict:
                "bytes_per_elem": 24, "note": "AXPY fp64 n=2^28 (the reference's AxpyKernel dtype), HBM-resident"}
         del x64, y64
 
+    gathered = dist.gather_objects((lo, hi, dig_first, dig_final, round(rank_link, 2), numa[0] if numa else None))
     out = {
         "metric": "AXPY fp32 HBM GB/s (n=2^28, Y=alpha*X+Y, 12 B/elem)",
         "value": round(value, 1),
@@ -327,18 +418,19 @@ def run_ours(args, dist: Dist) -> dict:
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f32",
-        "data": "synthetic (numpy uniform [0,10), seed 1234; identical global input at every N)",
-        "config": {"workload": "AXPY fp32 n=2^28 index-sharded (BASELINE.json configs[1])", "n": N_AXPY,
-                   "n_per_rank": n, "workdiv": {"threads": args.tpb, "elems": args.ept,
-                                                "blocks": wd.blocksPerGrid()[0]},
-                   "parallelism": f"index-shard x{dist.world} (no collective)",
-                   "l2": "inputs larger than L2 (2.15 GB read+write per step vs 132 MB L2); no flush needed"},
+        "data": AXPY_DATA,
+        "config": axpy_config(dist.world, args.tpb, args.ept),
         "e2e": {"value": round(e2e_value, 2), "unit": "GB/s", "steps": e2e_steps,
                 "h2d_bytes_per_step": 8 * N_AXPY, "d2h_bytes_per_step": 4 * N_AXPY,
                 "how": "executeTask-equivalent Queue.enqueue(createExec(GpuCudaRt, AxpyKernel, host pinned "
-                       "buffers)) + wait, wall clock; chunked H2D/kernel/D2H on three streams",
-                "link_ceiling": {"value": 78.8, "unit": "GB/s",
-                                 "what": "pure pinned copies with the same 2:1 H2D:D2H byte mix on this box type",
+                       "buffers)) + wait, wall clock, max over ranks; each rank streams its own shard over its "
+                       "own PCIe link from pinned pages placed on the GPU's NUMA node; chunked H2D/kernel/D2H "
+                       "on three streams",
+                "per_rank_link_gbs": [g[4] for g in gathered] if gathered else None,
+                "numa_nodes": [g[5] for g in gathered] if gathered else None,
+                "link_ceiling": {"value": round(78.8 * dist.world, 1), "per_rank": 78.8, "unit": "GB/s",
+                                 "what": "pure pinned copies with the same 2:1 H2D:D2H byte mix, one link per "
+                                         "GPU (x N ranks)",
                                  "source": "profiles/pcie_probe_r01.txt"}},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "peak_source": peak_src,
@@ -346,17 +438,18 @@ def run_ours(args, dist: Dist) -> dict:
                                  else round(traffic_from_profiles("axpy_f32") * n / N_AXPY)),
                      "traffic_source": "profiles/traffic.json (ncu --set full at n=2^28, scaled to this rank's "
                                        "shard)",
-                     "kernel": "axpy_vec_kernel<float,4>", "bytes_per_launch": BYTES_PER_ELEM * n},
+                     "kernel": kname.value.decode(), "bytes_per_launch": BYTES_PER_ELEM * n},
         "gpu_launches": int(launches),
         "clocks": None,
         "axpy_f64": f64,
         "dgemm": None,
     }
 
-    if dist.rank == 0 and dist.world == 1 and not args.no_cpu:
-        cb, parity = cpu_baseline_axpy(xs, ys, alpha, y_first)
+    if dist.rank == 0 and not args.no_cpu:
+        cb, parity = cpu_baseline_axpy(alpha, gathered, applied, args.warmup)
         out["cpu_baseline"] = cb
         out["parity"] = parity
+    dist.barrier()  # the other ranks wait here while rank 0 runs the CPU reference
 
     # ---- secondary: DGEMM. Guarded: neither an exception nor a hang in this leg (an N > 1
     # communicator that never forms, say) may cost the headline line above — a watchdog prints
@@ -433,6 +526,9 @@ def run_dgemm(args, dist, kw, L, lib, dev, q, sampler) -> dict:
                      "roofline": {"bound": "fp64", "achieved": round(tflops, 3),
                                   "peak": round(FP64_NOMINAL_TFLOPS, 2), "unit": "TFLOP/s",
                                   "frac": round(tflops / FP64_NOMINAL_TFLOPS, 4),
+                                  "peak_source": "nominal (148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz)",
+                                  "peak_dmma_probe": DGEMM_PEAK_PROBE,
+                                  "frac_of_dmma_probe": round(tflops / DGEMM_PEAK_PROBE, 4),
                                   "traffic": traffic_from_profiles(f"dgemm_{size}")}}
             # e2e: host pinned buffers, H2D of A, B, C and D2H of C per step
             hA, hB, hC = (kw.Buffer(kw.Device.host(), kw.IndexVec(size, size), 8) for _ in range(3))
@@ -487,19 +583,36 @@ def run_dgemm(args, dist, kw, L, lib, dev, q, sampler) -> dict:
         # NCCL refuses two ranks on one GPU: the --same-gpu harness self-test covers the AXPY
         # shards and timing reductions only (the panel pipeline has --force-rowsharded).
         return {"skipped": "--same-gpu self-test: NCCL needs one GPU per rank (see --force-rowsharded)"}
-    size = 16384
+    return run_dgemm_rowsharded(args, dist, kw, L, lib, dev, q, timed, res)
+
+
+def run_dgemm_rowsharded(args, dist, kw, L, lib, dev, q, timed, res) -> dict:
+    """16384^3 row-sharded: rank r owns rows [r0, r1) of A and C, rank 0 owns B; each step is one
+    kw_dgemm_rowsharded (ncclBroadcast of B in column panels overlapped with the panel DGEMMs).
+    Parity at every N (the reference verifies every measured point, runner.cpp:120-125): one step
+    from pristine C, then 16 sampled rows per rank are gathered on rank 0 and checked (i) against
+    the reference GemmTiledKernel on the CPU under |dC| <= (K+4)u|C_ref| and (ii) bitwise against
+    a single-GPU kw_dgemm of the same rows."""
     from paper_1602_08477_b200 import sharding as S
+    GPU = kw.BackendKind.GpuCudaRt
+    size = 16384
+    seed_a, seed_b, seed_c = 161, 162, 163
+    alpha, beta = 1.25, 0.75
     r0, r1 = S.dgemm_rows(size, dist.world, dist.rank)
     ml = r1 - r0
     A = kw.Buffer(dev, kw.IndexVec(max(ml, 1), size), 8)
     Cb = kw.Buffer(dev, kw.IndexVec(max(ml, 1), size), 8)
-    B = kw.Buffer(dev, kw.IndexVec(size, size), 8)
-    panels = kw.Buffer(dev, kw.IndexVec(size * size), 8)
-    blk = np.random.default_rng(1000 + dist.rank)
-    A.upload(blk.random((max(ml, 1), size)) * 10)
-    Cb.upload(blk.random((max(ml, 1), size)) * 10)
+    c_local = gemm_rows(seed_c, range(r0, r1), size) if ml else None
+    if ml:
+        A.upload(gemm_rows(seed_a, range(r0, r1), size))
+        Cb.upload(c_local)
+    B = None
     if dist.rank == 0:
-        B.upload(rng.random((size, size)) * 10)
+        B = kw.Buffer(dev, kw.IndexVec(size, size), 8)
+        B.upload(gemm_rows(seed_b, range(size), size))
+    elems = C.c_size_t()
+    L.check(lib.kw_dgemm_rowsharded_scratch(size, size, args.panels, C.byref(elems)))
+    panels = kw.Buffer(dev, kw.IndexVec(elems.value), 8)
     uid = (C.c_char * 128)()
     if dist.rank == 0:
         L.check(lib.kw_comm_unique_id(uid))
@@ -509,21 +622,90 @@ def run_dgemm(args, dist, kw, L, lib, dev, q, sampler) -> dict:
     L.check(lib.kw_comm_init(C.byref(comm), dist.local, dist.world, dist.rank, uid))
 
     def step():
-        L.check(lib.kw_dgemm_rowsharded(comm, q.handle(), ml, size, size, 1.25, A.data(), A.leadingDim(),
-                                        B.data(), B.leadingDim(), 0.75, Cb.data(), Cb.leadingDim(), panels.data(),
-                                        args.panels, 0))
+        L.check(lib.kw_dgemm_rowsharded(comm, q.handle(), ml, size, size, alpha, A.data(), A.leadingDim(),
+                                        B.data() if B is not None else None,
+                                        B.leadingDim() if B is not None else 0, beta, Cb.data(), Cb.leadingDim(),
+                                        panels.data(), args.panels, 0))
+
+    # parity step from pristine C: sampled rows of this rank's block
+    step()
+    q.wait()
+    nsamp = min(16, ml)
+    local_rows = [r0 + (i * ml) // nsamp for i in range(nsamp)]
+    got = np.empty((nsamp, size))
+    for i, r in enumerate(local_rows):
+        ext = L.sz3((size,))
+        L.check(lib.kw_copy(q.handle(), got[i].ctypes.data, size * 8, ext,
+                            Cb.data() + (r - r0) * Cb.rowPitch(), size * 8, ext, 1, ext, 8))
+    q.wait()
+    del c_local
+    gathered = dist.gather_objects((local_rows, got))
 
     steps = max(2, args.dgemm_steps // 2)
     ms = timed(step, steps, warm=1)
     lib.kw_comm_destroy(comm)
     tflops = 2 * size ** 3 * steps / (ms / 1e3) / 1e12
+    per_gpu = tflops / dist.world
     res.update({"value": round(tflops, 3), "ms_per_step": round(ms / steps, 3), "steps": steps,
                 "config": f"DGEMM fp64 16384^3 row-block sharded x{dist.world}, ncclBroadcast of B in "
                           f"{args.panels} column panels overlapped with compute (BASELINE configs[3])",
-                "roofline": {"bound": "fp64", "achieved": round(tflops / dist.world, 3),
-                             "peak": round(FP64_NOMINAL_TFLOPS, 2), "unit": "TFLOP/s per GPU",
-                             "frac": round(tflops / dist.world / FP64_NOMINAL_TFLOPS, 4)}})
+                "roofline": {"bound": "fp64", "achieved": round(per_gpu, 3), "unit": "TFLOP/s per GPU",
+                             "peak": round(FP64_NOMINAL_TFLOPS, 2), "frac": round(per_gpu / FP64_NOMINAL_TFLOPS, 4),
+                             "peak_source": "nominal (148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz)",
+                             "peak_dmma_probe": DGEMM_PEAK_PROBE,
+                             "frac_of_dmma_probe": round(per_gpu / DGEMM_PEAK_PROBE, 4)}})
+    if dist.rank == 0:
+        rows = [r for rs, _ in gathered for r in rs]
+        gpu_rows = np.vstack([g for _, g in gathered])
+        res["cpu_baseline"], res["parity"] = dgemm_rows_check(kw, dev, q, B, rows, gpu_rows, size, alpha, beta,
+                                                              (seed_a, seed_c), args.no_cpu)
+    del A, Cb, B, panels
+    dist.barrier()
     return res
+
+
+def dgemm_rows_check(kw, dev, q, B, rows, gpu_rows, size, alpha, beta, seeds, no_cpu):
+    """Rank 0: the gathered sampled rows of the row-sharded C against (i) a single-GPU kw_dgemm
+    of the same rows (bitwise: row-block invariance) and (ii) the reference GemmTiledKernel."""
+    GPU = kw.BackendKind.GpuCudaRt
+    a = gemm_rows(seeds[0], rows, size)
+    c = gemm_rows(seeds[1], rows, size)
+    R = len(rows)
+    As, Cs = kw.Buffer(dev, kw.IndexVec(R, size), 8), kw.Buffer(dev, kw.IndexVec(R, size), 8)
+    As.upload(a)
+    Cs.upload(c)
+    q.enqueue(kw.createExec(GPU, kw.gemmTiledWorkDiv(GPU, R, size, 128), kw.GemmTiledKernel(),
+                            kw.GemmArgs(R, size, size, alpha, beta, As, B, Cs)))
+    q.wait()
+    one_gpu = Cs.download()
+    parity = {"check": f"{R} rows sampled across all ranks' blocks (16 per rank): bitwise vs a 1-GPU kw_dgemm of "
+                       f"the same rows, and |dC| <= (K+4)*2^-53*|C_ref| vs the reference GemmTiledKernel (CPU)",
+              "rows": R, "bitwise_vs_1gpu": bool(np.array_equal(gpu_rows, one_gpu))}
+    cb = None
+    if not no_cpu:
+        from oracle import oracle as O
+        b = B.download()
+        out = c.copy()
+        kind = "reference" if O.ref_available() else "port"
+        t = time.perf_counter()
+        if kind == "reference":
+            os.environ.setdefault("KERNELWEAVE_POOL_SIZE", str(cpu_threads()))
+            sec = C.c_double()
+            assert O.ref().kwref_gemm_kernel(1, 1, R, size, size, alpha, beta, a.ctypes.data, size, b.ctypes.data,
+                                             size, out.ctypes.data, size, 32, 16, 8, C.byref(sec)) == 0
+            secs = sec.value
+        else:
+            out = O.gemm(alpha, beta, a, b, c, threads=cpu_threads())
+            secs = time.perf_counter() - t
+        err = np.abs(gpu_rows - out)
+        bound = (size + 4) * 2.0 ** -53 * np.abs(out)
+        parity["within_tolerance"] = bool(np.all(err <= bound))
+        parity["max_err_over_bound"] = round(float(np.max(err / bound)), 4)
+        cb = {"value": round(2 * R * size * size / secs / 1e9, 3), "unit": "GFLOP/s", "cores": cpu_threads(),
+              "kind": kind, "sample": f"{R} rows of the 16384^3 workload (GemmTiledKernel tile 32, BlocksParallel); "
+                                      f"{secs:.2f} s"}
+    parity["match"] = bool(parity["bitwise_vs_1gpu"] and parity.get("within_tolerance", True))
+    return cb, parity
 
 
 def cublas_dgemm(device: int, sizes) -> dict:
@@ -559,51 +741,69 @@ def cpu_threads():
     return len(os.sched_getaffinity(0))
 
 
-def _ref_axpy_f32(xs, ys, alpha, reps, warm=1):
+def _ref_axpy_f32(xs, ys, alpha, runs, on_run=None):
     """The reference's own runtime (oracle/_ref) running the AxpyKernel functor restated for
-    float on BlocksParallel with every host core; returns (median seconds, output, kind)."""
+    float on BlocksParallel with every host core, applied `runs` times in place (Y compounds,
+    as the GPU's does); on_run(i, read) may read Y after run i. Returns (seconds per run, kind)."""
     from oracle import oracle as O
     n = xs.size
+    times = []
     if O.ref_available():
         r = O.ref()
         os.environ.setdefault("KERNELWEAVE_POOL_SIZE", str(cpu_threads()))
         h = r.kwref_axpy_session_new(1, 1, n, float(alpha), xs.ctypes.data, ys.ctypes.data, 16, 4096)
         assert h, r.kwref_last_error()
         sec = C.c_double()
-        times = []
-        first = None
-        for i in range(warm + reps):
-            assert r.kwref_axpy_session_run(h, C.byref(sec)) == 0
-            if i == 0:
-                first = np.empty(n, np.float32)
-                r.kwref_axpy_session_read(h, first.ctypes.data)
-            if i >= warm:
+        try:
+            for i in range(runs):
+                assert r.kwref_axpy_session_run(h, C.byref(sec)) == 0
                 times.append(sec.value)
-        r.kwref_axpy_session_free(h)
-        return statistics.median(times), first, "reference"
+                if on_run:
+                    def read():
+                        out = np.empty(n, np.float32)
+                        r.kwref_axpy_session_read(h, out.ctypes.data)
+                        return out
+                    on_run(i, read)
+        finally:
+            r.kwref_axpy_session_free(h)
+        return times, "reference"
     out = ys.copy()
-    first = None
-    times = []
-    for i in range(warm + reps):
+    for i in range(runs):
         t = time.perf_counter()
         O.lib().kw_oracle_axpy_threaded(n, float(alpha), xs.ctypes.data, out.ctypes.data, 1, cpu_threads())
-        dt = time.perf_counter() - t
-        if i == 0:
-            first = out.copy()
-        if i >= warm:
-            times.append(dt)
-    return statistics.median(times), first, "port"
+        times.append(time.perf_counter() - t)
+        if on_run:
+            on_run(i, lambda: out.copy())
+    return times, "port"
 
 
-def cpu_baseline_axpy(xs, ys, alpha, y_gpu_first):
-    reps = 5
-    sec, first, kind = _ref_axpy_f32(xs, ys, alpha, reps)
-    value = BYTES_PER_ELEM * xs.size / sec / 1e9
+def cpu_baseline_axpy(alpha, gathered, applied, warm):
+    """Rank 0, every N: the reference CPU AXPY on the GLOBAL input, applied as many times as the
+    GPU applied it. Its Y after the first run and after the last is hashed over each rank's
+    [lo, hi) and compared with that rank's GPU digests (the reference verifies every measured
+    point, runner.cpp:120-125, 264-265); its per-run time is the CPU baseline."""
+    xs, ys = axpy_inputs(0, N_AXPY)
+    checks = {}
+
+    def on_run(i, read):
+        if i == 0 or i == applied - 1:
+            yr = read()
+            checks[i] = [digest(yr[lo:hi]) for (lo, hi, *_r) in gathered]
+
+    times, kind = _ref_axpy_f32(xs, ys, alpha, applied, on_run)
+    del xs, ys
+    timed = times[warm:] if len(times) > warm else times
+    sec = statistics.median(timed)
+    value = BYTES_PER_ELEM * N_AXPY / sec / 1e9
     cb = {"value": round(value, 2), "unit": "GB/s", "cores": cpu_threads(), "kind": kind,
-          "sample": f"full workload n=2^28 fp32, 1 warm-up + median of {reps} reps of enqueue+wait "
-                    f"(reference AxpyKernel functor (float) on the reference BlocksParallel engine, ept=4096)"}
-    parity = {"check": "GPU Y after one step == reference CPU Y (bitwise, 2^28 elements)",
-              "match": bool(y_gpu_first is not None and np.array_equal(first, y_gpu_first))}
+          "sample": f"full workload n=2^28 fp32, median of {len(timed)} enqueue+wait runs after {len(times) - len(timed)} "
+                    f"warm-up (reference AxpyKernel functor (float) on the reference BlocksParallel engine, ept=4096)"}
+    first_ok = checks.get(0) == [g[2] for g in gathered]
+    final_ok = checks.get(applied - 1) == [g[3] for g in gathered]
+    parity = {"check": (f"per-rank blake2b of GPU Y vs the reference CPU Y over the same index range, after the "
+                        f"first step and after all {applied} steps (parity + warm-up + timed; Y compounds)"),
+              "ranks": len(gathered), "first_step_match": bool(first_ok), "final_match": bool(final_ok),
+              "match": bool(first_ok and final_ok)}
     return cb, parity
 
 
@@ -650,19 +850,22 @@ def cpu_baseline_dgemm(a, b, c, alpha, beta, Cb, q, task, bw_task=None):
                 "bitwise_mode_match": bitwise}
 
 
-def run_reference(args, dist: Dist) -> dict | None:
+def run_reference(args, dist) -> dict | None:
+    """The reference arm: the reference's own CPU AXPY (oracle/_ref, BlocksParallel on every host
+    core) on the same global input, --warmup untimed + --steps timed enqueue+wait runs; rank 0
+    only. `config`, `metric`, `unit` and `steps` are the product arm's."""
     if dist.rank != 0:
         return None
-    rng = np.random.default_rng(1234)
-    xs = (rng.random(N_AXPY, dtype=np.float32) * 10).astype(np.float32)
-    ys = (rng.random(N_AXPY, dtype=np.float32) * 10).astype(np.float32)
+    xs, ys = axpy_inputs(0, N_AXPY)
     alpha = np.float32(9.096465)
-    steps = max(1, min(args.steps, args.ref_steps))
-    sec, _, kind = _ref_axpy_f32(xs, ys, alpha, steps, warm=max(1, min(args.warmup, 2)))
+    warm = max(1, args.warmup)
+    times, kind = _ref_axpy_f32(xs, ys, alpha, warm + args.steps)
+    del xs, ys
+    sec = statistics.median(times[warm:])
     value = BYTES_PER_ELEM * N_AXPY / sec / 1e9
     cb = {"value": round(value, 2), "unit": "GB/s", "cores": cpu_threads(), "kind": kind,
-          "sample": f"full workload n=2^28 fp32, median of {steps} reps (reference BlocksParallel engine, "
-                    f"AxpyKernel functor for float, ept=4096)"}
+          "sample": f"full workload n=2^28 fp32, median of {args.steps} runs after {warm} warm-up (reference "
+                    f"BlocksParallel engine, AxpyKernel functor for float, ept=4096)"}
     dg = None
     try:
         from oracle import oracle as O
@@ -681,10 +884,10 @@ def run_reference(args, dist: Dist) -> dict | None:
     except Exception as ex:  # noqa: BLE001
         dg = {"error": str(ex)[:200]}
     return {"impl": "reference", "metric": "AXPY fp32 HBM GB/s (n=2^28, Y=alpha*X+Y, 12 B/elem)",
-            "value": round(value, 2), "unit": "GB/s", "n_gpus": dist.world, "steps": steps,
+            "value": round(value, 2), "unit": "GB/s", "n_gpus": dist.world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "AXPY fp32 n=2^28 index-sharded (BASELINE.json configs[1])", "n": N_AXPY},
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": AXPY_DATA,
+            "config": axpy_config(dist.world, args.tpb, args.ept),
             "cpu_baseline": cb, "e2e": {"value": round(value, 2), "unit": "GB/s", "h2d_bytes_per_step": 0,
                                         "d2h_bytes_per_step": 0}, "dgemm": dg}
 
@@ -702,7 +905,6 @@ def main():
     ap.add_argument("--panels", type=int, default=8)
     ap.add_argument("--dgemm-timeout", type=float, default=300.0,
                     help="seconds the DGEMM leg may take before the headline line is printed without it")
-    ap.add_argument("--ref-steps", type=int, default=10)
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-dgemm", action="store_true")
     ap.add_argument("--no-f64", action="store_true")

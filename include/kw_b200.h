@@ -89,6 +89,9 @@ KW_EXPORT const char* kw_version(void);
 KW_EXPORT kw_status kw_device_count(int* n);
 KW_EXPORT kw_status kw_device_props_get(int device, kw_device_props* props);
 KW_EXPORT kw_status kw_device_synchronize(int device);
+/* PCI bus id ("0000:1b:00.0" form, lower case) of a device: host code uses it to place pinned
+ * staging buffers on the GPU's NUMA node (sysfs numa_node). */
+KW_EXPORT kw_status kw_device_pci_bus_id(int device, char* buf, int len);
 
 /* ---- buffers (replaces Buffer::Buffer / ~Buffer, core/src/buffer.cpp:25-46) --------------
  * device >= 0: device memory on that CUDA device; device == -1: page-locked host memory.
@@ -173,6 +176,10 @@ KW_EXPORT kw_status kw_axpy_f32(kw_queue q, const kw_workdiv* wd, size_t n, floa
                                 float* y);
 KW_EXPORT kw_status kw_axpy_f64(kw_queue q, const kw_workdiv* wd, size_t n, double alpha, const double* x,
                                 double* y);
+/* Name of the kernel template a device-resident kw_axpy_* launch with this division runs for
+ * these operand addresses (alignment decides the vector path; nothing is dereferenced). */
+KW_EXPORT kw_status kw_axpy_kernel_name(const kw_workdiv* wd, int elem_size, const void* x, const void* y,
+                                        char* buf, size_t len);
 
 /* ---- K2: tiled DGEMM  C = alpha*A*B + beta*C  (GemmTiledKernel, gemm.cpp:40-118) ----------
  * Row-major pitched fp64; lda/ldb/ldc in elements. FP64 DMMA tensor-core kernel fed by TMA and

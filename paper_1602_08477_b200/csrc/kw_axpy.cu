@@ -27,7 +27,9 @@
 
 #include <climits>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
+#include <string>
 
 namespace {
 
@@ -278,38 +280,59 @@ void launch_pdl(void (*kernel)(Params...), unsigned grid, unsigned threads, cuda
     cudaLaunchKernelEx(&cfg, kernel, static_cast<Params>(args)...);
 }
 
+// Which kernel template a device-resident launch runs (the one place that decides: the launcher
+// below and kw_axpy_kernel_name both call it, so the name bench.py reports is the launched one).
+enum class AxpyPath { V32x2, V32x1, Vec4, Vec2, Vec1, Scalar };
+
+template <typename T>
+AxpyPath select_path(uint32_t elems, const void* x, const void* y)
+{
+    constexpr int W = Vec<T>::W;
+    constexpr int W32 = V32<T>::W;
+    const bool aligned = (reinterpret_cast<uintptr_t>(x) % 16 == 0) && (reinterpret_cast<uintptr_t>(y) % 16 == 0);
+    const bool aligned32 = (reinterpret_cast<uintptr_t>(x) % 32 == 0) && (reinterpret_cast<uintptr_t>(y) % 32 == 0);
+    if (vector_bytes_policy() == 32 && aligned32 && elems % W32 == 0)
+        return elems / W32 >= 2 ? AxpyPath::V32x2 : AxpyPath::V32x1;
+    if (aligned && elems % W == 0) {
+        const uint32_t vpt = elems / W;
+        return vpt >= 4 ? AxpyPath::Vec4 : vpt >= 2 ? AxpyPath::Vec2 : AxpyPath::Vec1;
+    }
+    return AxpyPath::Scalar;
+}
+
+template <typename T>
+std::string path_name(AxpyPath p)
+{
+    const std::string t = sizeof(T) == 4 ? "float" : "double";
+    switch (p) {
+    case AxpyPath::V32x2: return "axpy_v32_kernel<" + t + ",2>";
+    case AxpyPath::V32x1: return "axpy_v32_kernel<" + t + ",1>";
+    case AxpyPath::Vec4: return "axpy_vec_kernel<" + t + ",4>";
+    case AxpyPath::Vec2: return "axpy_vec_kernel<" + t + ",2>";
+    case AxpyPath::Vec1: return "axpy_vec_kernel<" + t + ",1>";
+    default: return "axpy_scalar_kernel<" + t + ">";
+    }
+}
+
 template <typename T>
 void launch_device(cudaStream_t s, size_t blocks, uint32_t threads, uint32_t elems, size_t limit, T alpha,
                    const T* x, T* y)
 {
     constexpr int W = Vec<T>::W;
-    const bool aligned = (reinterpret_cast<uintptr_t>(x) % 16 == 0) && (reinterpret_cast<uintptr_t>(y) % 16 == 0);
+    constexpr int W32 = V32<T>::W;
     // Blocks entirely beyond `limit` have nothing to do: do not launch them.
     const size_t block_elems = static_cast<size_t>(threads) * elems;
     const size_t useful = kw::ceil_div(limit, block_elems);
     const unsigned grid = static_cast<unsigned>(useful < blocks ? useful : blocks);
     if (grid == 0)
         return;
-    constexpr int W32 = V32<T>::W;
-    const bool aligned32 = (reinterpret_cast<uintptr_t>(x) % 32 == 0) && (reinterpret_cast<uintptr_t>(y) % 32 == 0);
-    if (vector_bytes_policy() == 32 && aligned32 && elems % W32 == 0) {
-        const uint32_t vpt = elems / W32;
-        if (vpt >= 2)
-            launch_pdl(axpy_v32_kernel<T, 2>, grid, threads, s, limit, alpha, x, y, vpt);
-        else
-            launch_pdl(axpy_v32_kernel<T, 1>, grid, threads, s, limit, alpha, x, y, vpt);
-    }
-    else if (aligned && elems % W == 0) {
-        const uint32_t vpt = elems / W;
-        if (vpt >= 4)
-            launch_pdl(axpy_vec_kernel<T, 4>, grid, threads, s, limit, alpha, x, y, vpt);
-        else if (vpt >= 2)
-            launch_pdl(axpy_vec_kernel<T, 2>, grid, threads, s, limit, alpha, x, y, vpt);
-        else
-            launch_pdl(axpy_vec_kernel<T, 1>, grid, threads, s, limit, alpha, x, y, vpt);
-    }
-    else {
-        launch_pdl(axpy_scalar_kernel<T>, grid, threads, s, limit, alpha, x, y, elems);
+    switch (select_path<T>(elems, x, y)) {
+    case AxpyPath::V32x2: launch_pdl(axpy_v32_kernel<T, 2>, grid, threads, s, limit, alpha, x, y, elems / W32); break;
+    case AxpyPath::V32x1: launch_pdl(axpy_v32_kernel<T, 1>, grid, threads, s, limit, alpha, x, y, elems / W32); break;
+    case AxpyPath::Vec4: launch_pdl(axpy_vec_kernel<T, 4>, grid, threads, s, limit, alpha, x, y, elems / W); break;
+    case AxpyPath::Vec2: launch_pdl(axpy_vec_kernel<T, 2>, grid, threads, s, limit, alpha, x, y, elems / W); break;
+    case AxpyPath::Vec1: launch_pdl(axpy_vec_kernel<T, 1>, grid, threads, s, limit, alpha, x, y, elems / W); break;
+    default: launch_pdl(axpy_scalar_kernel<T>, grid, threads, s, limit, alpha, x, y, elems); break;
     }
     kw::g_launches.fetch_add(1, std::memory_order_relaxed);
 }
@@ -453,6 +476,22 @@ kw_status kw_axpy_f32(kw_queue q, const kw_workdiv* wd, size_t n, float alpha, c
 kw_status kw_axpy_f64(kw_queue q, const kw_workdiv* wd, size_t n, double alpha, const double* x, double* y)
 {
     return axpy_entry<double>(q, wd, n, alpha, x, y);
+}
+
+kw_status kw_axpy_kernel_name(const kw_workdiv* wd, int elem_size, const void* x, const void* y, char* buf,
+                              size_t len)
+{
+    if (!wd || !buf || len == 0)
+        return kw::usage("kw_axpy_kernel_name: null argument");
+    if (elem_size != 4 && elem_size != 8)
+        return kw::usage("kw_axpy_kernel_name: element size must be 4 or 8");
+    if (wd->dim != 1 || wd->elems[0] == 0 || wd->elems[0] > (1u << 30))
+        return kw::usage("kw_axpy_kernel_name: not a valid 1-D AXPY division");
+    const uint32_t elems = static_cast<uint32_t>(wd->elems[0]);
+    const std::string name = elem_size == 4 ? path_name<float>(select_path<float>(elems, x, y))
+                                            : path_name<double>(select_path<double>(elems, x, y));
+    std::snprintf(buf, len, "%s", name.c_str());
+    return KW_OK;
 }
 
 } // extern "C"

@@ -10,6 +10,8 @@
 
 #include <cstdint>
 
+#include <cctype>
+#include <cstdio>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -227,6 +229,30 @@ kw_status kw_device_props_get(int device, kw_device_props* props)
     props->sm_clock_khz = clk;
     props->mem_clock_khz = mclk;
     props->mem_bus_width_bits = bus;
+    return KW_OK;
+}
+
+kw_status kw_device_pci_bus_id(int device, char* buf, int len)
+{
+    if (!buf || len < 13)
+        return kw::usage("kw_device_pci_bus_id: buffer must hold at least 13 bytes");
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || device < 0 || device >= count) {
+        cudaGetLastError();
+        return kw::usage("kw_device_pci_bus_id: device index " + std::to_string(device) + " does not exist");
+    }
+    char id[64] = {};
+    cudaError_t e = cudaDeviceGetPCIBusId(id, sizeof(id), device);
+    if (e != cudaSuccess)
+        return kw::cuda_fail("cudaDeviceGetPCIBusId", e);
+    // CUDA reports "0000:1B:00.0" (possibly with an 8-digit domain); sysfs uses 4 lower-case digits.
+    std::string s(id);
+    const size_t colon = s.find(':');
+    if (colon != std::string::npos && colon > 4)
+        s = s.substr(colon - 4);
+    for (char& ch : s)
+        ch = static_cast<char>(std::tolower(static_cast<unsigned char>(ch)));
+    std::snprintf(buf, static_cast<size_t>(len), "%s", s.c_str());
     return KW_OK;
 }
 
