@@ -72,8 +72,12 @@ struct Queue {
     cudaEvent_t ev_order = nullptr;
     // Device-side failure slots of launches not yet resolved (guarded by mu), and the slot the
     // next kw_event_record attaches to its event.
+    // A slot joins pending_slots only once its kernel is in the stream (armed by
+    // kw_queue_end_launch / kw_queue_complete_launch): a drain that began before the launch
+    // must not resolve (and recycle) it.
     std::vector<std::shared_ptr<FailSlot>> pending_slots;
     std::shared_ptr<FailSlot> last_slot;
+    std::shared_ptr<FailSlot> staged; // kw_queue_begin_launch .. end_launch (enqueue lock held)
 };
 
 // RAII device selector: the reference's queues are bound to one device; every entry point
@@ -106,9 +110,15 @@ kw_status task_fail(Queue* q, const std::string& msg);
 // Sync queue, completes the task before returning (queue.cpp:21-23, 57-72).
 kw_status after_enqueue(Queue* q, const char* what);
 
-// Reads, counts (if `count_failures`) and recycles q's pending device-side failure slots; the
-// caller guarantees q->stream has drained.
-kw_status resolve_slots(Queue* q, bool count_failures);
+// Device-side failure slots are resolved in two steps around a drain of q->stream: take the
+// armed slots (their kernels are already in the stream) BEFORE synchronising, then read, count
+// (if `count_failures`) and recycle exactly those once the stream has drained.
+std::vector<std::shared_ptr<FailSlot>> take_slots(Queue* q);
+kw_status resolve_slots(Queue* q, std::vector<std::shared_ptr<FailSlot>>& slots, bool count_failures);
+
+// A fresh zeroed mapped slot (nullptr when pinned allocation fails) / its release.
+std::shared_ptr<FailSlot> make_slot(const std::string& what);
+void release_slot(FailSlot& fs);
 
 // Ensures q->scratch holds at least `bytes` of device memory on q's device.
 kw_status ensure_scratch(Queue* q, size_t bytes);

@@ -86,28 +86,59 @@ void slot_release(uint32_t* s)
 }
 } // namespace
 
-// Called once q->stream has drained: every pending device-side failure slot is read, counted
-// as a failed task if set, and recycled.
-kw_status resolve_slots(Queue* q, bool count_failures)
+std::shared_ptr<FailSlot> make_slot(const std::string& what)
 {
-    std::vector<std::shared_ptr<FailSlot>> done;
-    {
-        std::lock_guard<std::mutex> lock(q->mu);
-        done.swap(q->pending_slots);
+    auto fs = std::make_shared<FailSlot>();
+    fs->slot = slot_alloc();
+    if (!fs->slot)
+        return nullptr;
+    fs->what = what;
+    return fs;
+}
+
+void release_slot(FailSlot& fs)
+{
+    std::lock_guard<std::mutex> lock(fs.mu);
+    if (fs.slot) {
+        fs.code = *reinterpret_cast<volatile uint32_t*>(fs.slot);
+        slot_release(fs.slot);
+        fs.slot = nullptr;
     }
+}
+
+std::vector<std::shared_ptr<FailSlot>> take_slots(Queue* q)
+{
+    std::vector<std::shared_ptr<FailSlot>> out;
+    std::lock_guard<std::mutex> lock(q->mu);
+    out.swap(q->pending_slots);
+    return out;
+}
+
+namespace {
+// Failure codes the runtime itself writes from device code (kw_b200.h KW_FAIL_*).
+std::string failure_text(const FailSlot& fs, uint32_t code)
+{
+    switch (code) {
+    case KW_FAIL_SHARED_OVERFLOW:
+        return fs.what + ": allocSharedMem request exceeds the block's shared memory (the reference's UsageError, "
+                         "accel.cpp:286-292)";
+    case KW_FAIL_READY_TIMEOUT:
+        return fs.what + ": a streamed operand panel was never published (ready-flag wait timed out)";
+    default:
+        return fs.what + ": device functor reported failure (code " + std::to_string(code) + ")";
+    }
+}
+} // namespace
+
+kw_status resolve_slots(Queue* q, std::vector<std::shared_ptr<FailSlot>>& slots, bool count_failures)
+{
     kw_status st = KW_OK;
-    for (auto& fs : done) {
-        uint32_t code = 0;
-        {
-            std::lock_guard<std::mutex> lock(fs->mu);
-            code = *reinterpret_cast<volatile uint32_t*>(fs->slot);
-            fs->code = code;
-            slot_release(fs->slot);
-            fs->slot = nullptr;
-        }
-        if (code != 0 && count_failures)
-            st = task_fail(q, fs->what + ": device functor reported failure (code " + std::to_string(code) + ")");
+    for (auto& fs : slots) {
+        release_slot(*fs);
+        if (fs->code != 0 && count_failures)
+            st = task_fail(q, failure_text(*fs, fs->code));
     }
+    slots.clear();
     return st;
 }
 
@@ -117,10 +148,13 @@ kw_status after_enqueue(Queue* q, const char* what)
     if (e != cudaSuccess)
         return task_fail(q, std::string(what) + ": " + cudaGetErrorString(e));
     if (q->flavor == KW_QUEUE_SYNC) {
+        auto slots = take_slots(q);
         e = cudaStreamSynchronize(q->stream);
-        if (e != cudaSuccess)
+        if (e != cudaSuccess) {
+            resolve_slots(q, slots, false);
             return task_fail(q, std::string(what) + ": " + cudaGetErrorString(e));
-        return resolve_slots(q, true);
+        }
+        return resolve_slots(q, slots, true);
     }
     return KW_OK;
 }
@@ -428,7 +462,12 @@ kw_status kw_queue_destroy(kw_queue qh)
     for (cudaEvent_t e : q->ev_bp)
         if (e)
             cudaEventDestroy(e);
-    kw::resolve_slots(q, false);
+    {
+        auto slots = kw::take_slots(q);
+        if (q->staged)
+            kw::release_slot(*q->staged);
+        kw::resolve_slots(q, slots, false);
+    }
     if (q->ev_order)
         cudaEventDestroy(q->ev_order);
     if (q->order_host)
@@ -453,11 +492,14 @@ kw_status kw_queue_wait(kw_queue qh)
         return kw::usage("null queue");
     auto* q = reinterpret_cast<Queue*>(qh);
     kw::DeviceGuard g(q->device);
+    auto slots = kw::take_slots(q); // armed before this drain starts: complete once it returns
     cudaError_t e = cudaStreamSynchronize(q->stream);
-    if (e != cudaSuccess)
+    if (e != cudaSuccess) {
+        kw::resolve_slots(q, slots, false);
         kw::task_fail(q, std::string("stream: ") + cudaGetErrorString(e));
+    }
     else
-        kw::resolve_slots(q, true);
+        kw::resolve_slots(q, slots, true);
     std::lock_guard<std::mutex> lock(q->mu);
     if (q->failed == 0)
         return KW_OK;
@@ -521,19 +563,78 @@ kw_status kw_queue_shutdown(kw_queue qh)
     return KW_OK;
 }
 
+namespace {
+// Arms (or, after a failed launch, drops) the slot staged for the launch that just happened and
+// completes the enqueue like every other entry point.
+kw_status finish_launch(Queue* q, std::shared_ptr<kw::FailSlot> slot, int cuda_error, const char* what)
+{
+    const std::string w = what ? what : "kernel";
+    if (cuda_error != 0) {
+        if (slot)
+            kw::release_slot(*slot);
+        cudaGetLastError();
+        return kw::task_fail(q, w + ": " + cudaGetErrorString(static_cast<cudaError_t>(cuda_error)));
+    }
+    if (slot) {
+        std::lock_guard<std::mutex> lock(q->mu);
+        q->pending_slots.push_back(slot);
+        q->last_slot = std::move(slot);
+    }
+    kw::g_launches.fetch_add(1, std::memory_order_relaxed);
+    kw::DeviceGuard g(q->device);
+    return kw::after_enqueue(q, w.c_str());
+}
+
+// Slot of the legacy kw_queue_fail_slot / kw_queue_complete_launch pair, per calling thread.
+thread_local Queue* t_legacy_queue = nullptr;
+thread_local std::shared_ptr<kw::FailSlot> t_legacy_slot;
+} // namespace
+
+kw_status kw_queue_begin_launch(kw_queue qh, const char* what, void** stream, int* device, uint32_t** slot)
+{
+    if (!qh || !stream || !device || !slot)
+        return kw::usage("kw_queue_begin_launch: null argument");
+    auto* q = reinterpret_cast<Queue*>(qh);
+    q->enqueue.lock(); // held until kw_queue_end_launch: the launch is one FIFO enqueue
+    if (q->shut) {
+        q->enqueue.unlock();
+        return kw::usage("queue: enqueue after shutdown");
+    }
+    auto fs = kw::make_slot(what ? what : "kernel");
+    if (!fs) {
+        q->enqueue.unlock();
+        return kw::resource("kw_queue_begin_launch: mapped pinned allocation failed");
+    }
+    q->staged = fs;
+    *stream = q->stream;
+    *device = q->device;
+    *slot = fs->slot; // mapped + UVA: the host address is the device address
+    return KW_OK;
+}
+
+kw_status kw_queue_end_launch(kw_queue qh, int cuda_error, const char* what)
+{
+    if (!qh)
+        return kw::usage("null queue");
+    auto* q = reinterpret_cast<Queue*>(qh);
+    std::lock_guard<std::mutex> held(q->enqueue, std::adopt_lock);
+    auto fs = std::move(q->staged);
+    q->staged.reset();
+    return finish_launch(q, std::move(fs), cuda_error, what);
+}
+
 kw_status kw_queue_complete_launch(kw_queue qh, int cuda_error, const char* what)
 {
     if (!qh)
         return kw::usage("null queue");
     auto* q = reinterpret_cast<Queue*>(qh);
-    const std::string w = what ? what : "kernel";
-    if (cuda_error != 0) {
-        cudaGetLastError();
-        return kw::task_fail(q, w + ": " + cudaGetErrorString(static_cast<cudaError_t>(cuda_error)));
+    std::shared_ptr<kw::FailSlot> fs;
+    if (t_legacy_queue == q) {
+        fs = std::move(t_legacy_slot);
+        t_legacy_slot.reset();
+        t_legacy_queue = nullptr;
     }
-    kw::g_launches.fetch_add(1, std::memory_order_relaxed);
-    kw::DeviceGuard g(q->device);
-    return kw::after_enqueue(q, w.c_str());
+    return finish_launch(q, std::move(fs), cuda_error, what);
 }
 
 kw_status kw_queue_fail_slot(kw_queue qh, const char* what, uint32_t** slot)
@@ -541,17 +642,16 @@ kw_status kw_queue_fail_slot(kw_queue qh, const char* what, uint32_t** slot)
     if (!qh || !slot)
         return kw::usage("kw_queue_fail_slot: null argument");
     auto* q = reinterpret_cast<Queue*>(qh);
-    auto fs = std::make_shared<kw::FailSlot>();
-    fs->slot = kw::slot_alloc();
-    if (!fs->slot)
+    if (q->shut)
+        return kw::usage("queue: enqueue after shutdown");
+    auto fs = kw::make_slot(what ? what : "kernel");
+    if (!fs)
         return kw::resource("kw_queue_fail_slot: mapped pinned allocation failed");
-    fs->what = what ? what : "kernel";
-    {
-        std::lock_guard<std::mutex> lock(q->mu);
-        q->pending_slots.push_back(fs);
-        q->last_slot = fs;
-    }
-    *slot = fs->slot; // mapped + UVA: the host address is the device address
+    if (t_legacy_slot)
+        kw::release_slot(*t_legacy_slot); // staged but never launched
+    t_legacy_queue = q;
+    t_legacy_slot = fs;
+    *slot = fs->slot;
     return KW_OK;
 }
 
