@@ -78,6 +78,16 @@ inline BufferView view(const Buffer& b)
     return v;
 }
 
+/// Fails the running task with a non-zero code (any thread, any number of times; one code is
+/// kept). Device code cannot throw, so the functor returns after calling this — the reference's
+/// `throw` inside operator() (test_accel.cpp:403-430). Reported by Queue::wait() as TaskError and
+/// by the task's TaskHandle as TaskState::Failed; later tasks on the queue still run.
+__device__ inline void failTask(const AccContext& acc, unsigned code = 1)
+{
+    if (std::uint32_t* s = acc.failSlot())
+        *reinterpret_cast<volatile std::uint32_t*>(s) = code ? code : 1u;
+}
+
 /// Block-shared region of count*elemSize bytes; every thread of the block must issue the same
 /// allocation sequence (acc.hpp:75-84 contract), which makes this a collective: the region is
 /// zeroed cooperatively and published with a block barrier.
@@ -85,8 +95,15 @@ __device__ inline void* allocSharedMem(const AccContext& acc, std::size_t elemCo
 {
     const std::size_t bytes = elemCount * elemSize;
     const std::size_t off = (acc.sharedCursor() + 15) & ~static_cast<std::size_t>(15);
-    if (bytes == 0 || off + bytes > acc.sharedBytes())
-        __trap(); // UsageError / ResourceError in the reference
+    if (bytes == 0 || off + bytes > acc.sharedBytes()) {
+        // The reference throws UsageError out of operator() (accel.cpp:286-292): the task fails,
+        // the queue and later tasks live on. Here the allocation sequence is block-uniform, so
+        // every thread of the block takes this branch: record the failure and retire the block
+        // (the functor body never runs past the failed allocation). No trap — a trap would
+        // poison the CUDA context for every queue in the process.
+        failTask(acc, KW_FAIL_SHARED_OVERFLOW);
+        asm volatile("exit;");
+    }
     acc.sharedCursor() = off + bytes;
     std::byte* p = acc.sharedBase() + off;
     const unsigned nthreads = blockDim.x * blockDim.y * blockDim.z;
@@ -104,16 +121,6 @@ __device__ inline T* allocSharedMem(const AccContext& acc, std::size_t count)
 }
 
 __device__ inline void syncBlockThreads(const AccContext&) { __syncthreads(); }
-
-/// Fails the running task with a non-zero code (any thread, any number of times; one code is
-/// kept). Device code cannot throw, so the functor returns after calling this — the reference's
-/// `throw` inside operator() (test_accel.cpp:403-430). Reported by Queue::wait() as TaskError and
-/// by the task's TaskHandle as TaskState::Failed; later tasks on the queue still run.
-__device__ inline void failTask(const AccContext& acc, unsigned code = 1)
-{
-    if (std::uint32_t* s = acc.failSlot())
-        *reinterpret_cast<volatile std::uint32_t*>(s) = code ? code : 1u;
-}
 
 __device__ inline double atomicAdd(const AccContext&, double& cell, double operand)
 {
@@ -196,13 +203,10 @@ struct DeviceLauncher {
     {
         void* stream = nullptr;
         int dev = 0;
-        kw_status st = kw_queue_stream(q, &stream);
-        if (st == KW_OK)
-            st = kw_queue_device(q, &dev);
-        if (st != KW_OK)
-            return st;
         std::uint32_t* failSlot = nullptr;
-        st = kw_queue_fail_slot(q, "device functor", &failSlot);
+        // One enqueue: begin takes the queue's enqueue lock (FIFO against concurrent enqueues,
+        // rejects a shut-down queue); end arms the failure slot and releases the lock.
+        kw_status st = kw_queue_begin_launch(q, "device functor", &stream, &dev, &failSlot);
         if (st != KW_OK)
             return st;
         int prev = 0;
@@ -248,7 +252,7 @@ struct DeviceLauncher {
         functorKernel<Kernel, Args...><<<grid, block, smem, static_cast<cudaStream_t>(stream)>>>(w, smem, failSlot,
                                                                                                 kernel, args...);
         const int err = static_cast<int>(cudaGetLastError());
-        st = kw_queue_complete_launch(q, err, "device functor");
+        st = kw_queue_end_launch(q, err, "device functor");
         cudaSetDevice(prev);
         return st;
     }

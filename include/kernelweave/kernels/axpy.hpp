@@ -21,9 +21,76 @@ struct AxpyArgsT {
 using AxpyArgs = AxpyArgsT<double>;
 using AxpyArgsF32 = AxpyArgsT<float>;
 
-/// Element-extended AXPY functor (axpy.hpp:20-26). On GpuCudaRt each block covers the same
-/// elements as the reference block; the element level becomes 128-bit vectors per thread.
-struct AxpyKernel {};
+/// Device-usable form of AxpyArgsT: raw element pointers, captured by value by a functor
+/// (AxpyArgsT holds host-side Buffer objects, which device code cannot dereference).
+template <class T>
+struct AxpyArgsView {
+    std::size_t n = 0;
+    T alpha = T(0);
+    const T* x = nullptr;
+    T* y = nullptr;
+};
+
+template <class T>
+inline AxpyArgsView<T> toView(const AxpyArgsT<T>& a)
+{
+    if (!a.x || !a.y)
+        throw UsageError("AxpyArgs: null buffer");
+    return AxpyArgsView<T>{a.n, a.alpha, a.x->template rowData<T>(0), a.y->template rowData<T>(0)};
+}
+
+namespace detail_ops {
+/// fl(fl(a * x) + y): the product and the sum rounded separately, never contracted to an FMA
+/// (the reference's SSE mulpd/addpd).
+template <class T>
+KW_HD inline T mulThenAdd(T a, T x, T y)
+{
+#if defined(__CUDA_ARCH__)
+    if constexpr (sizeof(T) == 4)
+        return __fadd_rn(__fmul_rn(a, x), y);
+    else
+        return __dadd_rn(__dmul_rn(a, x), y);
+#else
+    volatile T p = a * x; // volatile: the host compiler may not fuse it into an FMA either
+    return p + y;
+#endif
+}
+} // namespace detail_ops
+
+/// Element-extended AXPY functor (axpy.hpp:20-26, axpy.cpp:10-23).
+///
+/// executeTask / createExec never call operator(): they dispatch to the tuned sm_100a kernel
+/// (kw_axpy_f32/_f64; each block covers the reference block's elements, the element level as
+/// 128-bit vectors). operator() is the reference's per-invocation body, for code that invokes
+/// or composes the functor itself:
+///   * device form (view args): grid thread g updates [g*V, g*V + min(V, n - g*V)) — call it
+///     from a KW_DEVICE_FUNCTOR functor; bit-exact against axpyReference;
+///   * reference signature (const AccContext&, const AxpyArgs&): the same body on HOST buffers,
+///     run where the call is made (one invocation, as the reference's runGrid calls it).
+struct AxpyKernel {
+    template <class T>
+    KW_HD void operator()(const AccContext& acc, const AxpyArgsView<T>& a) const
+    {
+        const std::size_t gridThreadIdx = idx::getIdx<Grid, Threads>(acc)[0];
+        const std::size_t threadElemExtent = workdiv::getWorkDiv<Thread, Elems>(acc)[0];
+        const std::size_t first = gridThreadIdx * threadElemExtent;
+        if (first >= a.n)
+            return;
+        const std::size_t elems = threadElemExtent < a.n - first ? threadElemExtent : a.n - first;
+        for (std::size_t i = first; i < first + elems; ++i)
+            a.y[i] = detail_ops::mulThenAdd(a.alpha, a.x[i], a.y[i]);
+    }
+    template <class T>
+    void operator()(const AccContext& acc, const AxpyArgsT<T>& a) const
+    {
+        const AxpyArgsView<T> v = toView(a);
+        if (!a.x->device().isHost() || !a.y->device().isHost())
+            throw UsageError("AxpyKernel: a direct call runs one invocation where it is made and needs host "
+                             "buffers; GPU buffers go through executeTask / createExec (or the view form inside a "
+                             "device functor)");
+        (*this)(acc, v);
+    }
+};
 
 /// axpy.cpp:25-30.
 inline WorkDiv axpyWorkDiv(BackendKind backend, std::size_t n, std::size_t threadsPerBlock,

@@ -120,10 +120,23 @@ KW_EXPORT kw_status kw_queue_flavor(kw_queue q, int* flavor);
 KW_EXPORT kw_status kw_queue_stream(kw_queue q, void** cuda_stream);
 KW_EXPORT kw_status kw_queue_shutdown(kw_queue q);
 
-/* Completes a kernel launch made OUTSIDE this library on q's stream (the header-only generic
- * functor launcher, include/kernelweave/cuda_exec.cuh): `cuda_error` is the launch's
- * cudaGetLastError() value. Records a failure for kw_queue_wait, counts the launch, and for a
- * Sync queue completes the task before returning. */
+/* A kernel launch made OUTSIDE this library on q's stream (the header-only generic functor
+ * launcher, include/kernelweave/cuda_exec.cuh) is one enqueue, bracketed by this pair:
+ *   kw_queue_begin_launch  takes q's enqueue lock (FIFO order against every other enqueue on q),
+ *                          rejects a shut-down queue (KW_USAGE, the reference's "enqueue on a
+ *                          shut-down queue"), and returns q's stream and device plus a zeroed
+ *                          device-side failure slot for the kernel (see kw_queue_fail_slot);
+ *   kw_queue_end_launch    `cuda_error` = the launch's cudaGetLastError() value. Arms the slot
+ *                          (only now can a drain of q resolve it), records a launch failure for
+ *                          kw_queue_wait, counts the launch, completes the task on a Sync queue,
+ *                          and releases the lock. Must follow every successful begin. */
+KW_EXPORT kw_status kw_queue_begin_launch(kw_queue q, const char* what, void** cuda_stream, int* device,
+                                          uint32_t** fail_slot);
+KW_EXPORT kw_status kw_queue_end_launch(kw_queue q, int cuda_error, const char* what);
+
+/* Legacy form of the pair above without the enqueue lock: kw_queue_fail_slot stages a slot for
+ * the calling thread's next launch on q; kw_queue_complete_launch arms it and completes the
+ * launch. Prefer begin/end (FIFO-safe against concurrent enqueues). */
 KW_EXPORT kw_status kw_queue_complete_launch(kw_queue q, int cuda_error, const char* what);
 
 /* Device-side task failure (the GPU form of "a kernel exception fails the task; later tasks
@@ -133,6 +146,9 @@ KW_EXPORT kw_status kw_queue_complete_launch(kw_queue q, int cuda_error, const c
  * a non-zero code counts as one failed task, reported as `what: ... (code N)`. The next
  * kw_event_record on q attaches the slot to its event, whose state is then FAILED. */
 KW_EXPORT kw_status kw_queue_fail_slot(kw_queue q, const char* what, uint32_t** slot);
+/* Failure codes the library's own device code writes into a slot (user codes stay below). */
+#define KW_FAIL_SHARED_OVERFLOW 0xFFFF0001u /* allocSharedMem beyond the block's shared memory */
+#define KW_FAIL_READY_TIMEOUT 0xFFFF0002u   /* streamed DGEMM: a panel ready flag never arrived */
 
 /* TaskHandle (queue.hpp:36-52) as a CUDA event recorded after the last enqueued task. State is
  * PENDING until the event completes, then DONE — or FAILED on a device fault or when the task's

@@ -53,6 +53,9 @@ SIGNATURES = {
     "kw_queue_stream": (st, [vp, C.POINTER(vp)]),
     "kw_queue_shutdown": (st, [vp]),
     "kw_queue_complete_launch": (st, [vp, C.c_int, C.c_char_p]),
+    "kw_queue_begin_launch": (st, [vp, C.c_char_p, C.POINTER(vp), C.POINTER(C.c_int),
+                                   C.POINTER(C.POINTER(C.c_uint32))]),
+    "kw_queue_end_launch": (st, [vp, C.c_int, C.c_char_p]),
     "kw_queue_fail_slot": (st, [vp, C.c_char_p, C.POINTER(C.POINTER(C.c_uint32))]),
     "kw_event_record": (st, [vp, C.POINTER(vp)]),
     "kw_task_marker": (st, [vp, C.POINTER(vp)]),

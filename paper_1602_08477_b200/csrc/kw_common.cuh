@@ -119,6 +119,8 @@ kw_status resolve_slots(Queue* q, std::vector<std::shared_ptr<FailSlot>>& slots,
 // A fresh zeroed mapped slot (nullptr when pinned allocation fails) / its release.
 std::shared_ptr<FailSlot> make_slot(const std::string& what);
 void release_slot(FailSlot& fs);
+// Makes a slot whose writer is already enqueued on q->stream pending (and the next event's slot).
+void arm_slot(Queue* q, std::shared_ptr<FailSlot> fs);
 
 // Ensures q->scratch holds at least `bytes` of device memory on q's device.
 kw_status ensure_scratch(Queue* q, size_t bytes);

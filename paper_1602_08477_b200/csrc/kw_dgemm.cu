@@ -350,16 +350,24 @@ __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* flag)
     return v;
 }
 
-// Streamed mode: waits until the copy stream has published a panel (ready flag != 0). Bounded:
-// a flag that never arrives traps (a device fault the queue reports) instead of hanging the GPU.
-__device__ __forceinline__ void wait_ready(const uint32_t* flag)
+// Streamed mode: waits until the copy stream has published a panel (ready flag != 0). Bounded,
+// and never a trap (a trap would poison the CUDA context for every queue in the process): a flag
+// that has not arrived after ~2^26 polls sets the launch's abort word (the launcher copies it
+// into the task's failure slot, so kw_queue_wait reports KW_FAIL_READY_TIMEOUT) and returns; once
+// the abort word is set every later wait returns at once, so the kernel drains quickly instead
+// of hanging the GPU, with the task already failed.
+__device__ __forceinline__ void wait_ready(const uint32_t* flag, uint32_t* abort)
 {
     uint32_t ns = 64;
     for (long long spins = 0;; ++spins) {
         if (ld_acquire_gpu(flag) != 0)
             return;
-        if (spins > (1ll << 26))
-            __trap();
+        if ((spins & 255) == 0 && *reinterpret_cast<volatile uint32_t*>(abort) != 0)
+            return;
+        if (spins > (1ll << 26)) {
+            atomicExch(abort, KW_FAIL_READY_TIMEOUT);
+            return;
+        }
         __nanosleep(ns);
         ns = ns < 2048 ? ns * 2 : ns;
     }
@@ -461,6 +469,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
             tma_prefetch_desc(&tmA);
             tma_prefetch_desc(&tmB);
             int it = 0; // k-tile iteration counter across this CTA's tiles (ring position)
+            // streamed: the abort word follows the done[] counters (GemmParams)
+            uint32_t* abort = nullptr;
+            if constexpr (STREAMED)
+                abort = p.ready + p.tile_list[0].y * (p.npr + p.npc) + 2 * p.npr * p.npc;
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
                 int bm, bn, kt0, kt1;
                 if (!origin(tile, bm, bn, kt0, kt1))
@@ -470,8 +482,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
                     // block is waited for before the last k-tile, below.)
                     const uint32_t* pass_flags =
                         p.ready + (p.tile_list[1 + tile].w >> 27) * (p.npr + p.npc);
-                    wait_ready(pass_flags + bm / p.panel_rows);
-                    wait_ready(pass_flags + p.npr + bn / p.panel_cols);
+                    wait_ready(pass_flags + bm / p.panel_rows, abort);
+                    wait_ready(pass_flags + p.npr + bn / p.panel_cols, abort);
                     // the panels were written by the copy engine; order the TMA reads after
                     asm volatile("fence.proxy.async.global;\n" ::: "memory");
                 }
@@ -486,7 +498,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
                         // the upload a whole tile of slack.
                         if (kt == ktiles - 1)
                             wait_ready(p.ready + p.tile_list[0].y * (p.npr + p.npc) +
-                                       (bm / p.panel_rows) * p.npc + bn / p.panel_cols);
+                                           (bm / p.panel_rows) * p.npc + bn / p.panel_cols,
+                                       abort);
                     }
                     mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
                     const uint32_t sa = smem_u32(smem + s * Cfg::STAGE_BYTES);
@@ -1422,6 +1435,24 @@ kw_status dgemm_device(cudaStream_t s, int tile, size_t m, size_t n, size_t k, d
 }
 } // namespace kw
 
+namespace {
+// The device-only entry points (bitwise, naive, with_config): every operand is device memory on
+// the queue's own device — a buffer of another GPU (no peer mapping) would fault the context.
+kw_status device_operands(const kw::Queue* q, const char* what, size_t k, const double* A, const double* B,
+                          const double* C)
+{
+    const double* ops[3] = {C, A, B};
+    for (int i = 0; i < (k > 0 ? 3 : 1); ++i) {
+        int d = -1;
+        if (kw::pointer_kind(ops[i], &d) != KW_MEM_DEVICE)
+            return kw::usage(std::string(what) + ": operands must be device buffers");
+        if (d != q->device)
+            return kw::usage(std::string(what) + ": buffer lives on a different device than the queue");
+    }
+    return KW_OK;
+}
+} // namespace
+
 extern "C" {
 
 kw_status kw_dgemm_default_workdiv(size_t m, size_t n, size_t tile, kw_workdiv* out)
@@ -1519,10 +1550,9 @@ kw_status kw_dgemm_bitwise(kw_queue qh, const kw_workdiv* wd, size_t m, size_t n
     if (m == 0 || n == 0)
         return KW_OK;
     kw::DeviceGuard g(q->device);
-    int d = -1;
-    if (kw::pointer_kind(C, &d) != KW_MEM_DEVICE || (k > 0 && (kw::pointer_kind(A, &d) != KW_MEM_DEVICE ||
-                                                               kw::pointer_kind(B, &d) != KW_MEM_DEVICE)))
-        return kw::usage("dgemm_bitwise: operands must be device buffers");
+    st = device_operands(q, "dgemm_bitwise", k, A, B, C);
+    if (st != KW_OK)
+        return st;
     st = launch_bitwise(q->stream, make_params(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc));
     if (st != KW_OK)
         return kw::task_fail(q, kw::last_error());
@@ -1555,10 +1585,9 @@ kw_status kw_dgemm_with_config(kw_queue qh, int cfg, size_t m, size_t n, size_t 
     if (st != KW_OK || m == 0 || n == 0)
         return st;
     kw::DeviceGuard g(q->device);
-    int d = -1;
-    if (kw::pointer_kind(C, &d) != KW_MEM_DEVICE || (k > 0 && (kw::pointer_kind(A, &d) != KW_MEM_DEVICE ||
-                                                               kw::pointer_kind(B, &d) != KW_MEM_DEVICE)))
-        return kw::usage("dgemm_with_config: operands must be device buffers");
+    st = device_operands(q, "dgemm_with_config", k, A, B, C);
+    if (st != KW_OK)
+        return st;
     st = kCfgs[cfg].launch(q->stream, make_params(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc));
     if (st != KW_OK)
         return kw::task_fail(q, kw::last_error());
@@ -1601,10 +1630,9 @@ kw_status kw_dgemm_naive(kw_queue qh, const kw_workdiv* wd, size_t m, size_t n, 
     if (m == 0 || n == 0)
         return KW_OK;
     kw::DeviceGuard g(q->device);
-    int d = -1;
-    if (kw::pointer_kind(C, &d) != KW_MEM_DEVICE || (k > 0 && (kw::pointer_kind(A, &d) != KW_MEM_DEVICE ||
-                                                               kw::pointer_kind(B, &d) != KW_MEM_DEVICE)))
-        return kw::usage("dgemm_naive: operands must be device buffers");
+    st = device_operands(q, "dgemm_naive", k, A, B, C);
+    if (st != KW_OK)
+        return st;
     dim3 grid(static_cast<unsigned>(wd->blocks[1]), static_cast<unsigned>(wd->blocks[0]));
     dim3 block(static_cast<unsigned>(wd->threads[1]), static_cast<unsigned>(wd->threads[0]));
     int er = static_cast<int>(wd->elems[0]), ec = static_cast<int>(wd->elems[1]);

@@ -132,8 +132,10 @@ kw_status dgemm_staged(kw::Queue* q, int tile, size_t m, size_t n, size_t k, dou
                 st = launch_tiled(q->stream, tile,
                                   make_params(rows, wj, k, alpha, Ad, ldad, Bd + n0, ldbd, beta, Cd + n0, ldcd));
                 if (st != KW_OK)
-                    return st;
+                    break;
             }
+            if (st != KW_OK)
+                break;
             if (trace)
                 cudaEventRecord(tev[1], q->h2d);
         }
@@ -146,7 +148,7 @@ kw_status dgemm_staged(kw::Queue* q, int tile, size_t m, size_t n, size_t k, dou
             }
             st = launch_tiled(comp, tile, make_params(rows, n, k, alpha, Ad, ldad, Bd, ldbd, beta, Cd, ldcd));
             if (st != KW_OK)
-                return st;
+                break;
         }
         e = cudaGetLastError();
         if (e == cudaSuccess && !c_dev) {
@@ -162,20 +164,34 @@ kw_status dgemm_staged(kw::Queue* q, int tile, size_t m, size_t n, size_t k, dou
             e = cudaEventRecord(q->ev_free[s], comp);
         }
     }
-    if (trace && e == cudaSuccess) {
+    // A launch that failed part-way still joins what was already enqueued (earlier panels' D2H on
+    // the aux stream, the second compute stream) into q->stream before the failure is recorded,
+    // so later tasks on the queue cannot overlap it.
+    const std::string launch_error = st != KW_OK ? kw::last_error() : std::string();
+    const cudaError_t loop_error = e;
+    e = cudaSuccess;
+    if (trace && loop_error == cudaSuccess && st == KW_OK) {
         cudaEventRecord(tev[2], q->h2d);
         cudaEventRecord(tev[3], (npanels & 1) ? q->stream : q->comp2); // stream of the last panel
         cudaEventRecord(tev[4], q->aux);
     }
-    if (e == cudaSuccess) {
-        e = cudaEventRecord(q->ev_join, q->aux);
+    e = cudaEventRecord(q->ev_join, q->aux);
+    if (e == cudaSuccess)
+        e = cudaStreamWaitEvent(q->stream, q->ev_join, 0);
+    if (e == cudaSuccess)
+        e = cudaEventRecord(q->ev_join2, q->comp2);
+    if (e == cudaSuccess)
+        e = cudaStreamWaitEvent(q->stream, q->ev_join2, 0);
+    if ((st != KW_OK || loop_error != cudaSuccess) && e == cudaSuccess) {
+        // an upload may have been enqueued for a panel that never launched: join it too
+        e = cudaEventRecord(q->ev_join, q->h2d);
         if (e == cudaSuccess)
             e = cudaStreamWaitEvent(q->stream, q->ev_join, 0);
-        if (e == cudaSuccess)
-            e = cudaEventRecord(q->ev_join2, q->comp2);
-        if (e == cudaSuccess)
-            e = cudaStreamWaitEvent(q->stream, q->ev_join2, 0);
     }
+    if (st != KW_OK)
+        return kw::task_fail(q, "dgemm (host-staged): " + launch_error);
+    if (e == cudaSuccess)
+        e = loop_error;
     if (trace && e == cudaSuccess) {
         cudaEventSynchronize(tev[4]);
         cudaStreamSynchronize(q->stream);
@@ -308,7 +324,7 @@ kw_status dgemm_streamed(kw::Queue* q, int tile, size_t m, size_t n, size_t k, d
     const size_t nflags = npass * (npr + npc) + npr * npc, ndone = npr * npc;
     const size_t mat_bytes = (m * ldas + k * ldbs + m * ldcs) * sizeof(double);
     const size_t part_bytes = passes > 1 ? tiles * bm * bn * sizeof(double) : 0;
-    const size_t aux_bytes = (nflags + ndone) * sizeof(uint32_t) + 512;
+    const size_t aux_bytes = (nflags + ndone + 1) * sizeof(uint32_t) + 512; // + the abort word
     if (q->scratch_bytes < mat_bytes + part_bytes + aux_bytes) {
         // growing the scratch: only when the operands fit comfortably (a resource-manager query,
         // so not on every call)
@@ -398,7 +414,8 @@ kw_status dgemm_streamed(kw::Queue* q, int tile, size_t m, size_t n, size_t k, d
     const size_t key[8] = {m, n, R, W, static_cast<size_t>(cfg), npass, bhash, grid};
     const bool order_current = std::equal(key, key + 8, q->order_key);
     auto flag = [&](size_t idx) { return reinterpret_cast<CUdeviceptr>(ready + idx); };
-    cudaError_t e = cudaMemsetAsync(ready, 0, (nflags + ndone) * sizeof(uint32_t), q->stream);
+    uint32_t* abort_word = done + ndone;
+    cudaError_t e = cudaMemsetAsync(ready, 0, (nflags + ndone + 1) * sizeof(uint32_t), q->stream);
     if (e == cudaSuccess && !order_current) {
         if (q->ev_order)
             e = cudaEventSynchronize(q->ev_order); // the previous upload still reads order_host
@@ -531,6 +548,15 @@ kw_status dgemm_streamed(kw::Queue* q, int tile, size_t m, size_t n, size_t k, d
     if (st != KW_OK)
         return kw::task_fail(q, kw::last_error());
     e = cudaGetLastError();
+    // The kernel's abort word -> this task's failure slot (resolved by kw_queue_wait).
+    if (auto fs = kw::make_slot("dgemm (streamed)")) {
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(fs->slot, abort_word, sizeof(uint32_t), cudaMemcpyDeviceToHost, q->stream);
+        if (e == cudaSuccess)
+            kw::arm_slot(q, std::move(fs));
+        else
+            kw::release_slot(*fs);
+    }
     if (trace)
         cudaEventRecord(tev[2], q->stream);
 

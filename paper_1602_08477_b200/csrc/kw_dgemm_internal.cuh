@@ -25,7 +25,8 @@ struct GemmParams {
     // Streamed mode (host-resident operands, dgemm_streamed): the copy stream uploads A in row
     // panels, B in column panels and C in blocks, and publishes each with a stream write of
     // ready[] = 1: [pass 0: npr A | npc B] ... [pass P-1: npr A | npc B][npr*npc C blocks],
-    // followed by the done[npr*npc] counters. The persistent kernel walks tile_list
+    // followed by the done[npr*npc] counters and one abort word (a ready-flag wait that timed
+    // out writes KW_FAIL_READY_TIMEOUT there). The persistent kernel walks tile_list
     // (tile_list[0] = {entry count, P}, then entries {tile row, tile col, first k-tile, end
     // k-tile | pass << 27}; tile row < 0 = padding) in availability order and waits for a tile's
     // panels of the entry's pass before loading them. A tile runs as P entries over consecutive

@@ -106,6 +106,13 @@ void release_slot(FailSlot& fs)
     }
 }
 
+void arm_slot(Queue* q, std::shared_ptr<FailSlot> fs)
+{
+    std::lock_guard<std::mutex> lock(q->mu);
+    q->pending_slots.push_back(fs);
+    q->last_slot = std::move(fs);
+}
+
 std::vector<std::shared_ptr<FailSlot>> take_slots(Queue* q)
 {
     std::vector<std::shared_ptr<FailSlot>> out;
@@ -575,11 +582,8 @@ kw_status finish_launch(Queue* q, std::shared_ptr<kw::FailSlot> slot, int cuda_e
         cudaGetLastError();
         return kw::task_fail(q, w + ": " + cudaGetErrorString(static_cast<cudaError_t>(cuda_error)));
     }
-    if (slot) {
-        std::lock_guard<std::mutex> lock(q->mu);
-        q->pending_slots.push_back(slot);
-        q->last_slot = std::move(slot);
-    }
+    if (slot)
+        kw::arm_slot(q, std::move(slot));
     kw::g_launches.fetch_add(1, std::memory_order_relaxed);
     kw::DeviceGuard g(q->device);
     return kw::after_enqueue(q, w.c_str());

@@ -378,3 +378,54 @@ int main()
     }
     return kwcheck::run();
 }
+
+// The functors' reference-signature operator() (axpy.hpp:23-25, gemm.hpp:33, :47), invoked
+// directly the way the reference's runGrid does — one call per (block, thread) of a division —
+// on host buffers, against the sequential oracles; and device buffers are refused.
+TEST_CASE("functor operator()(acc, args): direct invocation over a division equals the oracle")
+{
+    std::mt19937_64 rng(4242);
+    const std::size_t n = 1003;
+    Buffer x(kHost, IndexVec(n), 8), y(kHost, IndexVec(n), 8);
+    fillUniform<double>(x, rng, 0.0, 10.0);
+    fillUniform<double>(y, rng, 0.0, 10.0);
+    std::vector<double> want(y.rowData<double>(0), y.rowData<double>(0) + n);
+    axpyRef<double>(n, 3.25, x.rowData<double>(0), want.data());
+    const WorkDiv wd = axpyWorkDiv(BackendKind::ThreadsParallel, n, 16, 8);
+    const AxpyArgs args{n, 3.25, &x, &y};
+    for (std::size_t b = 0; b < wd.blocksPerGrid()[0]; ++b)
+        for (std::size_t t = 0; t < wd.threadsPerBlock()[0]; ++t)
+            AxpyKernel{}(AccContext(wd, IndexVec(b), IndexVec(t)), args);
+    CHECK(std::memcmp(want.data(), y.rowData<double>(0), n * 8) == 0);
+
+    const std::size_t m = 37, nn = 29, k = 41;
+    Buffer a(kHost, IndexVec(m, k), 8), bb(kHost, IndexVec(k, nn), 8), c(kHost, IndexVec(m, nn), 8);
+    fillUniform<double>(a, rng, 0.0, 10.0);
+    fillUniform<double>(bb, rng, 0.0, 10.0);
+    fillUniform<double>(c, rng, 0.0, 10.0);
+    std::vector<double> da(m * k), db(k * nn), dc(m * nn);
+    for (std::size_t r = 0; r < m; ++r)
+        std::memcpy(da.data() + r * k, a.rowData<double>(r), k * 8);
+    for (std::size_t r = 0; r < k; ++r)
+        std::memcpy(db.data() + r * nn, bb.rowData<double>(r), nn * 8);
+    for (std::size_t r = 0; r < m; ++r)
+        std::memcpy(dc.data() + r * nn, c.rowData<double>(r), nn * 8);
+    gemmRef(m, nn, k, 1.5, 0.25, da.data(), db.data(), dc.data());
+    const WorkDiv nwd = gemmNaiveWorkDiv(BackendKind::ThreadsParallel, m, nn, 4, 3);
+    const GemmArgs g{m, nn, k, 1.5, 0.25, &a, &bb, &c};
+    const IndexVec blocks = nwd.blocksPerGrid(), threads = nwd.threadsPerBlock();
+    for (std::size_t b0 = 0; b0 < blocks[0]; ++b0)
+        for (std::size_t b1 = 0; b1 < blocks[1]; ++b1)
+            for (std::size_t t0 = 0; t0 < threads[0]; ++t0)
+                for (std::size_t t1 = 0; t1 < threads[1]; ++t1)
+                    GemmNaiveKernel{}(AccContext(nwd, IndexVec(b0, b1), IndexVec(t0, t1)), g);
+    bool same = true;
+    for (std::size_t r = 0; r < m; ++r)
+        same = same && std::memcmp(dc.data() + r * nn, c.rowData<double>(r), nn * 8) == 0;
+    CHECK(same);
+    // block-cooperative tiled body: device functors only
+    CHECK_THROWS_AS(GemmTiledKernel{}(AccContext(nwd, IndexVec(0, 0), IndexVec(0, 0)), g), UsageError);
+    // GPU buffers go through executeTask / createExec
+    Buffer gx(kGpu, IndexVec(n), 8), gy(kGpu, IndexVec(n), 8);
+    CHECK_THROWS_AS(AxpyKernel{}(AccContext(wd, IndexVec(0), IndexVec(0)), AxpyArgs{n, 1.0, &gx, &gy}), UsageError);
+}

@@ -7,6 +7,9 @@
 #include "check.hpp"
 
 #include <algorithm>
+#include <array>
+#include <atomic>
+#include <thread>
 #include <cmath>
 #include <chrono>
 #include <cstring>
@@ -117,6 +120,20 @@ struct TooMuchSharedKernel {
     __device__ void operator()(const AccContext&, BufferView) const {}
 };
 KW_DEVICE_FUNCTOR(TooMuchSharedKernel)
+
+// allocSharedMem past the block's declared arena: the reference throws UsageError out of
+// operator() (accel.cpp:286-292); here the block retires and the task fails (no trap).
+struct SharedOverflowKernel {
+    static constexpr std::size_t sharedMemBytes = 1024;
+    __device__ void operator()(const AccContext& acc, BufferView out) const
+    {
+        double* a = allocSharedMem<double>(acc, 64);  // 512 B: fits
+        double* b = allocSharedMem<double>(acc, 128); // 1 KiB more: past the 1 KiB arena
+        a[0] = b[0] = 1.0;                            // never reached
+        atomicAdd(acc, out.rowData<std::uint64_t>(0)[0], std::uint64_t{1});
+    }
+};
+KW_DEVICE_FUNCTOR(SharedOverflowKernel)
 
 // test_accel.cpp:403-430: the functor "throws" in block 3 — on the GPU, failTask + return.
 struct FailKernel {
@@ -353,6 +370,161 @@ TEST_CASE("failed tasks are collected, later tasks still run, wait() reports Tas
         ok = ok && v == 1; // the task between the failures ran
     CHECK(ok);
     q.wait(); // failures were reported once; the queue is clean again
+}
+
+TEST_CASE("allocSharedMem overflow fails the task, not the context; later tasks run (accel.cpp:286-292)")
+{
+    Buffer out = upload(std::vector<std::uint64_t>(64, 0));
+    Queue q(kGpu, QueueFlavor::Async);
+    TaskHandle bad = q.enqueue(createExec(kBk, WorkDiv(IndexVec(8), IndexVec(32), IndexVec(1)),
+                                          SharedOverflowKernel{}, view(out)));
+    TaskHandle good = q.enqueue(createExec(kBk, WorkDiv(IndexVec(1), IndexVec(64), IndexVec(1)), MarkKernel{},
+                                           view(out)));
+    std::string msg;
+    std::size_t failed = 0;
+    try {
+        q.wait();
+    }
+    catch (const TaskError& e) {
+        failed = e.failedCount();
+        msg = e.what();
+    }
+    CHECK(failed == 1);
+    CHECK(msg.find("allocSharedMem") != std::string::npos);
+    CHECK(bad.state() == TaskState::Failed);
+    CHECK(good.state() == TaskState::Done);
+    const auto got = download<std::uint64_t>(out, 64);
+    bool ok = got[0] == 1; // slot 0: MarkKernel's 1, never the overflow kernel's atomicAdd
+    for (std::size_t i = 1; i < 64; ++i)
+        ok = ok && got[i] == 1;
+    CHECK(ok);
+    // the context is healthy: a fresh synchronous task runs
+    executeTask(kBk, WorkDiv(IndexVec(1), IndexVec(64), IndexVec(1)), MarkKernel{}, view(out));
+    CHECK(download<std::uint64_t>(out, 64)[5] == 2);
+}
+
+TEST_CASE("a generic functor enqueue on a shut-down queue is a UsageError (queue.cpp enqueueBody)")
+{
+    Buffer out = upload(std::vector<std::uint64_t>(64, 0));
+    Queue q(kGpu, QueueFlavor::Async);
+    q.shutdown();
+    CHECK_THROWS_AS(q.enqueue(createExec(kBk, WorkDiv(IndexVec(1), IndexVec(64), IndexVec(1)), MarkKernel{},
+                                         view(out))),
+                    UsageError);
+    CHECK(download<std::uint64_t>(out, 64)[0] == 0);
+}
+
+TEST_CASE("concurrent enqueue and wait: every device-side failure is counted exactly once (queue.hpp:86-93)")
+{
+    // Thread A enqueues failing functors while thread B drains the queue in a loop. A failure
+    // slot may only be resolved by a drain that started after its kernel was in the stream;
+    // a slot resolved early would be recycled unread and its failure lost.
+    Queue q(kGpu, QueueFlavor::Async);
+    constexpr int kTasks = 400;
+    std::atomic<bool> done{false};
+    std::atomic<std::size_t> seen{0};
+    std::thread waiter([&] {
+        while (!done.load()) {
+            try {
+                q.wait();
+            }
+            catch (const TaskError& e) {
+                seen += e.failedCount();
+            }
+        }
+    });
+    for (int i = 0; i < kTasks; ++i)
+        q.enqueue(createExec(kBk, WorkDiv(IndexVec(8), IndexVec(32), IndexVec(1)), FailKernel{}, 1u + i % 7));
+    done = true;
+    waiter.join();
+    try {
+        q.wait();
+    }
+    catch (const TaskError& e) {
+        seen += e.failedCount();
+    }
+    std::printf("  %d failing tasks, %zu failures reported\n", kTasks, seen.load());
+    CHECK(seen.load() == kTasks);
+}
+
+// The shipped functors' operator() composed inside user device functors (verdict r1: "code
+// that invokes or composes the functor directly"): bitwise equal to the library's own launches.
+struct ComposedAxpy {
+    __device__ void operator()(const AccContext& acc, kernels::AxpyArgsView<float> a) const
+    {
+        kernels::AxpyKernel{}(acc, a);
+    }
+};
+KW_DEVICE_FUNCTOR(ComposedAxpy)
+struct ComposedNaive {
+    __device__ void operator()(const AccContext& acc, kernels::GemmArgsView g) const { kernels::GemmNaiveKernel{}(acc, g); }
+};
+KW_DEVICE_FUNCTOR(ComposedNaive)
+struct ComposedTiled {
+    static constexpr std::size_t sharedMemBytes = 3 * 16 * 16 * sizeof(double);
+    __device__ void operator()(const AccContext& acc, kernels::GemmArgsView g) const { kernels::GemmTiledKernel{}(acc, g); }
+};
+KW_DEVICE_FUNCTOR(ComposedTiled)
+
+TEST_CASE("AxpyKernel / GemmNaiveKernel / GemmTiledKernel operator() compose in device functors, bit-exact")
+{
+    std::mt19937_64 rng(77);
+    const std::size_t n = 1000003;
+    std::vector<float> xv(n), yv(n);
+    for (std::size_t i = 0; i < n; ++i) {
+        xv[i] = static_cast<float>((rng() >> 11) * 0x1.0p-53 * 10.0);
+        yv[i] = static_cast<float>((rng() >> 11) * 0x1.0p-53 * 10.0);
+    }
+    Buffer x = upload(xv), y1 = upload(yv), y2 = upload(yv);
+    executeTask(kBk, kernels::axpyWorkDiv(kBk, n, 256, 8), kernels::AxpyKernel{},
+                kernels::AxpyArgsF32{n, 2.75f, &x, &y1});
+    executeTask(kBk, kernels::axpyWorkDiv(kBk, n, 256, 8), ComposedAxpy{},
+                kernels::toView(kernels::AxpyArgsF32{n, 2.75f, &x, &y2}));
+    const auto a1 = download<float>(y1, n), a2 = download<float>(y2, n);
+    CHECK(std::memcmp(a1.data(), a2.data(), n * 4) == 0);
+
+    for (auto [m, nn, k] : {std::array<std::size_t, 3>{1, 1, 1}, {37, 29, 41}, {130, 67, 200}, {64, 64, 64}}) {
+        auto mat = [&](std::size_t r, std::size_t c) {
+            std::vector<double> v(r * c);
+            for (auto& e : v)
+                e = (rng() >> 11) * 0x1.0p-53 * 10.0;
+            Buffer h(Device::host(), IndexVec(r, c), 8);
+            for (std::size_t i = 0; i < r; ++i)
+                std::memcpy(h.rowData<double>(i), v.data() + i * c, c * 8);
+            Buffer d(kGpu, IndexVec(r, c), 8);
+            Queue q(kGpu, QueueFlavor::Sync);
+            copyBuffer(q, d, h, h.extent());
+            return d;
+        };
+        Buffer A = mat(m, k), B = mat(k, nn), C0 = mat(m, nn);
+        auto fresh = [&] {
+            Buffer c(kGpu, IndexVec(m, nn), 8);
+            Queue q(kGpu, QueueFlavor::Sync);
+            copyBuffer(q, c, C0, C0.extent());
+            return c;
+        };
+        auto rows = [&](const Buffer& c) {
+            Buffer h(Device::host(), c.extent(), 8);
+            Queue q(kGpu, QueueFlavor::Sync);
+            copyBuffer(q, h, c, c.extent());
+            std::vector<double> out(m * nn);
+            for (std::size_t i = 0; i < m; ++i)
+                std::memcpy(out.data() + i * nn, h.rowData<double>(i), nn * 8);
+            return out;
+        };
+        Buffer cRef = fresh(), cNaive = fresh(), cTiled = fresh();
+        const kernels::GemmArgs ref{m, nn, k, 1.25, 0.5, &A, &B, &cRef};
+        executeTask(kBk, kernels::gemmNaiveWorkDiv(kBk, m, nn, 4, 4), kernels::GemmNaiveKernel{}, ref);
+        executeTask(kBk, kernels::gemmNaiveWorkDiv(BackendKind::ThreadsParallel, m, nn, 8, 3), ComposedNaive{},
+                    kernels::toView(kernels::GemmArgs{m, nn, k, 1.25, 0.5, &A, &B, &cNaive}));
+        kernels::GemmArgs tg{m, nn, k, 1.25, 0.5, &A, &B, &cTiled};
+        tg.tile = 16;
+        executeTask(kBk, kernels::gemmTiledWorkDiv(BackendKind::ThreadsParallel, m, nn, 16), ComposedTiled{},
+                    kernels::toView(tg));
+        const auto want = rows(cRef);
+        CHECK(want == rows(cNaive));
+        CHECK(std::memcmp(want.data(), rows(cTiled).data(), want.size() * 8) == 0);
+    }
 }
 
 TEST_CASE("invocation coverage: every (block, thread) exactly once (acceptance crit. 2)")

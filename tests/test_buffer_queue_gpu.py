@@ -306,6 +306,33 @@ def test_failures_aggregate_and_later_tasks_still_run(gpu):
         sync.wait()
 
 
+def test_begin_end_launch_bracket(gpu):
+    """The external-launch bracket the generic functor launcher uses: begin holds the enqueue
+    lock and rejects a shut-down queue (queue.cpp enqueueBody's UsageError); end with a launch
+    error records one failed task; a clean end arms a zeroed slot that nothing sets."""
+    import ctypes as C
+    lib = L.lib()
+    q = kw.Queue(gpu, kw.QueueFlavor.Async)
+    stream, dev, slot = C.c_void_p(), C.c_int(-1), C.POINTER(C.c_uint32)()
+    assert lib.kw_queue_begin_launch(q.handle(), b"ext", C.byref(stream), C.byref(dev), C.byref(slot)) == 0
+    assert dev.value == 0 and stream.value and slot[0] == 0
+    assert lib.kw_queue_end_launch(q.handle(), 0, b"ext") == 0
+    q.wait()
+    assert lib.kw_queue_begin_launch(q.handle(), b"ext", C.byref(stream), C.byref(dev), C.byref(slot)) == 0
+    assert lib.kw_queue_end_launch(q.handle(), 1, b"ext launch") == L.KW_TASK
+    with pytest.raises(kw.TaskError) as ei:
+        q.wait()
+    assert "ext launch" in str(ei.value)
+    # the lock was released: an ordinary enqueue still goes through
+    x, y = dev_vec(gpu, [1.0]), dev_vec(gpu, [0.0])
+    q.enqueue(axpy_task(1, 2.0, x, y))
+    q.wait()
+    assert y.download()[0] == 2.0
+    q.shutdown()
+    assert lib.kw_queue_begin_launch(q.handle(), b"ext", C.byref(stream), C.byref(dev), C.byref(slot)) == L.KW_USAGE
+    assert lib.kw_queue_fail_slot(q.handle(), b"ext", C.byref(slot)) == L.KW_USAGE
+
+
 def test_sync_queue_shutdown_rejects_enqueue(gpu):
     """test_queue.cpp:187-202, Sync half (the Async half is test_axpy_gpu)."""
     q = kw.Queue(gpu, kw.QueueFlavor.Sync)
