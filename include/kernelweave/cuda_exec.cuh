@@ -148,6 +148,23 @@ struct SharedBytesOf<Kernel, std::void_t<decltype(Kernel::sharedMemBytes)>> {
     static constexpr std::size_t value = Kernel::sharedMemBytes;
 };
 
+/// Logical blocks of a division, and logical block `lb` (row-major, last component fastest —
+/// delinearize of index_vec.hpp) as the device computes it for every functor launch. Scalar,
+/// array-free. Pinned exhaustively on the device by acceptance criterion 03's extent set
+/// (tests/cpp/test_functor_gpu.cu).
+KW_HD inline std::size_t logicalBlockCount(const kw_workdiv& wd) noexcept
+{
+    const unsigned d = wd.dim;
+    return wd.blocks[d - 1] * (d >= 2 ? wd.blocks[d - 2] : 1) * (d == 3 ? wd.blocks[0] : 1);
+}
+KW_HD inline IndexVec logicalBlockIdx(const kw_workdiv& wd, std::size_t lb) noexcept
+{
+    const unsigned d = wd.dim;
+    const std::size_t bLast = wd.blocks[d - 1], bMid = d >= 2 ? wd.blocks[d - 2] : 1;
+    const std::size_t c = lb % bLast, r = lb / bLast;
+    return d == 1 ? IndexVec(c) : d == 2 ? IndexVec(r, c) : IndexVec(r / bMid, r % bMid, c);
+}
+
 template <class Kernel, class... Args>
 __global__ void functorKernel(kw_workdiv wd, std::size_t sharedBytes, std::uint32_t* failSlot, Kernel kernel,
                               Args... args)
@@ -162,12 +179,9 @@ __global__ void functorKernel(kw_workdiv wd, std::size_t sharedBytes, std::uint3
     const IndexVec tIdx = d == 1 ? IndexVec(threadIdx.x)
                           : d == 2 ? IndexVec(threadIdx.y, threadIdx.x)
                                    : IndexVec(threadIdx.z, threadIdx.y, threadIdx.x);
-    const std::size_t bLast = wd.blocks[d - 1], bMid = d >= 2 ? wd.blocks[d - 2] : 1;
-    const std::size_t nb = bLast * bMid * (d == 3 ? wd.blocks[0] : 1);
+    const std::size_t nb = logicalBlockCount(wd);
     for (std::size_t lb = blockIdx.x; lb < nb; lb += gridDim.x) {
-        const std::size_t c = lb % bLast, r = lb / bLast;
-        const IndexVec bIdx = d == 1 ? IndexVec(c) : d == 2 ? IndexVec(r, c) : IndexVec(r / bMid, r % bMid, c);
-        const AccContext acc(wd, bIdx, tIdx, kwSharedArena, sharedBytes, failSlot);
+        const AccContext acc(wd, logicalBlockIdx(wd, lb), tIdx, kwSharedArena, sharedBytes, failSlot);
         kernel(acc, args...);
         if (lb + gridDim.x < nb)
             __syncthreads(); // the next logical block reuses the shared arena

@@ -71,8 +71,9 @@ struct AxpyKernel {
     template <class T>
     KW_HD void operator()(const AccContext& acc, const AxpyArgsView<T>& a) const
     {
-        const std::size_t gridThreadIdx = idx::getIdx<Grid, Threads>(acc)[0];
-        const std::size_t threadElemExtent = workdiv::getWorkDiv<Thread, Elems>(acc)[0];
+        // the paper's spelling: idx::getIdx<Grid, Threads>(acc)[0u]
+        const std::size_t gridThreadIdx = idx::getIdx<Grid, Threads>(acc)[0u];
+        const std::size_t threadElemExtent = workdiv::getWorkDiv<Thread, Elems>(acc)[0u];
         const std::size_t first = gridThreadIdx * threadElemExtent;
         if (first >= a.n)
             return;

@@ -72,6 +72,60 @@ TEST_CASE("divideForBackend table shapes (test_work_div.cpp:60-115)")
     }
 }
 
+// Acceptance criterion 04 (acceptance.cpp:269-306), same seed, sampler and checks, over every
+// backend including GpuCudaRt (whose division the C-ABI must reproduce).
+TEST_CASE("criterion 04: work-division law (acceptance.cpp:269-306)")
+{
+    std::mt19937_64 rng(404);
+    const BackendKind backends[] = {BackendKind::Serial, BackendKind::ThreadsParallel, BackendKind::BlocksParallel,
+                                    BackendKind::GpuCudaRt};
+    auto randomExtent = [&](std::size_t dim, std::size_t maxProduct) {
+        std::size_t comp[3] = {1, 1, 1};
+        std::size_t budget = maxProduct;
+        for (std::size_t k = 0; k < dim; ++k) {
+            std::uniform_int_distribution<std::size_t> dist(1, std::max<std::size_t>(1, budget));
+            comp[k] = dist(rng);
+            budget = std::max<std::size_t>(1, budget / comp[k]);
+        }
+        return dim == 1 ? IndexVec(comp[0]) : dim == 2 ? IndexVec(comp[0], comp[1]) : IndexVec(comp[0], comp[1], comp[2]);
+    };
+    std::size_t failures = 0, gpuCases = 0;
+    for (int iter = 0; iter < 1000; ++iter) {
+        const std::size_t dim = 1 + rng() % 3;
+        const IndexVec n = randomExtent(dim, 1 << 20);
+        IndexVec b = IndexVec::filled(dim, 1), v = IndexVec::filled(dim, 1);
+        for (std::size_t k = 0; k < dim; ++k) {
+            b = b.with(k, 1 + rng() % 64);
+            v = v.with(k, 1 + rng() % 16);
+        }
+        const BackendKind backend = backends[rng() % 4];
+        const WorkDiv wd = divideForBackend(n, backend, b, v);
+        const bool threadLevel = backend == BackendKind::ThreadsParallel || backend == BackendKind::GpuCudaRt;
+        if (!threadLevel && wd.threadsPerBlock() != IndexVec::filled(dim, 1))
+            ++failures;
+        if (threadLevel && wd.threadsPerBlock() != b)
+            ++failures;
+        const IndexVec coverage = totalExtent(wd, Level::Grid, Unit::Elems);
+        for (std::size_t k = 0; k < dim; ++k) {
+            if (coverage[k] < n[k])
+                ++failures;
+            const std::size_t perBlock = wd.threadsPerBlock()[k] * wd.elementsPerThread()[k];
+            if ((wd.blocksPerGrid()[k] - 1) * perBlock >= n[k])
+                ++failures;
+        }
+        if (backend == BackendKind::GpuCudaRt) {
+            ++gpuCases;
+            kw_workdiv c{};
+            const auto pp = n.padded(), tt = b.padded(), ee = v.padded();
+            if (kw_divide_for_gpu(static_cast<uint32_t>(dim), pp.data(), tt.data(), ee.data(), &c) != KW_OK ||
+                !(WorkDiv::fromC(c) == wd))
+                ++failures;
+        }
+    }
+    std::printf("  criterion 04: 1000 random (N, B, V), %zu on GpuCudaRt, %zu violations\n", gpuCases, failures);
+    CHECK(failures == 0);
+}
+
 TEST_CASE("getIdx / getWorkDiv: enum form == template-tag form (test_accel.cpp:61-86)")
 {
     const WorkDiv wd(IndexVec(4), IndexVec(16), IndexVec(8));
