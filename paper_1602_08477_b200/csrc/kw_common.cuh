@@ -122,6 +122,11 @@ void release_slot(FailSlot& fs);
 // Makes a slot whose writer is already enqueued on q->stream pending (and the next event's slot).
 void arm_slot(Queue* q, std::shared_ptr<FailSlot> fs);
 
+// SPLIT DGEMM launches keep per-stream scratch (kw_dgemm.cu): the abort word a bounded piece
+// wait sets (read and cleared here by kw_queue_wait), and the release on queue destruction.
+uint32_t split_take_abort(cudaStream_t s);
+void split_release(cudaStream_t s);
+
 // Ensures q->scratch holds at least `bytes` of device memory on q's device.
 kw_status ensure_scratch(Queue* q, size_t bytes);
 

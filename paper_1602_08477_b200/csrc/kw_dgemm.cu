@@ -407,10 +407,49 @@ struct TmaCfg {
     static_assert(WN % 16 == 0 && BN % 16 == 0 && BM <= 256, "tile shape");
 };
 
-template <class Cfg, bool STREAMED = false>
+// SPLIT (resident operands, one persistent CTA per SM): the T x K k-tiles of the problem
+// (T output tiles, K k-tiles each) are cut into G equal contiguous ranges in (tile, k-tile)
+// order, one per CTA, so every SM gets the same number of k-tiles however T divides by G (the
+// wave-quantisation loss of small outputs: 256 tiles on 148 SMs). A tile that straddles two
+// ranges runs as a head piece [0, x) on CTA c and a tail piece [x, K) on CTA c + 1: the head
+// parks its accumulators (exact doubles) in slot c and raises a per-warp flag; the tail waits
+// for the flag, reloads them and continues the same DMMA chain — same thread role, same k
+// order, so the bits equal a one-CTA tile (no split-k reduction; the bits do not depend on M,
+// N, G or the piece boundaries). Each CTA runs its head piece FIRST and its tail piece LAST,
+// and CTA indices are taken from an atomic ticket in start order, so the CTA a tail waits on
+// is already running and its head piece depends on nothing: no wait can deadlock.
+// Scratch (per stream, kw::gemm::split_scratch): p.ready = [u64 ticket][u64 abort-word pointer]
+// [G * CONSUMERS u32 flags], p.partial = G park slots of CONSUMERS * MT * NT * 32 double2.
+struct SplitRange {
+    int head, nfull, tail;     // piece counts (head/tail 0 or 1)
+    int t_head, x_head;        // head piece: tile, k-tiles [0, x_head)
+    int t_full0;               // first full tile
+    int t_tail, x_tail;        // tail piece: tile, k-tiles [x_tail, K)
+};
+__host__ __device__ inline SplitRange split_range(long long T, long long K, long long G, long long c)
+{
+    SplitRange r{};
+    const long long W = T * K, lo = W * c / G, hi = W * (c + 1) / G;
+    if (hi <= lo)
+        return r;
+    const long long tf = lo / K, tl = (hi - 1) / K;
+    r.tail = (lo % K) != 0;
+    r.t_tail = static_cast<int>(tf);
+    r.x_tail = static_cast<int>(lo % K);
+    r.head = (hi % K) != 0 && tl > tf;
+    r.t_head = static_cast<int>(tl);
+    r.x_head = static_cast<int>(hi % K);
+    const long long f0 = r.tail ? tf + 1 : tf, f1 = (hi % K) != 0 ? tl : tl + 1; // full tiles [f0, f1)
+    r.t_full0 = static_cast<int>(f0);
+    r.nfull = f1 > f0 ? static_cast<int>(f1 - f0) : 0;
+    return r;
+}
+
+template <class Cfg, bool STREAMED = false, bool SPLIT = false>
 __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmParams p)
 {
+    static_assert(!(STREAMED && SPLIT), "one tile-walk mode");
     extern __shared__ uint8_t smem_raw[];
     // 1 KiB alignment (128B-swizzled TMA boxes) by pointer arithmetic on the __shared__ array, not
     // through an integer cast: the compiler must still see a shared-space pointer, so fragment
@@ -426,8 +465,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     // stages while the consumers run the epilogue). All CTAs at step j work on consecutive tile
     // ids, which keeps the L2 locality of the rasterisation.
     constexpr int GROUP = 8;
-    const int ntiles = STREAMED ? p.tile_list[0].x : p.tiles_m * p.tiles_n;
+    int ntiles = STREAMED ? p.tile_list[0].x : p.tiles_m * p.tiles_n;
     const int ktiles = (p.k + Cfg::BK - 1) / Cfg::BK;
+    SplitRange sr{};
     // Tile origin and k-tile range [kt0, kt1) of work item `tile`; false = padding entry.
     auto origin = [&](int tile, int& bm, int& bn, int& kt0, int& kt1) {
         if constexpr (STREAMED) {
@@ -438,6 +478,28 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
             kt1 = v.w & 0x07ffffff; // bits 27..30: the entry's pass (its set of panel flags)
             return v.x >= 0;
         }
+        if constexpr (SPLIT) {
+            // piece `tile` of this CTA's range: head, full tiles, tail
+            if (tile < sr.head) {
+                kt0 = 0;
+                kt1 = sr.x_head;
+                tile = sr.t_head;
+            }
+            else if (tile < sr.head + sr.nfull) {
+                kt0 = 0;
+                kt1 = ktiles;
+                tile = sr.t_full0 + (tile - sr.head);
+            }
+            else {
+                kt0 = sr.x_tail;
+                kt1 = ktiles;
+                tile = sr.t_tail;
+            }
+        }
+        else {
+            kt0 = 0;
+            kt1 = ktiles;
+        }
         const int per_group = GROUP * p.tiles_n;
         const int group = tile / per_group;
         const int first_m = group * GROUP;
@@ -445,8 +507,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
         const int in_group = tile - group * per_group;
         bm = (first_m + in_group % gsize) * Cfg::BM;
         bn = (in_group / gsize) * Cfg::BN;
-        kt0 = 0;
-        kt1 = ktiles;
         return true;
     };
 
@@ -459,7 +519,22 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
         }
         fence_mbar_init();
     }
-    __syncthreads();
+    // SPLIT: this CTA's range index = its start-order ticket (see split_range)
+    int first = blockIdx.x, step = gridDim.x, ticket = 0;
+    if constexpr (SPLIT) {
+        __shared__ int s_ticket;
+        if (tid == 0)
+            s_ticket = static_cast<int>(atomicAdd(reinterpret_cast<unsigned long long*>(p.ready), 1ull) % gridDim.x);
+        __syncthreads();
+        ticket = s_ticket;
+        sr = split_range(static_cast<long long>(p.tiles_m) * p.tiles_n, ktiles, gridDim.x, ticket);
+        ntiles = sr.head + sr.nfull + sr.tail;
+        first = 0;
+        step = 1;
+    }
+    else {
+        __syncthreads();
+    }
 
     if (warp >= Cfg::CONSUMERS) {
         // ---------------- producer warpgroup ----------------
@@ -473,7 +548,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
             uint32_t* abort = nullptr;
             if constexpr (STREAMED)
                 abort = p.ready + p.tile_list[0].y * (p.npr + p.npc) + 2 * p.npr * p.npc;
-            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            for (int tile = first; tile < ntiles; tile += step) {
                 int bm, bn, kt0, kt1;
                 if (!origin(tile, bm, bn, kt0, kt1))
                     continue;
@@ -544,7 +619,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
 
     const bool c_vec = (p.ldc % 2 == 0) && (reinterpret_cast<uintptr_t>(p.c) % 16 == 0);
     int it0 = 0; // ring position of this tile's first k-tile
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    for (int tile = first; tile < ntiles; tile += step) {
     int bm, bn, kt0, kt1;
     if (!origin(tile, bm, bn, kt0, kt1))
         continue;
@@ -556,12 +631,49 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
         const size_t tid_tile = static_cast<size_t>(bm / Cfg::BM) * p.tiles_n + bn / Cfg::BN;
         park = reinterpret_cast<double2*>(p.partial) + (tid_tile * Cfg::CONSUMERS + warp) * (Cfg::MT * Cfg::NT) * 32 + lane;
     }
+    // SPLIT: a tail piece reloads slot ticket - 1 (its head ran on the previous ticket), a head
+    // piece parks into slot ticket.
+    uint32_t* split_flags = SPLIT ? p.ready + 4 : nullptr;
+    if constexpr (SPLIT) {
+        const int slot = kt0 > 0 ? ticket - 1 : ticket;
+        park = reinterpret_cast<double2*>(p.partial) +
+               (static_cast<size_t>(slot) * Cfg::CONSUMERS + warp) * (Cfg::MT * Cfg::NT) * 32 + lane;
+    }
     double acc[Cfg::MT][Cfg::NT][2];
 #pragma unroll
     for (int i = 0; i < Cfg::MT; ++i)
 #pragma unroll
         for (int j = 0; j < Cfg::NT; ++j)
             acc[i][j][0] = acc[i][j][1] = 0.0;
+    if constexpr (SPLIT) {
+        if (kt0 > 0) {
+            // wait for the head piece's park (flag of slot ticket - 1, this warp), bounded
+            uint32_t* f = split_flags + (ticket - 1) * Cfg::CONSUMERS + warp;
+            uint32_t ns = 32;
+            for (long long spins = 0; ld_acquire_gpu(f) == 0; ++spins) {
+                if (spins > (1ll << 26)) {
+                    // never by construction (split_range); report instead of hanging the GPU
+                    uint32_t* abort = *reinterpret_cast<uint32_t* const*>(p.ready + 2);
+                    if (lane == 0 && abort)
+                        atomicExch_system(abort, KW_FAIL_READY_TIMEOUT);
+                    break;
+                }
+                __nanosleep(ns);
+                ns = ns < 1024 ? ns * 2 : ns;
+            }
+#pragma unroll
+            for (int i = 0; i < Cfg::MT; ++i)
+#pragma unroll
+                for (int j = 0; j < Cfg::NT; ++j) {
+                    const double2 v = __ldcg(park + (i * Cfg::NT + j) * 32);
+                    acc[i][j][0] = v.x;
+                    acc[i][j][1] = v.y;
+                }
+            __syncwarp();
+            if (lane == 0)
+                *f = 0; // consumed: the flags are all zero again when the launch ends
+        }
+    }
     if constexpr (STREAMED) {
         if (kt0 > 0) {
 #pragma unroll
@@ -693,6 +805,23 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
 
     }
     it0 += nkt;
+    if constexpr (SPLIT) {
+        if (kt1 < ktiles) {
+            // head piece: park the accumulators in slot `ticket`, then raise this warp's flag
+#pragma unroll
+            for (int i = 0; i < Cfg::MT; ++i)
+#pragma unroll
+                for (int j = 0; j < Cfg::NT; ++j)
+                    __stcg(park + (i * Cfg::NT + j) * 32, make_double2(acc[i][j][0], acc[i][j][1]));
+            __threadfence();
+            __syncwarp();
+            if (lane == 0)
+                asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(split_flags + ticket * Cfg::CONSUMERS + warp),
+                             "r"(1u)
+                             : "memory");
+            continue;
+        }
+    }
     if constexpr (STREAMED) {
         if (kt1 < ktiles) {
             // first pass of a k-split: park the accumulators; the second pass (same CTA, same
@@ -1282,13 +1411,13 @@ kw_status launch_tma(cudaStream_t s, const GemmParams& p0)
             return kw::usage("dgemm (streamed): tensor map encoding failed");
         return launch_dmma<Cfg128>(s, p0);
     }
-    const kw_status st = ensure_smem(reinterpret_cast<const void*>(dgemm_tma_kernel<Cfg, STREAMED>), Cfg::SMEM,
+    const kw_status st = ensure_smem(reinterpret_cast<const void*>(dgemm_tma_kernel<Cfg, STREAMED, false>), Cfg::SMEM,
                                      "dgemm: cudaFuncSetAttribute");
     if (st != KW_OK)
         return st;
     const long long resident = static_cast<long long>(sm_count()) * Cfg::MIN_BLOCKS;
     const unsigned grid = static_cast<unsigned>(PERSISTENT && tiles > resident ? resident : tiles);
-    dgemm_tma_kernel<Cfg, STREAMED><<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(ma, mb, p);
+    dgemm_tma_kernel<Cfg, STREAMED, false><<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(ma, mb, p);
     kw::g_launches.fetch_add(1, std::memory_order_relaxed);
     return KW_OK;
 }
@@ -1303,7 +1432,116 @@ using Tma64x128x2 = TmaCfg<64, 128, 64, 32, 4, 2>; // 13
 using Tma128p = TmaCfg<128, 128, 64, 32, 6, 1, true>;       // 14: LDS.128 paired A fragments
 using Tma64x128x2p = TmaCfg<64, 128, 64, 32, 4, 2, true>;   // 16: paired, two CTAs per SM
 using Tma64x64x3p = TmaCfg<64, 64, 32, 32, 4, 3, true>;     // 17: paired, three CTAs per SM
+using Split64w8 = TmaCfg<64, 64, 32, 16, 8, 1, true>;       // 18: SPLIT, 8 consumers of 32x16, 1 CTA/SM
+using Split64w4 = TmaCfg<64, 64, 32, 32, 8, 1, true>;       // 19: SPLIT, 4 consumers of 32x32
+using Split64x128w8 = TmaCfg<64, 128, 32, 32, 6, 1, true>;  // 20: SPLIT, 8 consumers of 32x32
 // (16 consumer warps of 32x32 were measured out: 104 registers per consumer spill.)
+
+// ---- SPLIT launches: per-stream scratch (ticket, abort pointer, flags, park slots) ----------
+struct SplitScratch {
+    int device = -1;
+    cudaStream_t stream = nullptr;
+    uint32_t* flags = nullptr; // [u64 ticket][u64 abort pointer][flags]
+    size_t flag_words = 0;
+    double* park = nullptr;
+    size_t park_bytes = 0;
+    uint32_t* abort_host = nullptr; // mapped pinned: [u32 abort][pad][u64 its device address]
+};
+std::mutex g_split_mu;
+std::vector<SplitScratch*> g_split;
+
+kw_status split_scratch(cudaStream_t s, size_t flag_words, size_t park_bytes, uint32_t** flags, double** park)
+{
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(g_split_mu);
+    SplitScratch* sc = nullptr;
+    for (SplitScratch* x : g_split)
+        if (x->device == dev && x->stream == s)
+            sc = x;
+    if (!sc) {
+        sc = new SplitScratch;
+        sc->device = dev;
+        sc->stream = s;
+        g_split.push_back(sc);
+    }
+    cudaError_t e = cudaSuccess;
+    if (!sc->abort_host) {
+        void* h = nullptr;
+        e = cudaHostAlloc(&h, 16, cudaHostAllocMapped | cudaHostAllocPortable);
+        if (e != cudaSuccess)
+            return kw::cuda_fail("dgemm split: pinned abort word", e);
+        sc->abort_host = static_cast<uint32_t*>(h);
+        void* d = nullptr;
+        cudaHostGetDevicePointer(&d, h, 0);
+        sc->abort_host[0] = 0;
+        *reinterpret_cast<void**>(sc->abort_host + 2) = d;
+    }
+    if (sc->flag_words < flag_words || sc->park_bytes < park_bytes) {
+        cudaStreamSynchronize(s); // the previous launches on this stream still use the old scratch
+        if (sc->flag_words < flag_words) {
+            cudaFree(sc->flags);
+            sc->flags = nullptr;
+            sc->flag_words = 0;
+            e = cudaMalloc(&sc->flags, flag_words * sizeof(uint32_t));
+            if (e == cudaSuccess)
+                e = cudaMemsetAsync(sc->flags, 0, flag_words * sizeof(uint32_t), s);
+            if (e == cudaSuccess) // the kernel finds the abort word through the scratch
+                e = cudaMemcpyAsync(sc->flags + 2, sc->abort_host + 2, 8, cudaMemcpyHostToDevice, s);
+            if (e != cudaSuccess)
+                return kw::cuda_fail("dgemm split: flag scratch", e);
+            sc->flag_words = flag_words;
+        }
+        if (sc->park_bytes < park_bytes) {
+            cudaFree(sc->park);
+            sc->park = nullptr;
+            sc->park_bytes = 0;
+            e = cudaMalloc(&sc->park, park_bytes);
+            if (e != cudaSuccess)
+                return kw::cuda_fail("dgemm split: park scratch", e);
+            sc->park_bytes = park_bytes;
+        }
+    }
+    *flags = sc->flags;
+    *park = sc->park;
+    return KW_OK;
+}
+
+// One persistent CTA per SM over equal (tile, k-tile) ranges (dgemm_tma_kernel SPLIT).
+template <class Cfg>
+kw_status launch_split(cudaStream_t s, const GemmParams& p0)
+{
+    static_assert(Cfg::PAIRED && Cfg::MIN_BLOCKS == 1, "split: paired k-map, one CTA per SM");
+    GemmParams p = p0;
+    p.tiles_m = static_cast<int>(kw::ceil_div(p.m, Cfg::BM));
+    p.tiles_n = static_cast<int>(kw::ceil_div(p.n, Cfg::BN));
+    const long long tiles = static_cast<long long>(p.tiles_m) * p.tiles_n;
+    const long long G = sm_count();
+    const long long ktiles = kw::ceil_div(p.k, Cfg::BK);
+    // every range must span at least one whole tile (a tile is then split at most once)
+    if (tiles < G || ktiles < 2 || tiles * ktiles > INT_MAX || !tma_eligible(p))
+        return launch_tma<Tma64x64x3p>(s, p0);
+    CUtensorMap ma, mb;
+    if (!make_map(&ma, p.a, p.m, p.k, p.lda, Cfg::BM) || !make_map(&mb, p.b, p.k, p.n, p.ldb, 16))
+        return launch_dmma<Cfg128>(s, p0);
+    uint32_t* flags = nullptr;
+    double* park = nullptr;
+    kw_status st = split_scratch(s, 4 + static_cast<size_t>(G) * Cfg::CONSUMERS,
+                                 static_cast<size_t>(G) * Cfg::CONSUMERS * Cfg::MT * Cfg::NT * 32 * sizeof(double2), &flags,
+                                 &park);
+    if (st != KW_OK)
+        return st;
+    p.ready = flags;
+    p.partial = park;
+    p.tile_list = nullptr;
+    st = ensure_smem(reinterpret_cast<const void*>(dgemm_tma_kernel<Cfg, false, true>), Cfg::SMEM,
+                     "dgemm: cudaFuncSetAttribute");
+    if (st != KW_OK)
+        return st;
+    dgemm_tma_kernel<Cfg, false, true><<<static_cast<unsigned>(G), Cfg::THREADS, Cfg::SMEM, s>>>(ma, mb, p);
+    kw::g_launches.fetch_add(1, std::memory_order_relaxed);
+    return KW_OK;
+}
 
 struct CfgInfo {
     int bm, bn, bk, threads, stages;
@@ -1334,6 +1572,10 @@ const CfgInfo kCfgs[] = {
      launch_tma<Tma64x128x2p>},
     {Tma64x64x3p::BM, Tma64x64x3p::BN, Tma64x64x3p::BK, Tma64x64x3p::THREADS, Tma64x64x3p::STAGES,
      launch_tma<Tma64x64x3p>},
+    {Split64w8::BM, Split64w8::BN, Split64w8::BK, Split64w8::THREADS, Split64w8::STAGES, launch_split<Split64w8>},
+    {Split64w4::BM, Split64w4::BN, Split64w4::BK, Split64w4::THREADS, Split64w4::STAGES, launch_split<Split64w4>},
+    {Split64x128w8::BM, Split64x128w8::BN, Split64x128w8::BK, Split64x128w8::THREADS, Split64x128w8::STAGES,
+     launch_split<Split64x128w8>},
 };
 constexpr int kNumCfgs = sizeof(kCfgs) / sizeof(kCfgs[0]);
 // Tile choice for the GPU back-end. The tile work division (gemmTiledWorkDiv) is the coverage
@@ -1425,6 +1667,40 @@ kw_status launch_streamed(cudaStream_t s, int cfg, const GemmParams& p)
 } // namespace kw::gemm
 
 namespace kw {
+uint32_t split_take_abort(cudaStream_t s)
+{
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(g_split_mu);
+    for (SplitScratch* x : g_split)
+        if (x->device == dev && x->stream == s && x->abort_host) {
+            const uint32_t v = *reinterpret_cast<volatile uint32_t*>(x->abort_host);
+            if (v)
+                x->abort_host[0] = 0;
+            return v;
+        }
+    return 0;
+}
+
+void split_release(cudaStream_t s)
+{
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(g_split_mu);
+    for (size_t i = 0; i < g_split.size(); ++i) {
+        SplitScratch* x = g_split[i];
+        if (x->device == dev && x->stream == s) {
+            cudaStreamSynchronize(s);
+            cudaFree(x->flags);
+            cudaFree(x->park);
+            cudaFreeHost(x->abort_host);
+            delete x;
+            g_split.erase(g_split.begin() + static_cast<long>(i));
+            return;
+        }
+    }
+}
+
 // Used by the row-sharded driver (kw_comm.cu).
 kw_status dgemm_device(cudaStream_t s, int tile, size_t m, size_t n, size_t k, double alpha, const double* A,
                        size_t lda, const double* B, size_t ldb, double beta, double* C, size_t ldc)

@@ -484,6 +484,8 @@ kw_status kw_queue_destroy(kw_queue qh)
     if (q->scratch)
         cudaFree(q->scratch);
     cudaStreamSynchronize(q->comp2);
+    kw::split_release(q->stream);
+    kw::split_release(q->comp2);
     cudaStreamDestroy(q->comp2);
     cudaStreamDestroy(q->h2d);
     cudaStreamDestroy(q->aux);
@@ -507,6 +509,9 @@ kw_status kw_queue_wait(kw_queue qh)
     }
     else
         kw::resolve_slots(q, slots, true);
+    for (cudaStream_t st : {q->stream, q->comp2})
+        if (kw::split_take_abort(st))
+            kw::task_fail(q, "dgemm (split): a tail piece's head never parked (bounded wait timed out)");
     std::lock_guard<std::mutex> lock(q->mu);
     if (q->failed == 0)
         return KW_OK;

@@ -462,7 +462,8 @@ def test_paired_configs_are_bitwise_interchangeable(gpu, oracle):
     paired = [c for c in range(lib.kw_dgemm_config_count()) if c >= 14]
     rng = np.random.default_rng(31)
     q = kw.Queue(gpu, kw.QueueFlavor.Async)
-    for (m, n, k) in ((300, 260, 170), (1024, 1024, 1024), (129, 640, 48)):
+    for (m, n, k) in ((300, 260, 170), (1024, 1024, 1024), (129, 640, 48), (1000, 1100, 333), (700, 2000, 50),
+                      (640, 960, 2048)):
         a, b, c = rng.random((m, k)) * 10, rng.random((k, n)) * 10, rng.random((m, n)) * 10
         outs = []
         for cfg in paired:
@@ -474,6 +475,36 @@ def test_paired_configs_are_bitwise_interchangeable(gpu, oracle):
         for o in outs[1:]:
             assert np.array_equal(o, outs[0]), (m, n, k)
         assert within_tol(outs[0], oracle.gemm(0.9, 1.1, a, b, c), k)[0]
+
+
+def test_split_schedule_repeats_and_concurrent_queues(gpu, oracle):
+    """SPLIT configurations (18..20: one CTA per SM over equal (tile, k-tile) ranges, a tile
+    straddling two ranges finished by the next CTA from parked accumulators): the per-stream
+    ticket counter and the self-clearing flags survive back-to-back launches and two queues
+    running split launches at once; every result equals the one-CTA-per-tile launch."""
+    lib = L.lib()
+    rng = np.random.default_rng(8)
+    m, n, k = 1100, 1300, 700
+    a, b, c = rng.random((m, k)) * 10, rng.random((k, n)) * 10, rng.random((m, n)) * 10
+    A, B, C0 = mat(gpu, a), mat(gpu, b), mat(gpu, c)
+    q0 = kw.Queue(gpu, kw.QueueFlavor.Async)
+    assert lib.kw_dgemm_with_config(q0.handle(), 17, m, n, k, 1.3, A.data(), A.leadingDim(), B.data(), B.leadingDim(),
+                                    0.7, C0.data(), C0.leadingDim()) == 0
+    q0.wait()
+    want = C0.download()
+    qs = [kw.Queue(gpu, kw.QueueFlavor.Async) for _ in range(2)]
+    outs = [[mat(gpu, c) for _ in range(6)] for _ in qs]
+    for i in range(6):  # interleave enqueues on both queues
+        for qi, q in enumerate(qs):
+            Cb = outs[qi][i]
+            cfg = 18 + (i + qi) % 3
+            assert lib.kw_dgemm_with_config(q.handle(), cfg, m, n, k, 1.3, A.data(), A.leadingDim(), B.data(),
+                                            B.leadingDim(), 0.7, Cb.data(), Cb.leadingDim()) == 0
+    for q in qs:
+        q.wait()
+    for row in outs:
+        for Cb in row:
+            assert np.array_equal(Cb.download(), want)
 
 
 def test_mixed_residency_dgemm(gpu, oracle):
