@@ -262,6 +262,12 @@ KW_EXPORT kw_status kw_dgemm_rowsharded(kw_comm comm, kw_queue q, size_t m_local
 /* Doubles the b_panels scratch of kw_dgemm_rowsharded must hold for (n, k, panels). */
 KW_EXPORT kw_status kw_dgemm_rowsharded_scratch(size_t n, size_t k, int panels, size_t* elems);
 
+/* SPLIT DGEMM schedule of CTA `cta` of `ctas` (host-side view of the device planner, for tests):
+ * out = {ndp, dp0, dp_step, head, nfull, tail, t_head, x_head, t_full0, t_tail, x_tail};
+ * dp_tiles < 0 = the library's default data-parallel share. */
+KW_EXPORT kw_status kw_dgemm_split_plan(long long tiles, long long ktiles, long long ctas, long long cta,
+                                        long long dp_tiles, int out[11]);
+
 /* ---- measurement helpers (bench / tests) --------------------------------------------------- */
 /* Writes a device scratch buffer larger than L2 (flush between timed iterations). */
 KW_EXPORT kw_status kw_l2_flush(kw_queue q);

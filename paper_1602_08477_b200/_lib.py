@@ -87,6 +87,8 @@ SIGNATURES = {
                                  vp, size_t, vp, C.c_int, C.c_int]),
     "kw_dgemm_rowsharded_scratch": (st, [size_t, size_t, C.c_int, C.POINTER(size_t)]),
     "kw_l2_flush": (st, [vp]),
+    "kw_dgemm_split_plan": (st, [C.c_longlong, C.c_longlong, C.c_longlong, C.c_longlong, C.c_longlong,
+                                 C.POINTER(C.c_int)]),
     "kw_launch_count": (C.c_uint64, []),
     "kw_axpy_kernel_name": (st, [C.POINTER(kw_workdiv), C.c_int, vp, vp, C.c_char_p, size_t]),
     "kw_device_pci_bus_id": (st, [C.c_int, C.c_char_p, C.c_int]),

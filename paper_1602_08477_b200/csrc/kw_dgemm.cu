@@ -35,6 +35,7 @@
 #include <algorithm>
 #include <atomic>
 #include <climits>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -421,15 +422,31 @@ struct TmaCfg {
 // Scratch (per stream, kw::gemm::split_scratch): p.ready = [u64 ticket][u64 abort-word pointer]
 // [G * CONSUMERS u32 flags], p.partial = G park slots of CONSUMERS * MT * NT * 32 double2.
 struct SplitRange {
+    int ndp, dp0, dp_step;     // data-parallel tiles dp0 + j * dp_step, j < ndp (run first)
     int head, nfull, tail;     // piece counts (head/tail 0 or 1)
     int t_head, x_head;        // head piece: tile, k-tiles [0, x_head)
     int t_full0;               // first full tile
     int t_tail, x_tail;        // tail piece: tile, k-tiles [x_tail, K)
 };
-__host__ __device__ inline SplitRange split_range(long long T, long long K, long long G, long long c)
+// Tiles [0, Tdp) run data-parallel (CTA c: tiles c, c + G, ...: concurrent CTAs work on
+// neighbouring tiles, the L2 locality of the ordinary grid); the last Ts = T - Tdp tiles
+// (G <= Ts < 2G by default) are cut into the equal k-tile ranges. dp_override >= 0 sets Tdp.
+__host__ __device__ inline long long split_dp_tiles(long long T, long long G, long long dp_override)
+{
+    const long long cap = T >= G ? (T - G) / G * G : 0; // leaves >= G tiles to the ranges
+    if (dp_override >= 0)
+        return dp_override / G * G < cap ? dp_override / G * G : cap;
+    return cap;
+}
+__host__ __device__ inline SplitRange split_range(long long T, long long K, long long G, long long c,
+                                                   long long dp_override = -1)
 {
     SplitRange r{};
-    const long long W = T * K, lo = W * c / G, hi = W * (c + 1) / G;
+    const long long Tdp = split_dp_tiles(T, G, dp_override);
+    r.ndp = static_cast<int>(Tdp / G);
+    r.dp0 = static_cast<int>(c);
+    r.dp_step = static_cast<int>(G);
+    const long long W = (T - Tdp) * K, lo = Tdp * K + W * c / G, hi = Tdp * K + W * (c + 1) / G;
     if (hi <= lo)
         return r;
     const long long tf = lo / K, tl = (hi - 1) / K;
@@ -443,6 +460,14 @@ __host__ __device__ inline SplitRange split_range(long long T, long long K, long
     r.t_full0 = static_cast<int>(f0);
     r.nfull = f1 > f0 ? static_cast<int>(f1 - f0) : 0;
     return r;
+}
+
+// Reports a piece wait that timed out (abort word, see kw_queue_wait) instead of hanging the GPU.
+__device__ __noinline__ void split_abort(const uint32_t* scratch, int lane)
+{
+    uint32_t* abort = *reinterpret_cast<uint32_t* const*>(scratch + 2);
+    if (lane == 0 && abort)
+        atomicExch_system(abort, KW_FAIL_READY_TIMEOUT);
 }
 
 template <class Cfg, bool STREAMED = false, bool SPLIT = false>
@@ -467,7 +492,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     constexpr int GROUP = 8;
     int ntiles = STREAMED ? p.tile_list[0].x : p.tiles_m * p.tiles_n;
     const int ktiles = (p.k + Cfg::BK - 1) / Cfg::BK;
-    SplitRange sr{};
+    // SPLIT: this CTA's plan lives in shared memory (read per piece) — per-thread copies cost the
+    // 2- and 3-CTA/SM configurations their register budget (spills).
+    __shared__ SplitRange sr;
     // Tile origin and k-tile range [kt0, kt1) of work item `tile`; false = padding entry.
     auto origin = [&](int tile, int& bm, int& bn, int& kt0, int& kt1) {
         if constexpr (STREAMED) {
@@ -479,8 +506,13 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
             return v.x >= 0;
         }
         if constexpr (SPLIT) {
-            // piece `tile` of this CTA's range: head, full tiles, tail
-            if (tile < sr.head) {
+            // piece `tile` of this CTA: data-parallel tiles, then head, full tiles, tail
+            if (tile < sr.ndp) {
+                kt0 = 0;
+                kt1 = ktiles;
+                tile = sr.dp0 + tile * sr.dp_step;
+            }
+            else if ((tile -= sr.ndp) < sr.head) {
                 kt0 = 0;
                 kt1 = sr.x_head;
                 tile = sr.t_head;
@@ -519,16 +551,22 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
         }
         fence_mbar_init();
     }
+    // Programmatic dependent launch: the next grid on the stream may start its launch and the
+    // barrier setup above while this one drains; nothing in global memory (A, B, C, the split
+    // scratch) is touched before the previous grid has completed.
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
     // SPLIT: this CTA's range index = its start-order ticket (see split_range)
     int first = blockIdx.x, step = gridDim.x, ticket = 0;
     if constexpr (SPLIT) {
         __shared__ int s_ticket;
-        if (tid == 0)
+        if (tid == 0) {
             s_ticket = static_cast<int>(atomicAdd(reinterpret_cast<unsigned long long*>(p.ready), 1ull) % gridDim.x);
+            sr = split_range(static_cast<long long>(p.tiles_m) * p.tiles_n, ktiles, gridDim.x, s_ticket, p.npr);
+        }
         __syncthreads();
         ticket = s_ticket;
-        sr = split_range(static_cast<long long>(p.tiles_m) * p.tiles_n, ktiles, gridDim.x, ticket);
-        ntiles = sr.head + sr.nfull + sr.tail;
+        ntiles = sr.ndp + sr.head + sr.nfull + sr.tail;
         first = 0;
         step = 1;
     }
@@ -649,17 +687,12 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
         if (kt0 > 0) {
             // wait for the head piece's park (flag of slot ticket - 1, this warp), bounded
             uint32_t* f = split_flags + (ticket - 1) * Cfg::CONSUMERS + warp;
-            uint32_t ns = 32;
-            for (long long spins = 0; ld_acquire_gpu(f) == 0; ++spins) {
-                if (spins > (1ll << 26)) {
-                    // never by construction (split_range); report instead of hanging the GPU
-                    uint32_t* abort = *reinterpret_cast<uint32_t* const*>(p.ready + 2);
-                    if (lane == 0 && abort)
-                        atomicExch_system(abort, KW_FAIL_READY_TIMEOUT);
+            for (uint32_t spins = 0; ld_acquire_gpu(f) == 0; ++spins) {
+                if (spins > (1u << 25)) { // ~30 s: never by construction (split_range)
+                    split_abort(p.ready, lane);
                     break;
                 }
-                __nanosleep(ns);
-                ns = ns < 1024 ? ns * 2 : ns;
+                __nanosleep(256);
             }
 #pragma unroll
             for (int i = 0; i < Cfg::MT; ++i)
@@ -672,6 +705,29 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
             __syncwarp();
             if (lane == 0)
                 *f = 0; // consumed: the flags are all zero again when the launch ends
+        }
+    }
+    // One CTA per SM (SPLIT, MIN_BLOCKS 1): no co-resident CTA covers this tile's epilogue, so
+    // its C reads are issued now and land during the main loop (C belongs to this tile alone).
+    constexpr bool PREFETCH_C = SPLIT && Cfg::MIN_BLOCKS == 1;
+    double2 cpre[PREFETCH_C ? Cfg::MT : 1][PREFETCH_C ? Cfg::NT : 1];
+    if constexpr (PREFETCH_C) {
+        if (kt1 == ktiles) {
+#pragma unroll
+            for (int i = 0; i < Cfg::MT; ++i) {
+                const int row = bm + wm + i * 8 + g;
+                const double* crow = p.c + (row < p.m ? row : 0) * p.ldc;
+#pragma unroll
+                for (int j = 0; j < Cfg::NT; ++j) {
+                    const int col = bn + wn + j * 8 + 2 * t;
+                    if (row < p.m && c_vec && col + 1 < p.n)
+                        cpre[i][j] = __ldcs(reinterpret_cast<const double2*>(crow + col));
+                    else {
+                        cpre[i][j].x = (row < p.m && col < p.n) ? crow[col] : 0.0;
+                        cpre[i][j].y = (row < p.m && col + 1 < p.n) ? crow[col + 1] : 0.0;
+                    }
+                }
+            }
         }
     }
     if constexpr (STREAMED) {
@@ -844,7 +900,20 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
 #pragma unroll
         for (int j = 0; j < Cfg::NT; ++j) {
             const int col = bn + wn + j * 8 + 2 * t;
-            if (c_vec && col + 1 < p.n) {
+            if constexpr (PREFETCH_C) {
+                const double2 old = cpre[i][j];
+                const double x = __dadd_rn(__dmul_rn(p.alpha, acc[i][j][0]), __dmul_rn(p.beta, old.x));
+                const double y = __dadd_rn(__dmul_rn(p.alpha, acc[i][j][1]), __dmul_rn(p.beta, old.y));
+                if (c_vec && col + 1 < p.n)
+                    *reinterpret_cast<double2*>(crow + col) = make_double2(x, y);
+                else {
+                    if (col < p.n)
+                        crow[col] = x;
+                    if (col + 1 < p.n)
+                        crow[col + 1] = y;
+                }
+            }
+            else if (c_vec && col + 1 < p.n) {
                 double2 old = *reinterpret_cast<const double2*>(crow + col);
                 double2 out;
                 out.x = __dadd_rn(__dmul_rn(p.alpha, acc[i][j][0]), __dmul_rn(p.beta, old.x));
@@ -921,6 +990,36 @@ bool make_map_dense(CUtensorMap* map, const double* base, size_t rows, size_t co
     return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, estr,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// KW_DGEMM_PDL=0 launches the TMA kernels without programmatic dependent launch (A/B switch).
+bool dgemm_pdl()
+{
+    static const bool on = [] {
+        const char* e = std::getenv("KW_DGEMM_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+// PDL only where the early-launched grid cannot take free co-resident slots: a dependent CTA
+// placed beside a short grid's CTAs fixes its SM before the grid drains and unbalances the next
+// launch (measured: the 64 x 64 three-CTA tile at 1024^3 fell from 26.9 to 18.0 TFLOP/s).
+template <class Cfg, bool STREAMED, bool SPLIT>
+void launch_tma_kernel(unsigned grid, cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb,
+                       const GemmParams& p, bool pdl)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(Cfg::THREADS);
+    cfg.dynamicSmemBytes = Cfg::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = (pdl && dgemm_pdl()) ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, dgemm_tma_kernel<Cfg, STREAMED, SPLIT>, ma, mb, p);
 }
 
 template <class Cfg, bool PERSISTENT = false, bool STREAMED = false>
@@ -1417,7 +1516,10 @@ kw_status launch_tma(cudaStream_t s, const GemmParams& p0)
         return st;
     const long long resident = static_cast<long long>(sm_count()) * Cfg::MIN_BLOCKS;
     const unsigned grid = static_cast<unsigned>(PERSISTENT && tiles > resident ? resident : tiles);
-    dgemm_tma_kernel<Cfg, STREAMED, false><<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(ma, mb, p);
+    if constexpr (STREAMED)
+        dgemm_tma_kernel<Cfg, true, false><<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(ma, mb, p);
+    else
+        launch_tma_kernel<Cfg, false, false>(grid, s, ma, mb, p, grid >= resident);
     kw::g_launches.fetch_add(1, std::memory_order_relaxed);
     return KW_OK;
 }
@@ -1435,6 +1537,7 @@ using Tma64x64x3p = TmaCfg<64, 64, 32, 32, 4, 3, true>;     // 17: paired, three
 using Split64w8 = TmaCfg<64, 64, 32, 16, 8, 1, true>;       // 18: SPLIT, 8 consumers of 32x16, 1 CTA/SM
 using Split64w4 = TmaCfg<64, 64, 32, 32, 8, 1, true>;       // 19: SPLIT, 4 consumers of 32x32
 using Split64x128w8 = TmaCfg<64, 128, 32, 32, 6, 1, true>;  // 20: SPLIT, 8 consumers of 32x32
+using Split64w8t = TmaCfg<64, 64, 16, 32, 8, 1, true>;      // 23: SPLIT, 8 consumers of 16x32
 // (16 consumer warps of 32x32 were measured out: 104 registers per consumer spill.)
 
 // ---- SPLIT launches: per-stream scratch (ticket, abort pointer, flags, park slots) ----------
@@ -1511,12 +1614,12 @@ kw_status split_scratch(cudaStream_t s, size_t flag_words, size_t park_bytes, ui
 template <class Cfg>
 kw_status launch_split(cudaStream_t s, const GemmParams& p0)
 {
-    static_assert(Cfg::PAIRED && Cfg::MIN_BLOCKS == 1, "split: paired k-map, one CTA per SM");
+    static_assert(Cfg::PAIRED, "split: paired k-map configurations only");
     GemmParams p = p0;
     p.tiles_m = static_cast<int>(kw::ceil_div(p.m, Cfg::BM));
     p.tiles_n = static_cast<int>(kw::ceil_div(p.n, Cfg::BN));
     const long long tiles = static_cast<long long>(p.tiles_m) * p.tiles_n;
-    const long long G = sm_count();
+    const long long G = static_cast<long long>(sm_count()) * Cfg::MIN_BLOCKS; // every CTA resident
     const long long ktiles = kw::ceil_div(p.k, Cfg::BK);
     // every range must span at least one whole tile (a tile is then split at most once)
     if (tiles < G || ktiles < 2 || tiles * ktiles > INT_MAX || !tma_eligible(p))
@@ -1534,11 +1637,16 @@ kw_status launch_split(cudaStream_t s, const GemmParams& p0)
     p.ready = flags;
     p.partial = park;
     p.tile_list = nullptr;
+    static const long long dp_env = [] { // KW_SPLIT_DP_TILES: data-parallel tile count override (sweeps)
+        const char* e = std::getenv("KW_SPLIT_DP_TILES");
+        return e ? std::atoll(e) : -1ll;
+    }();
+    p.npr = static_cast<int>(dp_env);
     st = ensure_smem(reinterpret_cast<const void*>(dgemm_tma_kernel<Cfg, false, true>), Cfg::SMEM,
                      "dgemm: cudaFuncSetAttribute");
     if (st != KW_OK)
         return st;
-    dgemm_tma_kernel<Cfg, false, true><<<static_cast<unsigned>(G), Cfg::THREADS, Cfg::SMEM, s>>>(ma, mb, p);
+    launch_tma_kernel<Cfg, false, true>(static_cast<unsigned>(G), s, ma, mb, p, true);
     kw::g_launches.fetch_add(1, std::memory_order_relaxed);
     return KW_OK;
 }
@@ -1576,6 +1684,12 @@ const CfgInfo kCfgs[] = {
     {Split64w4::BM, Split64w4::BN, Split64w4::BK, Split64w4::THREADS, Split64w4::STAGES, launch_split<Split64w4>},
     {Split64x128w8::BM, Split64x128w8::BN, Split64x128w8::BK, Split64x128w8::THREADS, Split64x128w8::STAGES,
      launch_split<Split64x128w8>},
+    {Tma64x128x2p::BM, Tma64x128x2p::BN, Tma64x128x2p::BK, Tma64x128x2p::THREADS, Tma64x128x2p::STAGES,
+     launch_split<Tma64x128x2p>}, // 21: SPLIT of config 16 (two CTAs per SM)
+    {Tma64x64x3p::BM, Tma64x64x3p::BN, Tma64x64x3p::BK, Tma64x64x3p::THREADS, Tma64x64x3p::STAGES,
+     launch_split<Tma64x64x3p>}, // 22: SPLIT of config 17 (three CTAs per SM)
+    {Split64w8t::BM, Split64w8t::BN, Split64w8t::BK, Split64w8t::THREADS, Split64w8t::STAGES,
+     launch_split<Split64w8t>},
 };
 constexpr int kNumCfgs = sizeof(kCfgs) / sizeof(kCfgs[0]);
 // Tile choice for the GPU back-end. The tile work division (gemmTiledWorkDiv) is the coverage
@@ -1597,6 +1711,26 @@ int pick_config(const GemmParams& p)
     const long long load16 = (t16 + sms - 1) / sms * 8192, load17 = (t17 + sms - 1) / sms * 4096;
     const bool small = t16 <= sms || static_cast<double>(load17) < 0.97 * static_cast<double>(load16);
     return small ? kCfgSmall : kCfgWide;
+}
+
+// Resident launches add the SPLIT configurations (one CTA per SM over equal (tile, k-tile)
+// ranges — same paired DMMA sequence, so again no bit changes) where both data-parallel grids
+// quantise badly: the busiest SM of the better of 16 / 17 carries more than 1/0.93 of the mean
+// output (1024^3: 2 of 1.73 tiles, 0.865 -> split 18 at 30.2 vs 26.9 TFLOP/s; 1280^3: 0.90 ->
+// split 20 at 31.9 vs 28.7; profiles/dgemm_split_sweep_r02.txt). Split 20 (64 x 128 tiles, 8
+// warps of 32 x 32) where it still gives every SM a tile, else split 18 (64 x 64, 8 of 32 x 16).
+constexpr int kCfgSplit64 = 18, kCfgSplit128 = 20;
+int pick_resident(const GemmParams& p)
+{
+    const double sms = sm_count();
+    const long long rows = (p.m + 63) / 64;
+    const long long t16 = rows * ((p.n + 127) / 128), t17 = rows * ((p.n + 63) / 64);
+    const double ideal = static_cast<double>(p.m) * p.n / sms;
+    const double q16 = ideal / (std::ceil(t16 / sms) * 8192.0), q17 = ideal / (std::ceil(t17 / sms) * 4096.0);
+    const long long ktiles = (p.k + 15) / 16;
+    if (std::max(q16, q17) < 0.93 && t17 >= static_cast<long long>(sms) && ktiles >= 2 && tma_eligible(p))
+        return t16 >= static_cast<long long>(sms) ? kCfgSplit128 : kCfgSplit64;
+    return pick_config(p);
 }
 
 
@@ -1638,7 +1772,7 @@ GemmParams make_params(size_t m, size_t n, size_t k, double alpha, const double*
 size_t round2(size_t v) { return ::round2(v); }
 kw_status launch_tiled(cudaStream_t s, int tile, const GemmParams& p)
 {
-    return kCfgs[tile == 64 ? kCfgSmall : pick_config(p)].launch(s, p);
+    return kCfgs[tile == 64 ? kCfgSmall : pick_resident(p)].launch(s, p);
 }
 bool tma_eligible(const GemmParams& p)
 {
@@ -1836,6 +1970,18 @@ kw_status kw_dgemm_bitwise(kw_queue qh, const kw_workdiv* wd, size_t m, size_t n
 }
 
 int kw_dgemm_config_count(void) { return kNumCfgs; }
+
+kw_status kw_dgemm_split_plan(long long tiles, long long ktiles, long long ctas, long long cta, long long dp_tiles,
+                              int out[11])
+{
+    if (!out || tiles < ctas || ctas < 1 || ktiles < 1 || cta < 0 || cta >= ctas)
+        return kw::usage("kw_dgemm_split_plan: needs tiles >= ctas >= 1, ktiles >= 1, 0 <= cta < ctas");
+    const SplitRange r = split_range(tiles, ktiles, ctas, cta, dp_tiles);
+    const int v[11] = {r.ndp, r.dp0, r.dp_step, r.head, r.nfull, r.tail, r.t_head, r.x_head, r.t_full0, r.t_tail,
+                       r.x_tail};
+    std::memcpy(out, v, sizeof(v));
+    return KW_OK;
+}
 
 kw_status kw_dgemm_config_info(int cfg, int info[5])
 {

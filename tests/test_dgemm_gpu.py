@@ -477,6 +477,32 @@ def test_paired_configs_are_bitwise_interchangeable(gpu, oracle):
         assert within_tol(outs[0], oracle.gemm(0.9, 1.1, a, b, c), k)[0]
 
 
+@pytest.mark.parametrize("m,n,k", [(1024, 1024, 1024), (1280, 1280, 640), (1100, 1000, 2000)])
+def test_default_choice_split_is_bitwise_the_one_cta_tile(gpu, oracle, m, n, k):
+    """Shapes the library now runs with a SPLIT configuration (badly quantised data-parallel
+    grids): the default kw_dgemm result equals the one-CTA-per-tile config 17 bit for bit and the
+    oracle within (K+4)u."""
+    lib = L.lib()
+    rng = np.random.default_rng(m + n + k)
+    a, b, c = rng.random((m, k)) * 10, rng.random((k, n)) * 10, rng.random((m, n)) * 10
+    q = kw.Queue(gpu, kw.QueueFlavor.Async)
+    outs = []
+    for cfg in (None, 17):
+        A, B, Cb = mat(gpu, a), mat(gpu, b), mat(gpu, c)
+        if cfg is None:
+            st = lib.kw_dgemm(q.handle(), None, m, n, k, 1.5, A.data(), A.leadingDim(), B.data(), B.leadingDim(), 0.5,
+                              Cb.data(), Cb.leadingDim())
+        else:
+            st = lib.kw_dgemm_with_config(q.handle(), cfg, m, n, k, 1.5, A.data(), A.leadingDim(), B.data(),
+                                          B.leadingDim(), 0.5, Cb.data(), Cb.leadingDim())
+        assert st == 0, L.last_error()
+        q.wait()
+        outs.append(Cb.download())
+    assert np.array_equal(outs[0], outs[1])
+    if m * n * k <= 1 << 30:
+        assert within_tol(outs[0], oracle.gemm(1.5, 0.5, a, b, c, threads=8), k)[0]
+
+
 def test_split_schedule_repeats_and_concurrent_queues(gpu, oracle):
     """SPLIT configurations (18..20: one CTA per SM over equal (tile, k-tile) ranges, a tile
     straddling two ranges finished by the next CTA from parked accumulators): the per-stream
