@@ -574,10 +574,17 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
         __syncthreads();
     }
 
+    // SPLIT gives its producer warpgroup the minimum (24: one lane issues TMA from a short plan)
+    // so the consumers keep the registers the split bookkeeping costs (2- and 3-CTA/SM tiles
+    // spilled with 40).
+    constexpr int PREGS = (SPLIT && Cfg::MIN_BLOCKS > 1) ? 24 : Cfg::PRODUCER_REGS;
+    constexpr int CREGS_RAW = ((Cfg::POOL_PER_LANE - 4 * PREGS) / Cfg::CONSUMERS) / 8 * 8;
+    constexpr int CREGS = CREGS_RAW > 240 ? 240 : CREGS_RAW;
+    static_assert(4 * PREGS + Cfg::CONSUMERS * CREGS <= Cfg::POOL_PER_LANE, "register pool overcommitted");
     if (warp >= Cfg::CONSUMERS) {
         // ---------------- producer warpgroup ----------------
         if constexpr (Cfg::REBALANCE)
-            asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(Cfg::PRODUCER_REGS));
+            asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PREGS));
         if (warp == Cfg::CONSUMERS && lane == 0) {
             tma_prefetch_desc(&tmA);
             tma_prefetch_desc(&tmB);
@@ -628,7 +635,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
 
     // ---------------- consumers ----------------
     if constexpr (Cfg::REBALANCE)
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(Cfg::CONSUMER_REGS));
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(CREGS));
     const int wm = (warp / Cfg::WARPS_N) * Cfg::WM;
     const int wn = (warp % Cfg::WARPS_N) * Cfg::WN;
     const int g = lane >> 2, t = lane & 3;
