@@ -716,7 +716,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     }
     // One CTA per SM (SPLIT, MIN_BLOCKS 1): no co-resident CTA covers this tile's epilogue, so
     // its C reads are issued now and land during the main loop (C belongs to this tile alone).
-    constexpr bool PREFETCH_C = SPLIT && Cfg::MIN_BLOCKS == 1;
+    constexpr bool PREFETCH_C = SPLIT && Cfg::MIN_BLOCKS == 1 && Cfg::MT * Cfg::NT <= 16; // registers
     double2 cpre[PREFETCH_C ? Cfg::MT : 1][PREFETCH_C ? Cfg::NT : 1];
     if constexpr (PREFETCH_C) {
         if (kt1 == ktiles) {
@@ -1697,6 +1697,8 @@ const CfgInfo kCfgs[] = {
      launch_split<Tma64x64x3p>}, // 22: SPLIT of config 17 (three CTAs per SM)
     {Split64w8t::BM, Split64w8t::BN, Split64w8t::BK, Split64w8t::THREADS, Split64w8t::STAGES,
      launch_split<Split64w8t>},
+    {Tma128p::BM, Tma128p::BN, Tma128p::BK, Tma128p::THREADS, Tma128p::STAGES,
+     launch_split<Tma128p>}, // 24: SPLIT of config 14 (128 x 128, 8 consumers of 64 x 32, 1 CTA/SM)
 };
 constexpr int kNumCfgs = sizeof(kCfgs) / sizeof(kCfgs[0]);
 // Tile choice for the GPU back-end. The tile work division (gemmTiledWorkDiv) is the coverage
