@@ -109,3 +109,26 @@ def test_extreme_shapes(gpu, oracle, m, n, k, schedule, monkeypatch):
                          -1.5, Ch.data(), Ch.leadingDim()))
     q.wait()
     assert np.array_equal(Ch.host_view()[:, :n], got)
+
+
+def test_split_configs_agree_bitwise_on_random_cases(gpu):
+    """SPLIT tile walks (configs 18, 20, 24: equal (tile, k-tile) ranges per SM, straddling tiles
+    finished from parked accumulators) on random shapes large enough to split, random scalars
+    and padded leading dimensions: bits equal the one-CTA-per-tile launch (config 17)."""
+    rng = np.random.default_rng(77001)
+    lib = L.lib()
+    q = kw.Queue(gpu, kw.QueueFlavor.Async)
+    for case in range(36):
+        m, n = (int(v) for v in rng.integers(700, 2200, size=2))
+        k = int(rng.integers(17, 1500))
+        alpha = float(rng.choice([1.0, -0.5, 0.75]))
+        beta = float(rng.choice([0.0, 1.0, -1.25]))
+        a, b, c = rng.standard_normal((m, k)), rng.standard_normal((k, n)), rng.standard_normal((m, n))
+        outs = []
+        for cfg in (17, 18 + 2 * (case % 2), 24):
+            A, B, Cd = dev_mat(gpu, a), dev_mat(gpu, b), dev_mat(gpu, c)
+            L.check(lib.kw_dgemm_with_config(q.handle(), cfg, m, n, k, alpha, A.data(), A.leadingDim(), B.data(),
+                                             B.leadingDim(), beta, Cd.data(), Cd.leadingDim()))
+            q.wait()
+            outs.append(Cd.download())
+        assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2]), (case, m, n, k)
