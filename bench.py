@@ -572,8 +572,25 @@ def run_dgemm(args, dist, kw, L, lib, dev, q, sampler) -> dict:
                 entry["cpu_baseline"], entry["parity"] = cpu_baseline_dgemm(a, b, c, 1.25, 0.75, Cb, q, task, bw_task)
             res[f"n{size}"] = entry
             del A, B, Cb, hA, hB, hC
+        # the small end of the BASELINE configs[4] sweep (the library's own tile choice)
+        sweep = {}
+        for size in (1024, 2048):
+            a = rng.random((size, size)) * 10
+            A, B, Cb = (kw.Buffer(dev, kw.IndexVec(size, size), 8) for _ in range(3))
+            for buf in (A, B, Cb):
+                buf.upload(a)
+            task = kw.createExec(GPU, kw.gemmTiledWorkDiv(GPU, size, size, 128), kw.GemmTiledKernel(),
+                                 kw.GemmArgs(size, size, size, 1.25, 0.75, A, B, Cb))
+            steps = max(20, int(2e12 / (2 * size ** 3)))
+            ms = timed(lambda: q.enqueue(task), steps)
+            tflops = 2 * size ** 3 * steps / (ms / 1e3) / 1e12
+            sweep[f"n{size}"] = {"value": round(tflops, 3), "steps": steps, "unit": "TFLOP/s",
+                                 "frac": round(tflops / FP64_NOMINAL_TFLOPS, 4),
+                                 "frac_of_dmma_probe": round(tflops / DGEMM_PEAK_PROBE, 4)}
+            del A, B, Cb
+        res["sweep"] = sweep
         if not args.no_cublas:
-            res["cublas_same_box"] = cublas_dgemm(dist.local, (8192, 4096))
+            res["cublas_same_box"] = cublas_dgemm(dist.local, (8192, 4096, 2048, 1024))
         res["value"] = res["n8192"]["value"]
         res["config"] = "DGEMM fp64 M=N=K=8192 (north-star headline) and 4096 (BASELINE configs[2]), 1 GPU"
         return res
@@ -719,7 +736,7 @@ def cublas_dgemm(device: int, sizes) -> dict:
             for _ in range(2):
                 a @ b
             torch.cuda.synchronize()
-            reps = max(3, int(2e12 / (2 * n ** 3)))
+            reps = max(20, int(2e12 / (2 * n ** 3)))
             e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
             e0.record()
             for _ in range(reps):
