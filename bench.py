@@ -586,7 +586,8 @@ def run_dgemm(args, dist, kw, L, lib, dev, q, sampler) -> dict:
             tflops = 2 * size ** 3 * steps / (ms / 1e3) / 1e12
             sweep[f"n{size}"] = {"value": round(tflops, 3), "steps": steps, "unit": "TFLOP/s",
                                  "frac": round(tflops / FP64_NOMINAL_TFLOPS, 4),
-                                 "frac_of_dmma_probe": round(tflops / DGEMM_PEAK_PROBE, 4)}
+                                 "frac_of_dmma_probe": round(tflops / DGEMM_PEAK_PROBE, 4),
+                                 "traffic": traffic_from_profiles(f"dgemm_{size}")}
             del A, B, Cb
         res["sweep"] = sweep
         if not args.no_cublas:
