@@ -1571,11 +1571,14 @@ struct SplitScratch {
     double* park = nullptr;
     size_t park_bytes = 0;
     uint32_t* abort_host = nullptr; // mapped pinned: [u32 abort][pad][u64 its device address]
+    long long last_grid = 0;        // tickets are (counter % grid): the counter must be a multiple
+                                    // of the grid at every launch (start order = ticket order)
 };
 std::mutex g_split_mu;
 std::vector<SplitScratch*> g_split;
 
-kw_status split_scratch(cudaStream_t s, size_t flag_words, size_t park_bytes, uint32_t** flags, double** park)
+kw_status split_scratch(cudaStream_t s, long long grid, size_t flag_words, size_t park_bytes, uint32_t** flags,
+                        double** park)
 {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1627,6 +1630,15 @@ kw_status split_scratch(cudaStream_t s, size_t flag_words, size_t park_bytes, ui
             sc->park_bytes = park_bytes;
         }
     }
+    if (sc->last_grid != grid) {
+        // A launch with another grid size left the ticket counter at a multiple of ITS grid:
+        // restart it, stream-ordered after the previous launch, so tickets again follow start
+        // order (a rotated order would let a started CTA wait on one that has not started).
+        e = cudaMemsetAsync(sc->flags, 0, 8, s);
+        if (e != cudaSuccess)
+            return kw::cuda_fail("dgemm split: ticket reset", e);
+        sc->last_grid = grid;
+    }
     *flags = sc->flags;
     *park = sc->park;
     return KW_OK;
@@ -1651,7 +1663,7 @@ kw_status launch_split(cudaStream_t s, const GemmParams& p0)
         return launch_dmma<Cfg128>(s, p0);
     uint32_t* flags = nullptr;
     double* park = nullptr;
-    kw_status st = split_scratch(s, 4 + static_cast<size_t>(G) * Cfg::CONSUMERS,
+    kw_status st = split_scratch(s, G, 4 + static_cast<size_t>(G) * Cfg::CONSUMERS,
                                  static_cast<size_t>(G) * Cfg::CONSUMERS * Cfg::MT * Cfg::NT * 32 * sizeof(double2), &flags,
                                  &park);
     if (st != KW_OK)
