@@ -504,10 +504,11 @@ def test_default_choice_split_is_bitwise_the_one_cta_tile(gpu, oracle, m, n, k):
 
 
 def test_split_schedule_repeats_and_concurrent_queues(gpu, oracle):
-    """SPLIT configurations (18..20: one CTA per SM over equal (tile, k-tile) ranges, a tile
-    straddling two ranges finished by the next CTA from parked accumulators): the per-stream
-    ticket counter and the self-clearing flags survive back-to-back launches and two queues
-    running split launches at once; every result equals the one-CTA-per-tile launch."""
+    """SPLIT configurations (one persistent CTA per SM — or 2, 3 for 21, 22 — over equal (tile,
+    k-tile) ranges, a tile straddling two ranges finished by the next CTA from parked
+    accumulators): the per-stream ticket counter (restarted when the grid size changes) and the
+    self-clearing flags survive back-to-back launches of different grids and two queues running
+    split launches at once; every result equals the one-CTA-per-tile launch."""
     lib = L.lib()
     rng = np.random.default_rng(8)
     m, n, k = 1100, 1300, 700
@@ -523,7 +524,7 @@ def test_split_schedule_repeats_and_concurrent_queues(gpu, oracle):
     for i in range(6):  # interleave enqueues on both queues
         for qi, q in enumerate(qs):
             Cb = outs[qi][i]
-            cfg = 18 + (i + qi) % 3
+            cfg = (18, 21, 20, 22, 24, 23)[(i + qi) % 6]  # grids of 148, 296 and 444 CTAs interleaved
             assert lib.kw_dgemm_with_config(q.handle(), cfg, m, n, k, 1.3, A.data(), A.leadingDim(), B.data(),
                                             B.leadingDim(), 0.7, Cb.data(), Cb.leadingDim()) == 0
     for q in qs:
