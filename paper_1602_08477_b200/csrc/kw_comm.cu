@@ -18,11 +18,13 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <utility>
 #include <vector>
 
 namespace kw {
-kw_status dgemm_device(cudaStream_t s, int tile, size_t m, size_t n, size_t k, double alpha, const double* A,
-                       size_t lda, const double* B, size_t ldb, double beta, double* C, size_t ldc);
+int dgemm_pick(size_t m, size_t n, size_t k);
+kw_status dgemm_device_cfg(cudaStream_t s, int cfg, size_t m, size_t n, size_t k, double alpha, const double* A,
+                           size_t lda, const double* B, size_t ldb, double beta, double* C, size_t ldc);
 }
 
 // NCCL is resolved at run time, never linked: a process that already loaded a libnccl.so.2
@@ -98,12 +100,18 @@ kw_status nccl_fail(const char* what, ncclResult_t r)
     return KW_TASK;
 }
 
-// Column panel width (a multiple of the 128-column tile) and the panel's leading dimension in the
-// panel-major scratch (sharding.dgemm_panels mirrors both).
-size_t panel_width(size_t n, int panels)
+// Column panels of B: [n0, n0 + w) pairs, equal widths of ceil(n / panels) rounded up to the
+// 128-column tile. (A "head panel + one remainder" schedule measured slower on one GPU: the
+// root's 2-D copy of the large remainder into the panel-major scratch was exposed —
+// profiles/rowshard_rank_probe_r02.txt.) sharding.dgemm_panels mirrors this.
+std::vector<std::pair<size_t, size_t>> panel_bounds(size_t n, int panels)
 {
     const size_t tile = 128;
-    return kw::ceil_div(kw::ceil_div(n, static_cast<size_t>(panels)), tile) * tile;
+    const size_t w = kw::ceil_div(kw::ceil_div(n, static_cast<size_t>(panels)), tile) * tile;
+    std::vector<std::pair<size_t, size_t>> out;
+    for (size_t n0 = 0; n0 < n; n0 += w)
+        out.emplace_back(n0, n - n0 < w ? n - n0 : w);
+    return out;
 }
 size_t panel_ld(size_t wj) { return (wj + 7) & ~static_cast<size_t>(7); }
 
@@ -212,11 +220,9 @@ kw_status kw_dgemm_rowsharded_scratch(size_t n, size_t k, int panels, size_t* el
     if (panels < 1)
         return kw::usage("dgemm_rowsharded: panels must be >= 1");
     size_t total = 0;
-    if (n > 0) {
-        const size_t w = panel_width(n, panels);
-        for (size_t n0 = 0; n0 < n; n0 += w)
-            total += k * panel_ld(n - n0 < w ? n - n0 : w);
-    }
+    if (n > 0)
+        for (const auto& b : panel_bounds(n, panels))
+            total += k * panel_ld(b.second);
     *elems = total;
     return KW_OK;
 }
@@ -247,9 +253,9 @@ kw_status kw_dgemm_rowsharded(kw_comm c, kw_queue qh, size_t m_local, size_t n, 
         return kw::usage("dgemm_rowsharded: lda smaller than k");
     if (m_local > 0 && ldc < n)
         return kw::usage("dgemm_rowsharded: ldc smaller than n");
-    // Panel widths: multiples of the 128-column tile so every panel starts on a tile boundary.
-    const size_t w = panel_width(n, panels);
-    const int np = static_cast<int>(kw::ceil_div(n, w));
+    // Panels start on 128-column tile boundaries (panel_bounds).
+    const auto bounds = panel_bounds(n, panels);
+    const int np = static_cast<int>(bounds.size());
     kw::DeviceGuard g(q->device);
     kw_status st = ensure_events(c, np);
     if (st != KW_OK)
@@ -265,8 +271,13 @@ kw_status kw_dgemm_rowsharded(kw_comm c, kw_queue qh, size_t m_local, size_t n, 
         e = cudaStreamWaitEvent(q->comp2, c->start, 0);
     ncclResult_t r = ncclSuccess;
     size_t off = 0;
+    // One tile configuration for every panel launch of this rank — the one the whole m_local x n
+    // product would get: panel grids that overlap on the two compute streams then co-reside
+    // evenly (mixed 2- and 3-CTA/SM grids strand shared memory). Any paired configuration gives
+    // the same bits.
+    const int cfg = kw::dgemm_pick(m_local, n, k);
     for (int j = 0; j < np && e == cudaSuccess && r == ncclSuccess; ++j) {
-        const size_t n0 = static_cast<size_t>(j) * w, wj = n - n0 < w ? n - n0 : w;
+        const size_t n0 = bounds[j].first, wj = bounds[j].second;
         // k x wj panel at the Buffer pitch rule (leading dimension a multiple of 8 doubles): an
         // odd-width last panel stays TMA-addressable, so it runs the same kernel (and k grouping)
         // as the resident 1-GPU launch — a dense odd pitch would drop to the cp.async kernel.
@@ -286,7 +297,7 @@ kw_status kw_dgemm_rowsharded(kw_comm c, kw_queue qh, size_t m_local, size_t n, 
         if (e == cudaSuccess)
             e = cudaStreamWaitEvent(cs, c->panel_ready[j], 0);
         if (e == cudaSuccess && m_local > 0) {
-            st = kw::dgemm_device(cs, 128, m_local, wj, k, alpha, A, lda, panel, ldp, beta, C + n0, ldc);
+            st = kw::dgemm_device_cfg(cs, cfg, m_local, wj, k, alpha, A, lda, panel, ldp, beta, C + n0, ldc);
             if (st != KW_OK)
                 return kw::task_fail(q, kw::last_error());
         }

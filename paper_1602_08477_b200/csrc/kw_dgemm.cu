@@ -1880,6 +1880,23 @@ kw_status dgemm_device(cudaStream_t s, int tile, size_t m, size_t n, size_t k, d
         return KW_OK;
     return launch_tiled(s, tile, make_params(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc));
 }
+
+// The configuration the library would pick for the whole m x n x k problem (row-sharded: every
+// panel launch of a rank uses the rank's choice, so concurrent panel grids co-reside evenly).
+int dgemm_pick(size_t m, size_t n, size_t k)
+{
+    return pick_resident(make_params(m, n, k, 1.0, nullptr, k, nullptr, n, 0.0, nullptr, n));
+}
+
+kw_status dgemm_device_cfg(cudaStream_t s, int cfg, size_t m, size_t n, size_t k, double alpha, const double* A,
+                           size_t lda, const double* B, size_t ldb, double beta, double* C, size_t ldc)
+{
+    if (m == 0 || n == 0)
+        return KW_OK;
+    if (cfg < 0 || cfg >= kNumCfgs)
+        return kw::usage("dgemm: configuration index out of range");
+    return kCfgs[cfg].launch(s, make_params(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc));
+}
 } // namespace kw
 
 namespace {

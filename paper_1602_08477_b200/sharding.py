@@ -43,13 +43,13 @@ class Panel:
 
 
 def dgemm_panels(n: int, k: int, panels: int, tile: int = 128) -> list[Panel]:
-    """Column panels of B exactly as kw_dgemm_rowsharded lays them out."""
+    """Column panels of B exactly as kw_dgemm_rowsharded lays them out (kw_comm.cu panel_bounds):
+    equal tile-aligned widths of ceil(n / panels), each at leading dimension round8(width)."""
     if panels < 1:
         raise ValueError("panels must be >= 1")
     w = ceil_div(ceil_div(n, panels), tile) * tile
     out, off = [], 0
-    for j in range(ceil_div(n, w)):
-        n0 = j * w
+    for j, n0 in enumerate(range(0, n, w)):
         wj = min(w, n - n0)
         ld = ceil_div(wj, 8) * 8
         out.append(Panel(j, n0, wj, off, ld))

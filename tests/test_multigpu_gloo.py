@@ -115,3 +115,13 @@ def test_panel_layout_matches_the_c_abi_rule():
     assert [p.width for p in ps] == [384, 384, 233] and [p.ld for p in ps] == [384, 384, 240]
     assert [p.offset for p in ps] == [0, 200 * 384, 2 * 200 * 384]
     assert S.dgemm_panel_scratch(1001, 200, 3) == 200 * (384 + 384 + 240)
+    assert [p.width for p in S.dgemm_panels(100, 5, 4)] == [100]  # one tile: a single panel
+
+
+@pytest.mark.parametrize("n,k,panels", [(16384, 16384, 8), (1001, 200, 3), (127, 9, 2), (5000, 33, 7), (100, 5, 4)])
+def test_scratch_size_matches_the_c_abi(n, k, panels):
+    import ctypes as C
+    from paper_1602_08477_b200 import _lib as L
+    elems = C.c_size_t()
+    assert L.lib().kw_dgemm_rowsharded_scratch(n, k, panels, C.byref(elems)) == 0
+    assert elems.value == S.dgemm_panel_scratch(n, k, panels)
