@@ -374,7 +374,8 @@ __device__ __forceinline__ void wait_ready(const uint32_t* flag, uint32_t* abort
     }
 }
 
-template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int MIN_BLOCKS_ = 1, bool PAIRED_ = false>
+template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int MIN_BLOCKS_ = 1, bool PAIRED_ = false,
+          int GROUPS_ = 1>
 struct TmaCfg {
     static constexpr int BM = BM_, BN = BN_, BK = 16, WM = WM_, WN = WN_, STAGES = STAGES_;
     // PAIRED: k-slot map k = 8(t>>1) + 4(t&1) + 2((t>>1)^(s>>1)) + (s&1) puts the A fragments
@@ -382,10 +383,15 @@ struct TmaCfg {
     static constexpr bool PAIRED = PAIRED_;
     static constexpr int MIN_BLOCKS = MIN_BLOCKS_; // co-resident CTAs per SM
     static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
-    static constexpr int CONSUMERS = WARPS_M * WARPS_N;
-    // Consumer warps + one producer warpgroup (4 warps: one issues TMA, the others exit).
+    static constexpr int CONSUMERS = WARPS_M * WARPS_N; // per consumer group
+    // GROUPS > 1: that many independent consumer groups in one CTA, each with its own stage ring,
+    // producer lane and tile sequence (virtual CTAs sharing one SM's registers and one producer
+    // warpgroup — see the SPLIT notes).
+    static constexpr int GROUPS = GROUPS_;
+    static constexpr int TOTAL_CONSUMERS = CONSUMERS * GROUPS;
+    // Consumer warps + one producer warpgroup (4 warps: one issues TMA per group, the others exit).
     // setmaxnreg moves registers from the producer warpgroup to the consumers.
-    static constexpr int THREADS = 32 * (CONSUMERS + 4);
+    static constexpr int THREADS = 32 * (TOTAL_CONSUMERS + 4);
     static constexpr int PRODUCER_REGS = 40;
     // The CTA's register pool is fixed at launch: ptxas pins a setmaxnreg kernel to the
     // launch-bounds cap, floor(65536 / roundup(THREADS, 128) / 8) * 8 per thread. setmaxnreg.inc
@@ -393,18 +399,20 @@ struct TmaCfg {
     // warpgroup releases — asking for more deadlocks the CTA.
     static constexpr int LAUNCH_REGS_RAW = (65536 / MIN_BLOCKS / (((THREADS + 127) / 128) * 128)) / 8 * 8;
     static constexpr int LAUNCH_REGS = LAUNCH_REGS_RAW > 255 ? 255 : LAUNCH_REGS_RAW;
-    static constexpr int POOL_PER_LANE = LAUNCH_REGS * (CONSUMERS + 4);
-    static constexpr int CONSUMER_REGS_RAW = ((POOL_PER_LANE - 4 * PRODUCER_REGS) / CONSUMERS) / 8 * 8;
+    static constexpr int POOL_PER_LANE = LAUNCH_REGS * (TOTAL_CONSUMERS + 4);
+    static constexpr int CONSUMER_REGS_RAW = ((POOL_PER_LANE - 4 * PRODUCER_REGS) / TOTAL_CONSUMERS) / 8 * 8;
     static constexpr int CONSUMER_REGS = CONSUMER_REGS_RAW > 240 ? 240 : CONSUMER_REGS_RAW;
     // Small CTAs already get (nearly) 255 registers per thread: no redistribution needed.
     static constexpr bool REBALANCE = CONSUMER_REGS > LAUNCH_REGS;
-    static_assert(4 * PRODUCER_REGS + CONSUMERS * CONSUMER_REGS <= POOL_PER_LANE, "register pool overcommitted");
-    static_assert(CONSUMERS % 4 == 0, "consumer warps form whole warpgroups (setmaxnreg granularity)");
+    static_assert(4 * PRODUCER_REGS + TOTAL_CONSUMERS * CONSUMER_REGS <= POOL_PER_LANE, "register pool overcommitted");
+    static_assert(TOTAL_CONSUMERS % 4 == 0, "consumer warps form whole warpgroups (setmaxnreg granularity)");
+    static_assert(GROUPS >= 1 && GROUPS <= 4, "one producer warp per consumer group");
     static constexpr int MT = WM / 8, NT = WN / 8;
     static constexpr uint32_t A_BYTES = BM * 128; // BM rows of 16 doubles
     static constexpr uint32_t B_BYTES = BN * 128; // BN/16 boxes of 16 x 16 doubles (2 KB)
     static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr size_t SMEM = 1024 + static_cast<size_t>(STAGES) * STAGE_BYTES + 2 * STAGES * sizeof(uint64_t);
+    static constexpr size_t SMEM =
+        1024 + static_cast<size_t>(GROUPS) * STAGES * STAGE_BYTES + 2 * GROUPS * STAGES * sizeof(uint64_t);
     static_assert(WN % 16 == 0 && BN % 16 == 0 && BM <= 256, "tile shape");
 };
 
@@ -475,14 +483,24 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmParams p)
 {
     static_assert(!(STREAMED && SPLIT), "one tile-walk mode");
+    static_assert(!STREAMED || Cfg::GROUPS == 1, "streamed launches use one consumer group");
     extern __shared__ uint8_t smem_raw[];
     // 1 KiB alignment (128B-swizzled TMA boxes) by pointer arithmetic on the __shared__ array, not
     // through an integer cast: the compiler must still see a shared-space pointer, so fragment
     // loads compile to LDS. (Through uintptr_t they became generic LD.E — slower, and not ordered
     // before the empty-barrier arrive, so a refill could overwrite a stage still being read.)
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
-    uint64_t* empty = full + Cfg::STAGES;
+    uint64_t* full_all = reinterpret_cast<uint64_t*>(smem + Cfg::GROUPS * Cfg::STAGES * Cfg::STAGE_BYTES);
+    uint64_t* empty_all = full_all + Cfg::GROUPS * Cfg::STAGES;
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    // consumer group of this warp (producer warp TOTAL_CONSUMERS + g serves group g)
+    const int grp = Cfg::GROUPS == 1 ? 0 // a compile-time 0 keeps the one-group kernels' codegen
+                    : warp < Cfg::TOTAL_CONSUMERS ? warp / Cfg::CONSUMERS
+                    : (warp - Cfg::TOTAL_CONSUMERS < Cfg::GROUPS ? warp - Cfg::TOTAL_CONSUMERS : 0);
+    uint8_t* const ring = smem + grp * Cfg::STAGES * Cfg::STAGE_BYTES; // this group's stage ring
+    uint64_t* const full = full_all + grp * Cfg::STAGES;
+    uint64_t* const empty = empty_all + grp * Cfg::STAGES;
 
     // Grouped rasterisation: runs of 8 tile-rows sweep the tile-columns together. A CTA walks
     // tiles blockIdx.x, +gridDim.x, ... (one tile when the grid covers every tile; a persistent
@@ -495,7 +513,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     const int ktiles = (p.k + Cfg::BK - 1) / Cfg::BK;
     // SPLIT: this CTA's plan lives in shared memory (read per piece) — per-thread copies cost the
     // 2- and 3-CTA/SM configurations their register budget (spills).
-    __shared__ SplitRange sr;
+    __shared__ SplitRange sr_all[Cfg::GROUPS];
+    SplitRange& sr = sr_all[grp];
     // Tile origin and k-tile range [kt0, kt1) of work item `tile`; false = padding entry.
     auto origin = [&](int tile, int& bm, int& bn, int& kt0, int& kt1) {
         if constexpr (STREAMED) {
@@ -543,12 +562,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
         return true;
     };
 
-    const int tid = threadIdx.x;
-    const int warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
-        for (int s = 0; s < Cfg::STAGES; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], Cfg::CONSUMERS);
+        for (int s = 0; s < Cfg::GROUPS * Cfg::STAGES; ++s) {
+            mbar_init(&full_all[s], 1);
+            mbar_init(&empty_all[s], Cfg::CONSUMERS);
         }
         fence_mbar_init();
     }
@@ -558,15 +575,19 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     // SPLIT: this CTA's range index = its start-order ticket (see split_range)
-    int first = blockIdx.x, step = gridDim.x, ticket = 0;
+    // Virtual CTAs: consumer group g of CTA b is virtual CTA b * GROUPS + g of gridDim.x * GROUPS.
+    int first = blockIdx.x * Cfg::GROUPS + grp, step = gridDim.x * Cfg::GROUPS, ticket = 0;
     if constexpr (SPLIT) {
         __shared__ int s_ticket;
         if (tid == 0) {
-            s_ticket = static_cast<int>(atomicAdd(reinterpret_cast<unsigned long long*>(p.ready), 1ull) % gridDim.x);
-            sr = split_range(static_cast<long long>(p.tiles_m) * p.tiles_n, ktiles, gridDim.x, s_ticket, p.npr);
+            const int tk = static_cast<int>(atomicAdd(reinterpret_cast<unsigned long long*>(p.ready), 1ull) % gridDim.x);
+            s_ticket = tk;
+            for (int g2 = 0; g2 < Cfg::GROUPS; ++g2)
+                sr_all[g2] = split_range(static_cast<long long>(p.tiles_m) * p.tiles_n, ktiles,
+                                         static_cast<long long>(gridDim.x) * Cfg::GROUPS, tk * Cfg::GROUPS + g2, p.npr);
         }
         __syncthreads();
-        ticket = s_ticket;
+        ticket = s_ticket * Cfg::GROUPS + grp; // this group's virtual ticket
         ntiles = sr.ndp + sr.head + sr.nfull + sr.tail;
         first = 0;
         step = 1;
@@ -579,14 +600,14 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     // so the consumers keep the registers the split bookkeeping costs (2- and 3-CTA/SM tiles
     // spilled with 40).
     constexpr int PREGS = (SPLIT && Cfg::MIN_BLOCKS > 1) ? 24 : Cfg::PRODUCER_REGS;
-    constexpr int CREGS_RAW = ((Cfg::POOL_PER_LANE - 4 * PREGS) / Cfg::CONSUMERS) / 8 * 8;
+    constexpr int CREGS_RAW = ((Cfg::POOL_PER_LANE - 4 * PREGS) / Cfg::TOTAL_CONSUMERS) / 8 * 8;
     constexpr int CREGS = CREGS_RAW > 240 ? 240 : CREGS_RAW;
-    static_assert(4 * PREGS + Cfg::CONSUMERS * CREGS <= Cfg::POOL_PER_LANE, "register pool overcommitted");
-    if (warp >= Cfg::CONSUMERS) {
+    static_assert(4 * PREGS + Cfg::TOTAL_CONSUMERS * CREGS <= Cfg::POOL_PER_LANE, "register pool overcommitted");
+    if (warp >= Cfg::TOTAL_CONSUMERS) {
         // ---------------- producer warpgroup ----------------
         if constexpr (Cfg::REBALANCE)
             asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PREGS));
-        if (warp == Cfg::CONSUMERS && lane == 0) {
+        if (warp - Cfg::TOTAL_CONSUMERS < Cfg::GROUPS && lane == 0) {
             tma_prefetch_desc(&tmA);
             tma_prefetch_desc(&tmB);
             int it = 0; // k-tile iteration counter across this CTA's tiles (ring position)
@@ -623,7 +644,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
                                        abort);
                     }
                     mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
-                    const uint32_t sa = smem_u32(smem + s * Cfg::STAGE_BYTES);
+                    const uint32_t sa = smem_u32(ring + s * Cfg::STAGE_BYTES);
                     tma_load_2d(sa, &tmA, kt * Cfg::BK, bm, &full[s]);
 #pragma unroll
                     for (int j = 0; j < Cfg::BN / 16; ++j)
@@ -637,8 +658,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     // ---------------- consumers ----------------
     if constexpr (Cfg::REBALANCE)
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(CREGS));
-    const int wm = (warp / Cfg::WARPS_N) * Cfg::WM;
-    const int wn = (warp % Cfg::WARPS_N) * Cfg::WN;
+    const int lw = warp - grp * Cfg::CONSUMERS; // warp within its consumer group
+    const int wm = (lw / Cfg::WARPS_N) * Cfg::WM;
+    const int wn = (lw % Cfg::WARPS_N) * Cfg::WN;
     const int g = lane >> 2, t = lane & 3;
 
 
@@ -675,7 +697,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     double2* park = nullptr;
     if constexpr (STREAMED) {
         const size_t tid_tile = static_cast<size_t>(bm / Cfg::BM) * p.tiles_n + bn / Cfg::BN;
-        park = reinterpret_cast<double2*>(p.partial) + (tid_tile * Cfg::CONSUMERS + warp) * (Cfg::MT * Cfg::NT) * 32 + lane;
+        park = reinterpret_cast<double2*>(p.partial) + (tid_tile * Cfg::CONSUMERS + lw) * (Cfg::MT * Cfg::NT) * 32 + lane;
     }
     // SPLIT: a tail piece reloads slot ticket - 1 (its head ran on the previous ticket), a head
     // piece parks into slot ticket.
@@ -683,7 +705,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     if constexpr (SPLIT) {
         const int slot = kt0 > 0 ? ticket - 1 : ticket;
         park = reinterpret_cast<double2*>(p.partial) +
-               (static_cast<size_t>(slot) * Cfg::CONSUMERS + warp) * (Cfg::MT * Cfg::NT) * 32 + lane;
+               (static_cast<size_t>(slot) * Cfg::CONSUMERS + lw) * (Cfg::MT * Cfg::NT) * 32 + lane;
     }
     double acc[Cfg::MT][Cfg::NT][2];
 #pragma unroll
@@ -694,7 +716,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     if constexpr (SPLIT) {
         if (kt0 > 0) {
             // wait for the head piece's park (flag of slot ticket - 1, this warp), bounded
-            uint32_t* f = split_flags + (ticket - 1) * Cfg::CONSUMERS + warp;
+            uint32_t* f = split_flags + (ticket - 1) * Cfg::CONSUMERS + lw;
             for (uint32_t spins = 0; ld_acquire_gpu(f) == 0; ++spins) {
                 if (spins > (1u << 25)) { // ~30 s: never by construction (split_range)
                     split_abort(p.ready, lane);
@@ -784,12 +806,12 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
         if (nkt > 0) {
             const int s0 = it0 % Cfg::STAGES;
             mbar_wait(&full[s0], static_cast<uint32_t>(it0 / Cfg::STAGES) & 1u);
-            load_a2(smem + s0 * Cfg::STAGE_BYTES, 0, a2[0]);
-            load_b(smem + s0 * Cfg::STAGE_BYTES, 0, bf[0]);
+            load_a2(ring + s0 * Cfg::STAGE_BYTES, 0, a2[0]);
+            load_b(ring + s0 * Cfg::STAGE_BYTES, 0, bf[0]);
         }
         for (int kt = 0; kt < nkt; ++kt) {
             const int s = (it0 + kt) % Cfg::STAGES;
-            const uint8_t* sa = smem + s * Cfg::STAGE_BYTES;
+            const uint8_t* sa = ring + s * Cfg::STAGE_BYTES;
             const uint8_t* sa2 = sa;
 #pragma unroll
             for (int ks = 0; ks < 4; ++ks) {
@@ -804,7 +826,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
                     if (kt + 1 < nkt) {
                         const int s2 = (it0 + kt + 1) % Cfg::STAGES;
                         mbar_wait(&full[s2], static_cast<uint32_t>((it0 + kt + 1) / Cfg::STAGES) & 1u);
-                        sa2 = smem + s2 * Cfg::STAGE_BYTES;
+                        sa2 = ring + s2 * Cfg::STAGE_BYTES;
                         load_b(sa2, 0, bf[bn2]);
                         load_a2(sa2, 0, a2[0]); // a2[0] is idle during k-steps 2 and 3
                     }
@@ -834,11 +856,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     if (nkt > 0) {
         const int s0 = it0 % Cfg::STAGES;
         mbar_wait(&full[s0], static_cast<uint32_t>(it0 / Cfg::STAGES) & 1u);
-        load_frags(smem + s0 * Cfg::STAGE_BYTES, 0, af[0], bf[0]);
+        load_frags(ring + s0 * Cfg::STAGE_BYTES, 0, af[0], bf[0]);
     }
     for (int kt = 0; kt < nkt; ++kt) {
         const int s = (it0 + kt) % Cfg::STAGES;
-        const uint8_t* sa = smem + s * Cfg::STAGE_BYTES;
+        const uint8_t* sa = ring + s * Cfg::STAGE_BYTES;
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {
             const int cur = ks & 1, nxt = cur ^ 1;
@@ -850,7 +872,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
                 if (kt + 1 < nkt) {
                     const int s2 = (it0 + kt + 1) % Cfg::STAGES;
                     mbar_wait(&full[s2], static_cast<uint32_t>((it0 + kt + 1) / Cfg::STAGES) & 1u);
-                    load_frags(smem + s2 * Cfg::STAGE_BYTES, 0, af[nxt], bf[nxt]);
+                    load_frags(ring + s2 * Cfg::STAGE_BYTES, 0, af[nxt], bf[nxt]);
                 }
             }
 #pragma unroll
@@ -880,7 +902,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
             __threadfence();
             __syncwarp();
             if (lane == 0)
-                asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(split_flags + ticket * Cfg::CONSUMERS + warp),
+                asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(split_flags + ticket * Cfg::CONSUMERS + lw),
                              "r"(1u)
                              : "memory");
             continue;
@@ -1537,7 +1559,8 @@ kw_status launch_tma(cudaStream_t s, const GemmParams& p0)
     if (st != KW_OK)
         return st;
     const long long resident = static_cast<long long>(sm_count()) * Cfg::MIN_BLOCKS;
-    const unsigned grid = static_cast<unsigned>(PERSISTENT && tiles > resident ? resident : tiles);
+    const long long ctas = (tiles + Cfg::GROUPS - 1) / Cfg::GROUPS; // a CTA serves GROUPS tiles at a time
+    const unsigned grid = static_cast<unsigned>(PERSISTENT && ctas > resident ? resident : ctas);
     if constexpr (STREAMED)
         dgemm_tma_kernel<Cfg, true, false><<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(ma, mb, p);
     else
@@ -1560,6 +1583,9 @@ using Split64w8 = TmaCfg<64, 64, 32, 16, 8, 1, true>;       // 18: SPLIT, 8 cons
 using Split64w4 = TmaCfg<64, 64, 32, 32, 8, 1, true>;       // 19: SPLIT, 4 consumers of 32x32
 using Split64x128w8 = TmaCfg<64, 128, 32, 32, 6, 1, true>;  // 20: SPLIT, 8 consumers of 32x32
 using Split64w8t = TmaCfg<64, 64, 16, 32, 8, 1, true>;      // 23: SPLIT, 8 consumers of 16x32
+// 25 / 26: two consumer groups of config 16's geometry (64 x 128 tiles, 4 warps of 64 x 32) in one
+// CTA per SM, each with its own 4-stage ring and producer lane — SPLIT walk / data-parallel.
+using Pair64x128 = TmaCfg<64, 128, 64, 32, 4, 1, true, 2>;
 // (16 consumer warps of 32x32 were measured out: 104 registers per consumer spill.)
 
 // ---- SPLIT launches: per-stream scratch (ticket, abort pointer, flags, park slots) ----------
@@ -1654,17 +1680,18 @@ kw_status launch_split(cudaStream_t s, const GemmParams& p0)
     p.tiles_n = static_cast<int>(kw::ceil_div(p.n, Cfg::BN));
     const long long tiles = static_cast<long long>(p.tiles_m) * p.tiles_n;
     const long long G = static_cast<long long>(sm_count()) * Cfg::MIN_BLOCKS; // every CTA resident
+    const long long VG = G * Cfg::GROUPS;                                      // virtual CTAs
     const long long ktiles = kw::ceil_div(p.k, Cfg::BK);
     // every range must span at least one whole tile (a tile is then split at most once)
-    if (tiles < G || ktiles < 2 || tiles * ktiles > INT_MAX || !tma_eligible(p))
+    if (tiles < VG || ktiles < 2 || tiles * ktiles > INT_MAX || !tma_eligible(p))
         return launch_tma<Tma64x64x3p>(s, p0);
     CUtensorMap ma, mb;
     if (!make_map(&ma, p.a, p.m, p.k, p.lda, Cfg::BM) || !make_map(&mb, p.b, p.k, p.n, p.ldb, 16))
         return launch_dmma<Cfg128>(s, p0);
     uint32_t* flags = nullptr;
     double* park = nullptr;
-    kw_status st = split_scratch(s, G, 4 + static_cast<size_t>(G) * Cfg::CONSUMERS,
-                                 static_cast<size_t>(G) * Cfg::CONSUMERS * Cfg::MT * Cfg::NT * 32 * sizeof(double2), &flags,
+    kw_status st = split_scratch(s, G, 4 + static_cast<size_t>(VG) * Cfg::CONSUMERS,
+                                 static_cast<size_t>(VG) * Cfg::CONSUMERS * Cfg::MT * Cfg::NT * 32 * sizeof(double2), &flags,
                                  &park);
     if (st != KW_OK)
         return st;
@@ -1727,6 +1754,10 @@ const CfgInfo kCfgs[] = {
      launch_split<Split64w8t>},
     {Tma128p::BM, Tma128p::BN, Tma128p::BK, Tma128p::THREADS, Tma128p::STAGES,
      launch_split<Tma128p>}, // 24: SPLIT of config 14 (128 x 128, 8 consumers of 64 x 32, 1 CTA/SM)
+    {Pair64x128::BM, Pair64x128::BN, Pair64x128::BK, Pair64x128::THREADS, Pair64x128::STAGES,
+     launch_split<Pair64x128>}, // 25
+    {Pair64x128::BM, Pair64x128::BN, Pair64x128::BK, Pair64x128::THREADS, Pair64x128::STAGES,
+     launch_tma<Pair64x128>}, // 26
 };
 constexpr int kNumCfgs = sizeof(kCfgs) / sizeof(kCfgs[0]);
 // Tile choice for the GPU back-end. The tile work division (gemmTiledWorkDiv) is the coverage
@@ -1756,7 +1787,7 @@ int pick_config(const GemmParams& p)
 // output (1024^3: 2 of 1.73 tiles, 0.865 -> split 18 at 30.2 vs 26.9 TFLOP/s; 1280^3: 0.90 ->
 // split 20 at 31.9 vs 28.7; profiles/dgemm_split_sweep_r02.txt). Split 20 (64 x 128 tiles, 8
 // warps of 32 x 32) where it still gives every SM a tile, else split 18 (64 x 64, 8 of 32 x 16).
-constexpr int kCfgSplit64 = 18, kCfgSplit128 = 20;
+constexpr int kCfgSplit64 = 18, kCfgSplit128 = 20, kCfgSplitPair = 25;
 int pick_resident(const GemmParams& p)
 {
     const double sms = sm_count();
@@ -1767,6 +1798,13 @@ int pick_resident(const GemmParams& p)
     const long long ktiles = (p.k + 15) / 16;
     if (std::max(q16, q17) < 0.93 && t17 >= static_cast<long long>(sms) && ktiles >= 2 && tma_eligible(p))
         return t16 >= static_cast<long long>(sms) ? kCfgSplit128 : kCfgSplit64;
+    // Mid-size outputs (2 to 16 tiles of 64 x 128 per consumer group): the two-group SPLIT config
+    // (config 16's geometry twice in one CTA, equal k-tile ranges) — 3072^3 34.7 vs 34.1,
+    // 2560^3 34.2 vs 34.1, 4096^3 35.1 vs 35.0 TFLOP/s; beyond, the data-parallel grid's waves are
+    // many and it stays ahead (profiles/dgemm_split_sweep_r02.txt).
+    if (t16 >= 2 * static_cast<long long>(sms) && t16 <= 32 * static_cast<long long>(sms) && ktiles >= 2 &&
+        tma_eligible(p))
+        return kCfgSplitPair;
     return pick_config(p);
 }
 
@@ -1881,11 +1919,13 @@ kw_status dgemm_device(cudaStream_t s, int tile, size_t m, size_t n, size_t k, d
     return launch_tiled(s, tile, make_params(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc));
 }
 
-// The configuration the library would pick for the whole m x n x k problem (row-sharded: every
-// panel launch of a rank uses the rank's choice, so concurrent panel grids co-reside evenly).
+// The data-parallel configuration for the whole m x n x k problem (row-sharded: every panel
+// launch of a rank uses it, so panel grids on the two compute streams co-reside evenly and fill
+// each other's tails; one-CTA-per-SM SPLIT grids cannot overlap — measured 33.6 vs 34.6 TFLOP/s
+// for a 2048-row rank, profiles/rowshard_rank_probe_r02.txt).
 int dgemm_pick(size_t m, size_t n, size_t k)
 {
-    return pick_resident(make_params(m, n, k, 1.0, nullptr, k, nullptr, n, 0.0, nullptr, n));
+    return pick_config(make_params(m, n, k, 1.0, nullptr, k, nullptr, n, 0.0, nullptr, n));
 }
 
 kw_status dgemm_device_cfg(cudaStream_t s, int cfg, size_t m, size_t n, size_t k, double alpha, const double* A,
