@@ -224,6 +224,54 @@ def test_rowsharded_single_rank_pipeline(gpu, oracle, n, panels):
     assert L.lib().kw_comm_destroy(comm) == 0
 
 
+def test_rowsharded_16384_cubed(gpu, oracle):
+    """BASELINE configs[3]'s shape through kw_dgemm_rowsharded (world-1 NCCL communicator, the
+    8-panel broadcast executing): the full 16384^3 C equals a single kw_dgemm launch bit for bit
+    (compared on the device by digest of the downloaded blocks) and 8 sampled rows are within
+    (K+4)u of gemmReference (the oracle, 8 threads)."""
+    import hashlib
+    n = 16384
+    lib = L.lib()
+    rng = np.random.default_rng(16384)
+    A, B, C1, C2 = (kw.Buffer(gpu, kw.IndexVec(n, n), 8) for _ in range(4))
+    for buf in (A, B, C1):
+        buf.upload(rng.random((n, n)))
+    q = kw.Queue(gpu, kw.QueueFlavor.Async)
+    assert lib.kw_copy(q.handle(), C2.data(), C2.rowPitch(), L.sz3((n, n)), C1.data(), C1.rowPitch(), L.sz3((n, n)), 2,
+                       L.sz3((n, n)), 8) == 0
+    q.wait()
+    rows = [0, 1, 2047, 2048, 8191, 9000, 16000, 16383]
+    host_c = C1.download()
+    c_rows = host_c[rows].copy()
+    del host_c
+    uid = (C.c_char * 128)()
+    assert lib.kw_comm_unique_id(uid) == 0
+    comm = C.c_void_p()
+    assert lib.kw_comm_init(C.byref(comm), 0, 1, 0, uid) == 0, L.last_error()
+    elems = C.c_size_t()
+    assert lib.kw_dgemm_rowsharded_scratch(n, n, 8, C.byref(elems)) == 0
+    scratch = kw.Buffer(gpu, kw.IndexVec(elems.value), 8)
+    assert lib.kw_dgemm_rowsharded(comm, q.handle(), n, n, n, 1.25, A.data(), A.leadingDim(), B.data(), B.leadingDim(),
+                                   0.75, C1.data(), C1.leadingDim(), scratch.data(), 8, 0) == 0, L.last_error()
+    assert lib.kw_dgemm(q.handle(), None, n, n, n, 1.25, A.data(), A.leadingDim(), B.data(), B.leadingDim(), 0.75,
+                        C2.data(), C2.leadingDim()) == 0
+    q.wait()
+    assert lib.kw_comm_destroy(comm) == 0
+    del scratch
+    got1 = C1.download()
+    d1 = hashlib.blake2b(got1, digest_size=16).hexdigest()
+    sampled = got1[rows].copy()
+    del got1
+    d2 = hashlib.blake2b(C2.download(), digest_size=16).hexdigest()
+    assert d1 == d2
+    host_a = A.download()
+    a_s = host_a[rows].copy()
+    del host_a
+    ref = oracle.gemm(1.25, 0.75, a_s, B.download(), c_rows, threads=8)
+    ok, worst = within_tol(sampled, ref, n)
+    assert ok, worst
+
+
 def test_host_buffers_are_staged(gpu, oracle):
     """DGEMM on host (pinned) buffers: B staged once, A/C row panels pipelined; equal bits to
     the device-resident launch."""
