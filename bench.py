@@ -204,7 +204,8 @@ class Dist:
         if self.world > 1:
             import torch
             import torch.distributed as dist
-            torch.cuda.set_device(self.local)
+            if torch.cuda.is_available():
+                torch.cuda.set_device(self.local)
             if backend == "nccl":
                 dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
             else:
@@ -223,6 +224,20 @@ class Dist:
                 self.dist.barrier(device_ids=[self.local])
             else:
                 self.dist.barrier()
+
+    def quiet_wait_for_rank0(self, key: str):
+        """Ranks > 0 block in the rendezvous store (a socket wait, no spinning host thread) until
+        rank 0 calls it with the same key after its CPU-side work — so the CPU baseline rank 0
+        times is not competing with N - 1 ranks spinning in a collective on the same host."""
+        if self.world == 1:
+            return
+        store = self.dist.distributed_c10d._get_default_store()
+        if self.rank == 0:
+            store.set(key, "1")
+        else:
+            import datetime
+            store.wait([key], datetime.timedelta(seconds=1800))
+        self.barrier()
 
     def max(self, v: float) -> float:
         if self.world == 1:
@@ -449,7 +464,7 @@ def run_ours(args, dist: Dist) -> dict:
         cb, parity = cpu_baseline_axpy(alpha, gathered, applied, args.warmup)
         out["cpu_baseline"] = cb
         out["parity"] = parity
-    dist.barrier()  # the other ranks wait here while rank 0 runs the CPU reference
+    dist.quiet_wait_for_rank0("kw-axpy-cpu-baseline-done")  # rank 0 ran the CPU reference meanwhile
 
     # ---- secondary: DGEMM. Guarded: neither an exception nor a hang in this leg (an N > 1
     # communicator that never forms, say) may cost the headline line above — a watchdog prints
@@ -678,7 +693,7 @@ def run_dgemm_rowsharded(args, dist, kw, L, lib, dev, q, timed, res) -> dict:
         res["cpu_baseline"], res["parity"] = dgemm_rows_check(kw, dev, q, B, rows, gpu_rows, size, alpha, beta,
                                                               (seed_a, seed_c), args.no_cpu)
     del A, Cb, B, panels
-    dist.barrier()
+    dist.quiet_wait_for_rank0("kw-dgemm-cpu-check-done")
     return res
 
 
