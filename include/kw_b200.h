@@ -268,6 +268,11 @@ KW_EXPORT kw_status kw_dgemm_rowsharded_scratch(size_t n, size_t k, int panels, 
 KW_EXPORT kw_status kw_dgemm_split_plan(long long tiles, long long ktiles, long long ctas, long long cta,
                                         long long dp_tiles, int out[11]);
 
+/* Measurement: SPLIT DGEMM launches after this call stamp their timeline into `device_buffer`
+ * (40 u64 per virtual CTA: %globaltimer at start, SM id, start/end of up to 18 pieces, end);
+ * NULL turns it off. Only a library compiled with -DKW_SPLIT_TRACE stamps (a no-op otherwise). */
+KW_EXPORT kw_status kw_dgemm_split_trace(void* device_buffer);
+
 /* ---- measurement helpers (bench / tests) --------------------------------------------------- */
 /* Writes a device scratch buffer larger than L2 (flush between timed iterations). */
 KW_EXPORT kw_status kw_l2_flush(kw_queue q);

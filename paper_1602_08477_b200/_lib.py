@@ -87,6 +87,7 @@ SIGNATURES = {
                                  vp, size_t, vp, C.c_int, C.c_int]),
     "kw_dgemm_rowsharded_scratch": (st, [size_t, size_t, C.c_int, C.POINTER(size_t)]),
     "kw_l2_flush": (st, [vp]),
+    "kw_dgemm_split_trace": (st, [vp]),
     "kw_dgemm_split_plan": (st, [C.c_longlong, C.c_longlong, C.c_longlong, C.c_longlong, C.c_longlong,
                                  C.POINTER(C.c_int)]),
     "kw_launch_count": (C.c_uint64, []),

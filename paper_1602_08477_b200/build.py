@@ -22,6 +22,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
               "-Xptxas", "-v", f"-I{INCLUDE}", f"-I{CSRC}"]
+# measurement builds only (e.g. "-DKW_SPLIT_TRACE"): appended to every library compile
+NVCC_FLAGS += os.environ.get("KW_EXTRA_NVCC_FLAGS", "").split()
 SOURCES = ["kw_runtime.cu", "kw_axpy.cu", "kw_dgemm.cu", "kw_dgemm_e2e.cu", "kw_comm.cu"]
 
 

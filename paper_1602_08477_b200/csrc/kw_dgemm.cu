@@ -658,6 +658,31 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     // ---------------- consumers ----------------
     if constexpr (Cfg::REBALANCE)
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(CREGS));
+    // SPLIT timeline trace (kw_dgemm_split_trace; p.tile_list is free in SPLIT mode): per virtual
+    // CTA 40 u64 — start, SM id, (piece start, piece end) x 18, end — written by its first warp.
+    // Compiled in only with -DKW_SPLIT_TRACE (the bookkeeping costs the two-group config spills).
+#if defined(KW_SPLIT_TRACE)
+    uint64_t* trace = nullptr;
+    if constexpr (SPLIT) {
+        if (p.tile_list && warp % Cfg::CONSUMERS == 0 && lane == 0)
+            trace = reinterpret_cast<uint64_t*>(const_cast<int4*>(p.tile_list)) + static_cast<size_t>(ticket) * 40;
+    }
+    auto stamp = [&](int slot) {
+        if (trace && slot < 40) {
+            uint64_t t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            trace[slot] = t;
+        }
+    };
+    stamp(0);
+    if (trace) {
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        trace[1] = smid;
+    }
+#else
+    auto stamp = [](int) {};
+#endif
     const int lw = warp - grp * Cfg::CONSUMERS; // warp within its consumer group
     const int wm = (lw / Cfg::WARPS_N) * Cfg::WM;
     const int wn = (lw % Cfg::WARPS_N) * Cfg::WN;
@@ -760,6 +785,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
             }
         }
     }
+    stamp(2 + 2 * tile);
     if constexpr (STREAMED) {
         if (kt0 > 0) {
 #pragma unroll
@@ -905,6 +931,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
                 asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(split_flags + ticket * Cfg::CONSUMERS + lw),
                              "r"(1u)
                              : "memory");
+            stamp(3 + 2 * tile);
             continue;
         }
     }
@@ -967,7 +994,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
             atomicAdd(done + (bm / p.panel_rows) * p.npc + bn / p.panel_cols, 1u);
         }
     }
+    stamp(3 + 2 * tile);
     } // tile loop
+    stamp(39);
 }
 
 using PFN_encodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -1670,6 +1699,11 @@ kw_status split_scratch(cudaStream_t s, long long grid, size_t flag_words, size_
     return KW_OK;
 }
 
+// Debug/measurement: a device buffer the next SPLIT launches stamp their timeline into
+// (kw_dgemm_split_trace; 40 u64 per virtual CTA), or nullptr. Only a library built with
+// -DKW_SPLIT_TRACE (KW_EXTRA_NVCC_FLAGS) stamps.
+std::atomic<void*> g_split_trace{nullptr};
+
 // One persistent CTA per SM over equal (tile, k-tile) ranges (dgemm_tma_kernel SPLIT).
 template <class Cfg>
 kw_status launch_split(cudaStream_t s, const GemmParams& p0)
@@ -1697,7 +1731,11 @@ kw_status launch_split(cudaStream_t s, const GemmParams& p0)
         return st;
     p.ready = flags;
     p.partial = park;
+#if defined(KW_SPLIT_TRACE)
+    p.tile_list = static_cast<const int4*>(g_split_trace.load(std::memory_order_relaxed)); // trace or null
+#else
     p.tile_list = nullptr;
+#endif
     p.panel_rows = dgemm_group();
     static const long long dp_env = [] { // KW_SPLIT_DP_TILES: data-parallel tile count override (sweeps)
         const char* e = std::getenv("KW_SPLIT_DP_TILES");
@@ -2064,6 +2102,12 @@ kw_status kw_dgemm_bitwise(kw_queue qh, const kw_workdiv* wd, size_t m, size_t n
 }
 
 int kw_dgemm_config_count(void) { return kNumCfgs; }
+
+kw_status kw_dgemm_split_trace(void* device_buffer)
+{
+    g_split_trace.store(device_buffer, std::memory_order_relaxed);
+    return KW_OK;
+}
 
 kw_status kw_dgemm_split_plan(long long tiles, long long ktiles, long long ctas, long long cta, long long dp_tiles,
                               int out[11])
