@@ -11,6 +11,8 @@ from pathlib import Path
 
 _PKG = Path(__file__).resolve().parent
 LIB_PATH = _PKG / "libkw_b200.so"
+if os.environ.get("KW_LIB_PATH"):  # A/B measurements against another build of the same library
+    LIB_PATH = Path(os.environ["KW_LIB_PATH"])
 
 KW_OK, KW_USAGE, KW_RESOURCE, KW_TASK = 0, 1, 2, 3
 KW_QUEUE_SYNC, KW_QUEUE_ASYNC = 0, 1

@@ -948,6 +948,12 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
         }
     }
 
+    // Epilogue, one 8-row block of the warp tile at a time: the block's C values are read before
+    // any of them is written — interleaving load / compute / store serialises on the stores'
+    // possible aliasing with the later loads (one L2 round trip per element pair, ~6 us per
+    // 64 x 128 tile with the split timeline). A whole-tile batch would not fit the registers next
+    // to the accumulators. (PREFETCH_C configurations read C at tile start instead.)
+    constexpr int EB = Cfg::NT; // batch = the whole 8-row block (narrower batches measured no better)
 #pragma unroll
     for (int i = 0; i < Cfg::MT; ++i) {
         const int row = bm + wm + i * 8 + g;
@@ -955,34 +961,36 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
             continue;
         double* crow = p.c + row * p.ldc;
 #pragma unroll
-        for (int j = 0; j < Cfg::NT; ++j) {
+        for (int j0 = 0; j0 < Cfg::NT; j0 += EB) {
+        double2 old[EB];
+#pragma unroll
+        for (int jj = 0; jj < EB; ++jj) {
+            const int j = j0 + jj;
             const int col = bn + wn + j * 8 + 2 * t;
-            if constexpr (PREFETCH_C) {
-                const double2 old = cpre[i][j];
-                const double x = __dadd_rn(__dmul_rn(p.alpha, acc[i][j][0]), __dmul_rn(p.beta, old.x));
-                const double y = __dadd_rn(__dmul_rn(p.alpha, acc[i][j][1]), __dmul_rn(p.beta, old.y));
-                if (c_vec && col + 1 < p.n)
-                    *reinterpret_cast<double2*>(crow + col) = make_double2(x, y);
-                else {
-                    if (col < p.n)
-                        crow[col] = x;
-                    if (col + 1 < p.n)
-                        crow[col + 1] = y;
-                }
+            if constexpr (PREFETCH_C)
+                old[jj] = cpre[i][j];
+            else if (c_vec && col + 1 < p.n)
+                old[jj] = *reinterpret_cast<const double2*>(crow + col);
+            else {
+                old[jj].x = col < p.n ? crow[col] : 0.0;
+                old[jj].y = col + 1 < p.n ? crow[col + 1] : 0.0;
             }
-            else if (c_vec && col + 1 < p.n) {
-                double2 old = *reinterpret_cast<const double2*>(crow + col);
-                double2 out;
-                out.x = __dadd_rn(__dmul_rn(p.alpha, acc[i][j][0]), __dmul_rn(p.beta, old.x));
-                out.y = __dadd_rn(__dmul_rn(p.alpha, acc[i][j][1]), __dmul_rn(p.beta, old.y));
-                *reinterpret_cast<double2*>(crow + col) = out;
-            }
+        }
+#pragma unroll
+        for (int jj = 0; jj < EB; ++jj) {
+            const int j = j0 + jj;
+            const int col = bn + wn + j * 8 + 2 * t;
+            const double x = __dadd_rn(__dmul_rn(p.alpha, acc[i][j][0]), __dmul_rn(p.beta, old[jj].x));
+            const double y = __dadd_rn(__dmul_rn(p.alpha, acc[i][j][1]), __dmul_rn(p.beta, old[jj].y));
+            if (c_vec && col + 1 < p.n)
+                *reinterpret_cast<double2*>(crow + col) = make_double2(x, y);
             else {
                 if (col < p.n)
-                    crow[col] = __dadd_rn(__dmul_rn(p.alpha, acc[i][j][0]), __dmul_rn(p.beta, crow[col]));
+                    crow[col] = x;
                 if (col + 1 < p.n)
-                    crow[col + 1] = __dadd_rn(__dmul_rn(p.alpha, acc[i][j][1]), __dmul_rn(p.beta, crow[col + 1]));
+                    crow[col + 1] = y;
             }
+        }
         }
     }
     if constexpr (STREAMED) {

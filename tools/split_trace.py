@@ -64,6 +64,17 @@ def main():
           f"max {max(busy) / 1e3:.1f}")
     print(f"  gaps between pieces (incl. tail waits): median {statistics.median(gaps) / 1e3:.2f} us, "
           f"max {max(gaps) / 1e3:.2f} us")
+    # busy time and end per SM (both groups of an SM summed / max), to see whether the spread is
+    # per SM (placement) or per CTA
+    per_sm = {}
+    for r, b, e in zip(rows, busy, ends):
+        sm = int(r[1])
+        per_sm.setdefault(sm, []).append((b, e))
+    line = []
+    for sm in sorted(per_sm):
+        bs = per_sm[sm]
+        line.append(f"{sm}:{max(x[1] for x in bs) / 1e3:.0f}")
+    print("  end per SM (sm:us): " + " ".join(line))
     # per-piece durations by kind for the median CTA
     r = rows[len(rows) // 2]
     pieces = []
