@@ -1844,12 +1844,13 @@ int pick_resident(const GemmParams& p)
     const long long ktiles = (p.k + 15) / 16;
     if (std::max(q16, q17) < 0.93 && t17 >= static_cast<long long>(sms) && ktiles >= 2 && tma_eligible(p))
         return t16 >= static_cast<long long>(sms) ? kCfgSplit128 : kCfgSplit64;
-    // Mid-size outputs (2 to 16 tiles of 64 x 128 per consumer group): the two-group SPLIT config
-    // (config 16's geometry twice in one CTA, equal k-tile ranges) — 3072^3 34.7 vs 34.1,
-    // 2560^3 34.2 vs 34.1, 4096^3 35.1 vs 35.0 TFLOP/s; beyond, the data-parallel grid's waves are
-    // many and it stays ahead (profiles/dgemm_split_sweep_r02.txt).
-    if (t16 >= 2 * static_cast<long long>(sms) && t16 <= 32 * static_cast<long long>(sms) && ktiles >= 2 &&
-        tma_eligible(p))
+    // Mid-size outputs (2 to 16 tiles of 64 x 128 per consumer group) whose 64 x 128 grid leaves a
+    // partial last wave: the two-group SPLIT config (config 16's geometry twice in one CTA, equal
+    // k-tile ranges) — 2048^3 34.3 vs 34.0, 3072^3 35.0 vs 34.4, 3584^3 35.1 vs 34.2, 6144^3
+    // 35.4 vs 35.1 TFLOP/s; where config 16's waves come out whole (4096^3: 6.92 of 7) or are many
+    // (>= 7168^3) the data-parallel grid stays ahead (profiles/dgemm_split_sweep_r02.txt).
+    if (t16 >= 2 * static_cast<long long>(sms) && t16 <= 32 * static_cast<long long>(sms) && q16 < 0.985 &&
+        ktiles >= 2 && tma_eligible(p))
         return kCfgSplitPair;
     return pick_config(p);
 }
