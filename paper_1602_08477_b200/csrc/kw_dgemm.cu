@@ -1429,11 +1429,17 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         if (row >= p.m)
             continue;
         double* crow = p.c + row * p.ldc;
+        double old[Cfg::NJ]; // the row's C values read before any is written (see the DMMA kernel)
+#pragma unroll
+        for (int j = 0; j < Cfg::NJ; ++j) {
+            const int col = bn + lane + 32 * j;
+            old[j] = col < p.n ? crow[col] : 0.0;
+        }
 #pragma unroll
         for (int j = 0; j < Cfg::NJ; ++j) {
             const int col = bn + lane + 32 * j;
             if (col < p.n)
-                crow[col] = __dadd_rn(__dmul_rn(p.alpha, acc[i][j]), __dmul_rn(p.beta, crow[col]));
+                crow[col] = __dadd_rn(__dmul_rn(p.alpha, acc[i][j]), __dmul_rn(p.beta, old[j]));
         }
     }
 }
