@@ -112,9 +112,10 @@ def test_extreme_shapes(gpu, oracle, m, n, k, schedule, monkeypatch):
 
 
 def test_split_configs_agree_bitwise_on_random_cases(gpu):
-    """SPLIT tile walks (configs 18, 20, 24: equal (tile, k-tile) ranges per SM, straddling tiles
-    finished from parked accumulators) on random shapes large enough to split, random scalars
-    and padded leading dimensions: bits equal the one-CTA-per-tile launch (config 17)."""
+    """SPLIT tile walks (configs 18, 20, 24, 25: equal (tile, k-tile) ranges per SM or per consumer
+    group, straddling tiles finished from parked accumulators) and the two-group data-parallel
+    config 26 on random shapes large enough to split, random scalars and padded leading
+    dimensions: bits equal the one-CTA-per-tile launch (config 17)."""
     rng = np.random.default_rng(77001)
     lib = L.lib()
     q = kw.Queue(gpu, kw.QueueFlavor.Async)
@@ -125,7 +126,7 @@ def test_split_configs_agree_bitwise_on_random_cases(gpu):
         beta = float(rng.choice([0.0, 1.0, -1.25]))
         a, b, c = rng.standard_normal((m, k)), rng.standard_normal((k, n)), rng.standard_normal((m, n))
         outs = []
-        for cfg in (17, 18 + 2 * (case % 2), 24):
+        for cfg in (17, 18 + 2 * (case % 2), 24 + (case % 3)):  # 24: 128 x 128 split, 25/26: two groups
             A, B, Cd = dev_mat(gpu, a), dev_mat(gpu, b), dev_mat(gpu, c)
             L.check(lib.kw_dgemm_with_config(q.handle(), cfg, m, n, k, alpha, A.data(), A.leadingDim(), B.data(),
                                              B.leadingDim(), beta, Cd.data(), Cd.leadingDim()))
