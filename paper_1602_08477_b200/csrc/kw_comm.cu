@@ -23,6 +23,10 @@
 
 namespace kw {
 int dgemm_pick(size_t m, size_t n, size_t k);
+size_t dgemm_krange_park_bytes(int cfg, size_t m, size_t n);
+kw_status dgemm_device_krange(cudaStream_t s, int cfg, size_t m, size_t n, size_t k, double alpha, const double* A,
+                              size_t lda, const double* B, size_t ldb, double beta, double* C, size_t ldc, int kt0,
+                              int kt1, double* park);
 kw_status dgemm_device_cfg(cudaStream_t s, int cfg, size_t m, size_t n, size_t k, double alpha, const double* A,
                            size_t lda, const double* B, size_t ldb, double beta, double* C, size_t ldc);
 }
@@ -115,6 +119,31 @@ std::vector<std::pair<size_t, size_t>> panel_bounds(size_t n, int panels)
 }
 size_t panel_ld(size_t wj) { return (wj + 7) & ~static_cast<size_t>(7); }
 
+// Schedule of kw_dgemm_rowsharded (KW_ROWSHARD_SCHEDULE): "kslab" (default) broadcasts B in two
+// row slabs — contiguous rows, so the root broadcasts straight from its own B (no packing copy
+// when its pitch is the Buffer rule) — and runs the rank's product as two k-range launches (the
+// first slab's k-tiles, accumulators parked; then the rest, reloaded): only the first slab's
+// broadcast is exposed, the second overlaps the first pass, and each pass is one full
+// data-parallel grid. "panels" = round 1's column panels with one launch per panel.
+bool kslab_schedule()
+{
+    static const bool v = [] {
+        const char* e = std::getenv("KW_ROWSHARD_SCHEDULE");
+        return !(e && std::strcmp(e, "panels") == 0);
+    }();
+    return v;
+}
+
+// First slab of the k-slab schedule, in k-tiles of 16: 1/panels of the k-tiles (>= 1).
+size_t first_slab_ktiles(size_t k, int panels)
+{
+    const size_t ktiles = kw::ceil_div(k, static_cast<size_t>(16));
+    if (panels <= 1 || ktiles < 2)
+        return ktiles;
+    const size_t a = ktiles / static_cast<size_t>(panels);
+    return a < 1 ? 1 : a;
+}
+
 kw_status ensure_events(kw_comm_s* c, int n)
 {
     while (static_cast<int>(c->panel_ready.size()) < n) {
@@ -127,6 +156,84 @@ kw_status ensure_events(kw_comm_s* c, int n)
     return KW_OK;
 }
 
+} // namespace
+
+namespace {
+kw_status rowsharded_kslab(kw_comm_s* c, kw::Queue* q, size_t m_local, size_t n, size_t k, double alpha,
+                           const double* A, size_t lda, const double* B, size_t ldb, double beta, double* C,
+                           size_t ldc, double* scratch, int panels, int root)
+{
+    const size_t ldp = panel_ld(n);
+    const size_t ktiles = kw::ceil_div(k, static_cast<size_t>(16));
+    const size_t kt_a = first_slab_ktiles(k, panels);
+    const size_t rows_a = kt_a * 16 < k ? kt_a * 16 : k;
+    const bool is_root = c->rank == root;
+    const bool direct = is_root && ldb == ldp; // the root broadcasts from (and computes on) B itself
+    double* bmat = direct ? const_cast<double*>(B) : scratch;
+    const int cfg = kw::dgemm_pick(m_local, n, k);
+    double* park = nullptr;
+    if (kt_a < ktiles && m_local > 0) {
+        kw_status st = kw::ensure_scratch(q, kw::dgemm_krange_park_bytes(cfg, m_local, n));
+        if (st != KW_OK)
+            return st;
+        park = static_cast<double*>(q->scratch);
+    }
+    kw_status st = ensure_events(c, 2);
+    if (st != KW_OK)
+        return st;
+    cudaError_t e = cudaEventRecord(c->start, q->stream); // B and C may come from earlier tasks
+    if (e == cudaSuccess)
+        e = cudaStreamWaitEvent(c->stream, c->start, 0);
+    ncclResult_t r = ncclSuccess;
+    if (k > 0 && e == cudaSuccess) {
+        if (is_root && !direct)
+            e = cudaMemcpy2DAsync(scratch, ldp * 8, B, ldb * 8, n * 8, k, cudaMemcpyDeviceToDevice, c->stream);
+        // every rank, world 1 included, runs the broadcasts (in place at the root)
+        if (e == cudaSuccess)
+            r = ncclBroadcast(bmat, bmat, rows_a * ldp * sizeof(double), ncclChar, root, c->comm, c->stream);
+        if (e == cudaSuccess && r == ncclSuccess)
+            e = cudaEventRecord(c->panel_ready[0], c->stream);
+        if (e == cudaSuccess && r == ncclSuccess && rows_a < k)
+            r = ncclBroadcast(bmat + rows_a * ldp, bmat + rows_a * ldp, (k - rows_a) * ldp * sizeof(double), ncclChar,
+                              root, c->comm, c->stream);
+        if (e == cudaSuccess && r == ncclSuccess)
+            e = cudaEventRecord(c->panel_ready[1], c->stream);
+    }
+    else if (e == cudaSuccess) {
+        e = cudaEventRecord(c->panel_ready[0], c->stream);
+        if (e == cudaSuccess)
+            e = cudaEventRecord(c->panel_ready[1], c->stream);
+    }
+    if (r != ncclSuccess)
+        return kw::task_fail(q, std::string("ncclBroadcast: ") + ncclGetErrorString(r));
+    if (e == cudaSuccess)
+        e = cudaStreamWaitEvent(q->stream, c->panel_ready[0], 0);
+    if (e != cudaSuccess)
+        return kw::task_fail(q, std::string("dgemm_rowsharded: ") + cudaGetErrorString(e));
+    if (m_local > 0) {
+        if (kt_a >= ktiles) {
+            st = kw::dgemm_device_cfg(q->stream, cfg, m_local, n, k, alpha, A, lda, bmat, ldp, beta, C, ldc);
+        }
+        else {
+            st = kw::dgemm_device_krange(q->stream, cfg, m_local, n, k, alpha, A, lda, bmat, ldp, beta, C, ldc, 0,
+                                         static_cast<int>(kt_a), park);
+            if (st == KW_OK) {
+                e = cudaStreamWaitEvent(q->stream, c->panel_ready[1], 0);
+                if (e != cudaSuccess)
+                    return kw::task_fail(q, std::string("dgemm_rowsharded: ") + cudaGetErrorString(e));
+                st = kw::dgemm_device_krange(q->stream, cfg, m_local, n, k, alpha, A, lda, bmat, ldp, beta, C, ldc,
+                                             static_cast<int>(kt_a), static_cast<int>(ktiles), park);
+            }
+        }
+        if (st != KW_OK)
+            return kw::task_fail(q, kw::last_error());
+    }
+    // later tasks on the queue (and the next call's broadcasts into the scratch) follow both passes
+    e = cudaStreamWaitEvent(q->stream, c->panel_ready[1], 0);
+    if (e != cudaSuccess)
+        return kw::task_fail(q, std::string("dgemm_rowsharded: ") + cudaGetErrorString(e));
+    return kw::after_enqueue(q, "dgemm_rowsharded");
+}
 } // namespace
 
 extern "C" {
@@ -220,7 +327,9 @@ kw_status kw_dgemm_rowsharded_scratch(size_t n, size_t k, int panels, size_t* el
     if (panels < 1)
         return kw::usage("dgemm_rowsharded: panels must be >= 1");
     size_t total = 0;
-    if (n > 0)
+    if (n > 0 && kslab_schedule())
+        total = k * panel_ld(n); // B at the Buffer pitch rule
+    else if (n > 0)
         for (const auto& b : panel_bounds(n, panels))
             total += k * panel_ld(b.second);
     *elems = total;
@@ -253,6 +362,10 @@ kw_status kw_dgemm_rowsharded(kw_comm c, kw_queue qh, size_t m_local, size_t n, 
         return kw::usage("dgemm_rowsharded: lda smaller than k");
     if (m_local > 0 && ldc < n)
         return kw::usage("dgemm_rowsharded: ldc smaller than n");
+    if (kslab_schedule()) {
+        kw::DeviceGuard g(q->device);
+        return rowsharded_kslab(c, q, m_local, n, k, alpha, A, lda, B, ldb, beta, C, ldc, b_panels, panels, root);
+    }
     // Panels start on 128-column tile boundaries (panel_bounds).
     const auto bounds = panel_bounds(n, panels);
     const int np = static_cast<int>(bounds.size());

@@ -478,11 +478,16 @@ __device__ __noinline__ void split_abort(const uint32_t* scratch, int lane)
         atomicExch_system(abort, KW_FAIL_READY_TIMEOUT);
 }
 
-template <class Cfg, bool STREAMED = false, bool SPLIT = false>
+// KRANGE: a data-parallel launch over one k-tile range [p.npr, p.npc) of every tile — accumulators
+// reloaded from (kt0 > 0) and parked to (kt1 < K) p.partial per tile, so a product can run as
+// several launches in k order with the bits of one launch (the row-sharded DGEMM's k-slab
+// passes: each pass only needs the B rows broadcast so far).
+template <class Cfg, bool STREAMED = false, bool SPLIT = false, bool KRANGE = false>
 __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmParams p)
 {
-    static_assert(!(STREAMED && SPLIT), "one tile-walk mode");
+    static_assert(int(STREAMED) + int(SPLIT) + int(KRANGE) <= 1, "one tile-walk mode");
+    static_assert(!KRANGE || Cfg::GROUPS == 1, "k-range launches use one consumer group");
     static_assert(!STREAMED || Cfg::GROUPS == 1, "streamed launches use one consumer group");
     extern __shared__ uint8_t smem_raw[];
     // 1 KiB alignment (128B-swizzled TMA boxes) by pointer arithmetic on the __shared__ array, not
@@ -547,6 +552,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
                 kt1 = ktiles;
                 tile = sr.t_tail;
             }
+        }
+        else if constexpr (KRANGE) {
+            kt0 = p.npr;
+            kt1 = p.npc;
         }
         else {
             kt0 = 0;
@@ -720,7 +729,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     // k-split (streamed only): this thread's accumulators of the tile, parked between passes;
     // item i of lane l at ((tile * CONSUMERS + warp) * MT*NT + i) * 32 + l (coalesced double2).
     double2* park = nullptr;
-    if constexpr (STREAMED) {
+    if constexpr (STREAMED || KRANGE) {
         const size_t tid_tile = static_cast<size_t>(bm / Cfg::BM) * p.tiles_n + bn / Cfg::BN;
         park = reinterpret_cast<double2*>(p.partial) + (tid_tile * Cfg::CONSUMERS + lw) * (Cfg::MT * Cfg::NT) * 32 + lane;
     }
@@ -786,7 +795,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
         }
     }
     stamp(2 + 2 * tile);
-    if constexpr (STREAMED) {
+    if constexpr (STREAMED || KRANGE) {
         if (kt0 > 0) {
 #pragma unroll
             for (int i = 0; i < Cfg::MT; ++i)
@@ -935,10 +944,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
             continue;
         }
     }
-    if constexpr (STREAMED) {
+    if constexpr (STREAMED || KRANGE) {
         if (kt1 < ktiles) {
-            // first pass of a k-split: park the accumulators; the second pass (same CTA, same
-            // thread, later in this loop) reloads them and runs the epilogue
+            // first pass of a k-split: park the accumulators; the second pass (streamed: same
+            // CTA, same thread, later in this loop; k-range: the next launch) reloads them and
+            // runs the epilogue
 #pragma unroll
             for (int i = 0; i < Cfg::MT; ++i)
 #pragma unroll
@@ -1072,7 +1082,7 @@ bool dgemm_pdl()
 // PDL only where the early-launched grid cannot take free co-resident slots: a dependent CTA
 // placed beside a short grid's CTAs fixes its SM before the grid drains and unbalances the next
 // launch (measured: the 64 x 64 three-CTA tile at 1024^3 fell from 26.9 to 18.0 TFLOP/s).
-template <class Cfg, bool STREAMED, bool SPLIT>
+template <class Cfg, bool STREAMED, bool SPLIT, bool KRANGE = false>
 void launch_tma_kernel(unsigned grid, cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb,
                        const GemmParams& p, bool pdl)
 {
@@ -1086,7 +1096,7 @@ void launch_tma_kernel(unsigned grid, cudaStream_t s, const CUtensorMap& ma, con
     attr[0].val.programmaticStreamSerializationAllowed = (pdl && dgemm_pdl()) ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, dgemm_tma_kernel<Cfg, STREAMED, SPLIT>, ma, mb, p);
+    cudaLaunchKernelEx(&cfg, dgemm_tma_kernel<Cfg, STREAMED, SPLIT, KRANGE>, ma, mb, p);
 }
 
 template <class Cfg, bool PERSISTENT = false, bool STREAMED = false>
@@ -1765,6 +1775,36 @@ kw_status launch_split(cudaStream_t s, const GemmParams& p0)
     return KW_OK;
 }
 
+// One k-tile range [kt0, kt1) of every tile of a resident product (KRANGE), parking to /
+// reloading from `park` (dgemm_krange_park_bytes).
+template <class Cfg>
+kw_status launch_krange(cudaStream_t s, const GemmParams& p0, int kt0, int kt1, double* park)
+{
+    GemmParams p = p0;
+    p.tiles_m = static_cast<int>(kw::ceil_div(p.m, Cfg::BM));
+    p.tiles_n = static_cast<int>(kw::ceil_div(p.n, Cfg::BN));
+    const long long tiles = static_cast<long long>(p.tiles_m) * p.tiles_n;
+    if (tiles > INT_MAX)
+        return kw::usage("dgemm: problem too large for the tile grid");
+    if (!tma_eligible(p))
+        return kw::usage("dgemm (k-range): operands not TMA-addressable");
+    CUtensorMap ma, mb;
+    if (!make_map(&ma, p.a, p.m, p.k, p.lda, Cfg::BM) || !make_map(&mb, p.b, p.k, p.n, p.ldb, 16))
+        return kw::usage("dgemm (k-range): tensor map encoding failed");
+    const kw_status st = ensure_smem(reinterpret_cast<const void*>(dgemm_tma_kernel<Cfg, false, false, true>),
+                                     Cfg::SMEM, "dgemm: cudaFuncSetAttribute");
+    if (st != KW_OK)
+        return st;
+    p.npr = kt0;
+    p.npc = kt1;
+    p.partial = park;
+    p.panel_rows = dgemm_group();
+    const long long resident = static_cast<long long>(sm_count()) * Cfg::MIN_BLOCKS;
+    launch_tma_kernel<Cfg, false, false, true>(static_cast<unsigned>(tiles), s, ma, mb, p, tiles >= resident);
+    kw::g_launches.fetch_add(1, std::memory_order_relaxed);
+    return KW_OK;
+}
+
 struct CfgInfo {
     int bm, bn, bk, threads, stages;
     kw_status (*launch)(cudaStream_t, const GemmParams&);
@@ -1979,6 +2019,24 @@ kw_status dgemm_device(cudaStream_t s, int tile, size_t m, size_t n, size_t k, d
 int dgemm_pick(size_t m, size_t n, size_t k)
 {
     return pick_config(make_params(m, n, k, 1.0, nullptr, k, nullptr, n, 0.0, nullptr, n));
+}
+
+// k-range passes for the row-sharded k-slab schedule (configs 16 / 17, the data-parallel ones).
+size_t dgemm_krange_park_bytes(int cfg, size_t m, size_t n)
+{
+    const size_t bm = 64, bn = cfg == kCfgSmall ? 64 : 128;
+    return kw::ceil_div(m, bm) * bm * kw::ceil_div(n, bn) * bn * sizeof(double);
+}
+
+kw_status dgemm_device_krange(cudaStream_t s, int cfg, size_t m, size_t n, size_t k, double alpha, const double* A,
+                              size_t lda, const double* B, size_t ldb, double beta, double* C, size_t ldc, int kt0,
+                              int kt1, double* park)
+{
+    if (m == 0 || n == 0)
+        return KW_OK;
+    const GemmParams p = make_params(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
+    return cfg == kCfgSmall ? launch_krange<Tma64x64x3p>(s, p, kt0, kt1, park)
+                            : launch_krange<Tma64x128x2p>(s, p, kt0, kt1, park);
 }
 
 kw_status dgemm_device_cfg(cudaStream_t s, int cfg, size_t m, size_t n, size_t k, double alpha, const double* A,

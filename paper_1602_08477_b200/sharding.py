@@ -4,7 +4,9 @@ AXPY: contiguous index ranges, boundaries on 16-byte multiples; no collective â€
 is independent, so the sharded result is bit-identical to one GPU by construction.
 
 DGEMM: rank r owns row block r of A and C (boundaries on the 128-row tile); B lives on the root
-and is broadcast (ncclBroadcast over NVLink) in column panels, panel j stored k x w_j at leading
+and is broadcast (ncclBroadcast over NVLink). Default "kslab" schedule: two row slabs of B
+(dgemm_kslabs â€” contiguous rows, broadcast in place from the root's B), the rank's product run as
+two k-range launches. KW_ROWSHARD_SCHEDULE=panels: column panels, panel j stored k x w_j at leading
 dimension round8(w_j) in the panel-major scratch (the Buffer pitch rule, so an odd-width last
 panel stays TMA-addressable), each panel's broadcast overlapped with the previous panel's DGEMM.
 `dgemm_panels` is the exact layout kw_dgemm_rowsharded uses (kw_comm.cu), so host code and
@@ -12,6 +14,7 @@ tests can reproduce it.
 """
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 
@@ -57,6 +60,26 @@ def dgemm_panels(n: int, k: int, panels: int, tile: int = 128) -> list[Panel]:
     return out
 
 
+def dgemm_kslabs(k: int, panels: int) -> list[tuple[int, int]]:
+    """Row slabs [k0, k1) of B the default "kslab" schedule broadcasts (kw_comm.cu
+    first_slab_ktiles): the first 1/panels of the 16-row k-tiles, then the rest."""
+    ktiles = ceil_div(k, 16)
+    if panels <= 1 or ktiles < 2:
+        return [(0, k)]
+    a = max(1, ktiles // panels) * 16
+    return [(0, min(a, k))] + ([(a, k)] if a < k else [])
+
+
+def kslab_schedule() -> bool:
+    return os.environ.get("KW_ROWSHARD_SCHEDULE") != "panels"
+
+
 def dgemm_panel_scratch(n: int, k: int, panels: int, tile: int = 128) -> int:
-    """Doubles of panel-major scratch kw_dgemm_rowsharded needs (kw_dgemm_rowsharded_scratch)."""
+    """Doubles of B scratch kw_dgemm_rowsharded needs (kw_dgemm_rowsharded_scratch): B at the
+    Buffer pitch (k x round8(n)) for the default k-slab schedule, the panel-major layout for
+    KW_ROWSHARD_SCHEDULE=panels."""
+    if n == 0:
+        return 0
+    if kslab_schedule():
+        return k * ceil_div(n, 8) * 8
     return sum(k * p.ld for p in dgemm_panels(n, k, panels, tile))

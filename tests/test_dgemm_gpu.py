@@ -182,13 +182,15 @@ def test_row_panels_and_column_panels_are_bitwise_invariant(gpu, oracle):
     assert np.array_equal(full, cols)
 
 
-@pytest.mark.parametrize("n,panels", [(1000, 3), (1001, 3), (1001, 8), (127, 2), (2049, 5)])
-def test_rowsharded_single_rank_pipeline(gpu, oracle, n, panels):
-    """kw_dgemm_rowsharded with world = 1 (NCCL single-rank communicator): every panel goes
-    through ncclBroadcast (a single-rank broadcast is executed, not skipped), then the panel
-    DGEMMs on two compute streams. Must equal kw_dgemm bit for bit — including odd n, where the
-    last panel has an odd width and a padded leading dimension (a dense odd pitch
-    would drop that panel to the non-TMA kernel and change its k grouping)."""
+@pytest.mark.parametrize("n,panels,align", [(1000, 3, 64), (1001, 3, 64), (1001, 8, 256), (127, 2, 64),
+                                           (2049, 5, 256), (640, 1, 64)])
+def test_rowsharded_single_rank_pipeline(gpu, oracle, n, panels, align):
+    """kw_dgemm_rowsharded with world = 1 (NCCL single-rank communicator): B goes through
+    ncclBroadcast (a single-rank broadcast is executed, not skipped) in the default k-slab
+    schedule's two row slabs, then the rank's product runs as two k-range launches (accumulators
+    parked between them). Must equal kw_dgemm bit for bit — including odd n, and B pitches that
+    are not the Buffer rule (align 256: the root packs B into the scratch first, which must then
+    hold B at leading dimension round8(n))."""
     from paper_1602_08477_b200 import sharding as S
     rng = np.random.default_rng(5)
     m, k = 256, 200
@@ -200,28 +202,57 @@ def test_rowsharded_single_rank_pipeline(gpu, oracle, n, panels):
     assert L.lib().kw_comm_init(C.byref(comm), 0, 1, 0, uid) == 0, L.last_error()
     elems = C.c_size_t()
     assert L.lib().kw_dgemm_rowsharded_scratch(n, k, panels, C.byref(elems)) == 0
-    assert elems.value == S.dgemm_panel_scratch(n, k, panels)
-    A, B, Cb = mat(gpu, a), mat(gpu, b), mat(gpu, c)
+    assert elems.value == S.dgemm_panel_scratch(n, k, panels) == k * (-(-n // 8) * 8)
+    A, B, Cb = mat(gpu, a), mat(gpu, b, align=align), mat(gpu, c)
     scratch = kw.Buffer(gpu, kw.IndexVec(elems.value), 8)
+    scratch.fill_raw(0)
     q = kw.Queue(gpu, kw.QueueFlavor.Async)
-    st = L.lib().kw_dgemm_rowsharded(comm, q.handle(), m, n, k, 1.1, A.data(), A.leadingDim(), B.data(),
-                                     B.leadingDim(), 0.9, Cb.data(), Cb.leadingDim(), scratch.data(), panels, 0)
-    assert st == 0, L.last_error()
-    q.wait()
-    assert np.array_equal(Cb.download(), want)
-    # the scratch holds exactly the broadcast panels at their padded pitch
-    got = scratch.download()
-    for p in S.dgemm_panels(n, k, panels):
-        blk = got[p.offset:p.offset + k * p.ld].reshape(k, p.ld)[:, :p.width]
-        assert np.array_equal(blk, b[:, p.n0:p.n0 + p.width])
-    # a second call on the same communicator (events reused) gives the same bits from pristine C
-    Cb.upload(c)
-    st = L.lib().kw_dgemm_rowsharded(comm, q.handle(), m, n, k, 1.1, A.data(), A.leadingDim(), B.data(),
-                                     B.leadingDim(), 0.9, Cb.data(), Cb.leadingDim(), scratch.data(), panels, 0)
-    assert st == 0, L.last_error()
-    q.wait()
-    assert np.array_equal(Cb.download(), want)
+    for _ in range(2):  # a second call on the same communicator (events, park scratch reused)
+        Cb.upload(c)
+        st = L.lib().kw_dgemm_rowsharded(comm, q.handle(), m, n, k, 1.1, A.data(), A.leadingDim(), B.data(),
+                                         B.leadingDim(), 0.9, Cb.data(), Cb.leadingDim(), scratch.data(), panels, 0)
+        assert st == 0, L.last_error()
+        q.wait()
+        assert np.array_equal(Cb.download(), want)
+    ldp = -(-n // 8) * 8
+    got = scratch.download().reshape(k, ldp)[:, :n]
+    if B.leadingDim() != ldp:  # packed by the root
+        assert np.array_equal(got, b)
+    else:  # the root broadcast straight from B: the scratch is untouched
+        assert not got.any()
     assert L.lib().kw_comm_destroy(comm) == 0
+
+
+def test_rowsharded_panel_schedule_still_matches(gpu):
+    """KW_ROWSHARD_SCHEDULE=panels (round 1's column panels, one launch per panel, read once per
+    process) in a subprocess: bits equal kw_dgemm, panel-major scratch layout."""
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import ctypes as C, sys, numpy as np
+sys.path.insert(0, '.')
+from paper_1602_08477_b200 import _lib as L, kernelweave as kw, sharding as S
+gpu = kw.Device.gpu(0); GPU = kw.BackendKind.GpuCudaRt
+rng = np.random.default_rng(7); m, n, k, panels = 300, 1001, 150, 3
+a, b, c = rng.random((m, k)) * 10, rng.random((k, n)) * 10, rng.random((m, n)) * 10
+def buf(x):
+    t = kw.Buffer(gpu, kw.IndexVec(*x.shape), 8); t.upload(x); return t
+A, B, C1, C2 = buf(a), buf(b), buf(c), buf(c)
+kw.executeTask(GPU, kw.gemmTiledWorkDiv(GPU, m, n, 128), kw.GemmTiledKernel(), kw.GemmArgs(m, n, k, 1.1, 0.9, A, B, C1))
+uid = (C.c_char * 128)(); assert L.lib().kw_comm_unique_id(uid) == 0
+comm = C.c_void_p(); assert L.lib().kw_comm_init(C.byref(comm), 0, 1, 0, uid) == 0
+e = C.c_size_t(); assert L.lib().kw_dgemm_rowsharded_scratch(n, k, panels, C.byref(e)) == 0
+assert e.value == S.dgemm_panel_scratch(n, k, panels) == sum(k * p.ld for p in S.dgemm_panels(n, k, panels))
+sc = kw.Buffer(gpu, kw.IndexVec(e.value), 8); q = kw.Queue(gpu, kw.QueueFlavor.Async)
+assert L.lib().kw_dgemm_rowsharded(comm, q.handle(), m, n, k, 1.1, A.data(), A.leadingDim(), B.data(), B.leadingDim(),
+                                   0.9, C2.data(), C2.leadingDim(), sc.data(), panels, 0) == 0, L.last_error()
+q.wait(); assert np.array_equal(C1.download(), C2.download()); print("PANELS OK")
+"""
+    env = dict(os.environ, KW_ROWSHARD_SCHEDULE="panels")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                         cwd=str(__import__("pathlib").Path(__file__).resolve().parent.parent), timeout=300)
+    assert "PANELS OK" in out.stdout, out.stdout + out.stderr
 
 
 def test_rowsharded_16384_cubed(gpu, oracle):

@@ -41,26 +41,27 @@ def _worker(rank, world, port, q):
         full = np.concatenate([p[2] for p in sorted(parts, key=lambda t: t[0])])
         axpy_ok = np.array_equal(full, O.axpy(alpha, x, y))
 
-        # ---- DGEMM: row blocks + panel-major broadcast of B from rank 0
-        m, nn, k = 300, 521, 77  # odd n: the last panel's leading dimension is padded
+        # ---- DGEMM: row blocks + B broadcast from rank 0 in two row slabs (the default k-slab
+        # schedule: contiguous rows of B at the Buffer pitch, in place at the root)
+        m, nn, k = 300, 521, 77  # odd n: B's pitch is padded to round8(n)
         rng = np.random.default_rng(5)
         a = rng.random((m, k)) * 10
         c = rng.random((m, nn)) * 10
+        ldp = S.ceil_div(nn, 8) * 8
         b_root = rng.random((k, nn)) * 10 if rank == 0 else None
         r0, r1 = S.dgemm_rows(m, world, rank)
-        panels = S.dgemm_panels(nn, k, 3)
         scratch = torch.zeros(S.dgemm_panel_scratch(nn, k, 3), dtype=torch.float64)
-        for p in panels:
-            view = scratch[p.offset:p.offset + k * p.ld]
-            if rank == 0:
-                padded = np.zeros((k, p.ld))
-                padded[:, :p.width] = b_root[:, p.n0:p.n0 + p.width]
-                view.copy_(torch.from_numpy(padded.reshape(-1)))
-            dist.broadcast(view, src=0)
-        cl = c[r0:r1].copy()
-        for p in panels:
-            bp = scratch[p.offset:p.offset + k * p.ld].numpy().reshape(k, p.ld)[:, :p.width]
-            cl[:, p.n0:p.n0 + p.width] = O.gemm(1.3, 0.7, a[r0:r1], bp, c[r0:r1, p.n0:p.n0 + p.width], threads=1)
+        assert scratch.numel() == k * ldp
+        if rank == 0:
+            padded = np.zeros((k, ldp))
+            padded[:, :nn] = b_root
+            scratch.copy_(torch.from_numpy(padded.reshape(-1)))
+        slabs = S.dgemm_kslabs(k, 3)
+        assert slabs[0][0] == 0 and slabs[-1][1] == k
+        for k0, k1 in slabs:
+            dist.broadcast(scratch[k0 * ldp:k1 * ldp], src=0)
+        b_full = scratch.numpy().reshape(k, ldp)[:, :nn]
+        cl = O.gemm(1.3, 0.7, a[r0:r1], b_full, c[r0:r1], threads=1) if r1 > r0 else c[r0:r1]
         blocks = [None] * world
         dist.all_gather_object(blocks, (r0, cl))
         cfull = np.vstack([blk[1] for blk in sorted(blocks, key=lambda t: t[0]) if blk[1].size])
@@ -108,14 +109,21 @@ def test_panel_layout_matches_the_c_abi_rule():
     ps = S.dgemm_panels(16384, 16384, 8)
     assert [p.width for p in ps] == [2048] * 8
     assert ps[-1].offset + 16384 * ps[-1].width == 16384 * 16384
-    assert S.dgemm_panel_scratch(16384, 16384, 8) == 16384 * 16384
+    assert S.dgemm_panel_scratch(16384, 16384, 8) == 16384 * 16384  # either schedule
     ps = S.dgemm_panels(1000, 200, 3)
     assert [p.width for p in ps] == [384, 384, 232] and [p.n0 for p in ps] == [0, 384, 768]
     ps = S.dgemm_panels(1001, 200, 3)
     assert [p.width for p in ps] == [384, 384, 233] and [p.ld for p in ps] == [384, 384, 240]
     assert [p.offset for p in ps] == [0, 200 * 384, 2 * 200 * 384]
-    assert S.dgemm_panel_scratch(1001, 200, 3) == 200 * (384 + 384 + 240)
+    assert S.dgemm_panel_scratch(1001, 200, 3) == 200 * 1008  # k-slab schedule: k x round8(n)
     assert [p.width for p in S.dgemm_panels(100, 5, 4)] == [100]  # one tile: a single panel
+
+
+def test_kslabs_partition_k():
+    assert S.dgemm_kslabs(16384, 8) == [(0, 2048), (2048, 16384)]
+    assert S.dgemm_kslabs(77, 3) == [(0, 16), (16, 77)]  # 5 k-tiles of 16: the first slab is one
+    assert S.dgemm_kslabs(10, 8) == [(0, 10)]  # a single k-tile: one slab
+    assert S.dgemm_kslabs(1000, 1) == [(0, 1000)]
 
 
 @pytest.mark.parametrize("n,k,panels", [(16384, 16384, 8), (1001, 200, 3), (127, 9, 2), (5000, 33, 7), (100, 5, 4)])
