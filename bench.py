@@ -680,8 +680,11 @@ def run_dgemm_rowsharded(args, dist, kw, L, lib, dev, q, timed, res) -> dict:
     tflops = 2 * size ** 3 * steps / (ms / 1e3) / 1e12
     per_gpu = tflops / dist.world
     res.update({"value": round(tflops, 3), "ms_per_step": round(ms / steps, 3), "steps": steps,
-                "config": f"DGEMM fp64 16384^3 row-block sharded x{dist.world}, ncclBroadcast of B in "
-                          f"{args.panels} column panels overlapped with compute (BASELINE configs[3])",
+                "config": (f"DGEMM fp64 16384^3 row-block sharded x{dist.world}, ncclBroadcast of B in two row slabs "
+                           f"(first 1/{args.panels} of the k-tiles, then the rest) overlapped with two k-range launches "
+                           f"(BASELINE configs[3])" if os.environ.get("KW_ROWSHARD_SCHEDULE") != "panels" else
+                           f"DGEMM fp64 16384^3 row-block sharded x{dist.world}, ncclBroadcast of B in {args.panels} "
+                           f"column panels overlapped with compute (BASELINE configs[3])"),
                 "roofline": {"bound": "fp64", "achieved": round(per_gpu, 3), "unit": "TFLOP/s per GPU",
                              "peak": round(FP64_NOMINAL_TFLOPS, 2), "frac": round(per_gpu / FP64_NOMINAL_TFLOPS, 4),
                              "peak_source": "nominal (148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz)",
