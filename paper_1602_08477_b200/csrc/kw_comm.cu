@@ -362,6 +362,17 @@ kw_status kw_dgemm_rowsharded(kw_comm c, kw_queue qh, size_t m_local, size_t n, 
         return kw::usage("dgemm_rowsharded: lda smaller than k");
     if (m_local > 0 && ldc < n)
         return kw::usage("dgemm_rowsharded: ldc smaller than n");
+    {
+        // every operand (and the scratch) is device memory on the queue's device: a host or
+        // foreign-device pointer would fault the context inside a copy or a kernel
+        const void* ops[4] = {b_panels, k > 0 ? A : nullptr, m_local > 0 ? C : nullptr,
+                              (c->rank == root && k > 0) ? B : nullptr};
+        for (const void* ptr : ops) {
+            int d = -1;
+            if (ptr && (kw::pointer_kind(ptr, &d) != KW_MEM_DEVICE || d != q->device))
+                return kw::usage("dgemm_rowsharded: operands and scratch must be device memory on the queue's device");
+        }
+    }
     if (kslab_schedule()) {
         kw::DeviceGuard g(q->device);
         return rowsharded_kslab(c, q, m_local, n, k, alpha, A, lda, B, ldb, beta, C, ldc, b_panels, panels, root);

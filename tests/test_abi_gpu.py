@@ -78,6 +78,23 @@ def test_l2_flush_and_world1_broadcast(gpu):
         q.wait()
         assert np.array_equal(buf.download(), vals)  # the root's own data is unchanged
         assert lib.kw_comm_broadcast(comm, q.handle(), buf.data(), 8000, 1) == L.KW_USAGE  # no rank 1
+        # row-sharded DGEMM usage errors come back before anything is enqueued: host operands,
+        # missing root B, root out of range, zero panels
+        m = n = k = 64
+        dA, dB, dC = (kw.Buffer(gpu, kw.IndexVec(m, m), 8) for _ in range(3))
+        hB = kw.Buffer(kw.Device.host(), kw.IndexVec(m, m), 8)
+        sc = kw.Buffer(gpu, kw.IndexVec(m * m), 8)
+        args = lambda A, B, Cm, scr, panels=2, root=0: lib.kw_dgemm_rowsharded(  # noqa: E731
+            comm, q.handle(), m, n, k, 1.0, A.data(), A.leadingDim(), B.data() if B else None,
+            B.leadingDim() if B else 0, 0.0, Cm.data(), Cm.leadingDim(), scr.data(), panels, root)
+        assert args(dA, hB, dC, sc) == L.KW_USAGE
+        assert "device memory" in L.last_error()
+        assert args(dA, None, dC, sc) == L.KW_USAGE
+        assert args(dA, dB, dC, sc, root=1) == L.KW_USAGE
+        assert args(dA, dB, dC, sc, panels=0) == L.KW_USAGE
+        q.wait()  # nothing was enqueued, nothing failed
+        assert args(dA, dB, dC, sc) == 0
+        q.wait()
     finally:
         L.check(lib.kw_comm_destroy(comm))
 
