@@ -133,3 +133,38 @@ def test_split_configs_agree_bitwise_on_random_cases(gpu):
             q.wait()
             outs.append(Cd.download())
         assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2]), (case, m, n, k)
+
+
+def test_rowsharded_kslab_random_cases(gpu):
+    """The k-slab row-sharded schedule (world-1 NCCL communicator, broadcasts executing) on random
+    shapes, slab splits (panels), B pitches (root broadcasting in place or packing) and scalars:
+    bits equal kw_dgemm of the same block."""
+    rng = np.random.default_rng(55501)
+    lib = L.lib()
+    uid = (C.c_char * 128)()
+    assert lib.kw_comm_unique_id(uid) == 0
+    comm = C.c_void_p()
+    assert lib.kw_comm_init(C.byref(comm), 0, 1, 0, uid) == 0, L.last_error()
+    q = kw.Queue(gpu, kw.QueueFlavor.Async)
+    try:
+        for case in range(24):
+            m, n = (int(v) for v in rng.integers(1, 1500, size=2))
+            k = int(rng.integers(1, 1200))
+            panels = int(rng.choice([1, 2, 3, 8, 16]))
+            align = int(rng.choice([64, 128, 256]))
+            alpha, beta = float(rng.choice([1.0, -0.5])), float(rng.choice([0.0, 1.25]))
+            a, b, c = rng.standard_normal((m, k)), rng.standard_normal((k, n)), rng.standard_normal((m, n))
+            A, Cw, Cr = dev_mat(gpu, a), dev_mat(gpu, c), dev_mat(gpu, c)
+            B = kw.Buffer(gpu, kw.IndexVec(k, n), 8, align)
+            B.upload(b)
+            L.check(lib.kw_dgemm(q.handle(), None, m, n, k, alpha, A.data(), A.leadingDim(), B.data(), B.leadingDim(),
+                                 beta, Cw.data(), Cw.leadingDim()))
+            elems = C.c_size_t()
+            L.check(lib.kw_dgemm_rowsharded_scratch(n, k, panels, C.byref(elems)))
+            sc = kw.Buffer(gpu, kw.IndexVec(max(1, elems.value)), 8)
+            L.check(lib.kw_dgemm_rowsharded(comm, q.handle(), m, n, k, alpha, A.data(), A.leadingDim(), B.data(),
+                                            B.leadingDim(), beta, Cr.data(), Cr.leadingDim(), sc.data(), panels, 0))
+            q.wait()
+            assert np.array_equal(Cw.download(), Cr.download()), (case, m, n, k, panels, align)
+    finally:
+        lib.kw_comm_destroy(comm)
