@@ -1938,6 +1938,12 @@ GemmParams make_params(size_t m, size_t n, size_t k, double alpha, const double*
     return ::make_params(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
 }
 size_t round2(size_t v) { return ::round2(v); }
+// Data-parallel choices only (16 / 17): for callers that overlap consecutive launches on two
+// streams (the host-staged row-panel schedule), where one-CTA-per-SM SPLIT grids could not overlap.
+kw_status launch_tiled_dp(cudaStream_t s, int tile, const GemmParams& p)
+{
+    return kCfgs[tile == 64 ? kCfgSmall : pick_config(p)].launch(s, p);
+}
 kw_status launch_tiled(cudaStream_t s, int tile, const GemmParams& p)
 {
     return kCfgs[tile == 64 ? kCfgSmall : pick_resident(p)].launch(s, p);

@@ -129,7 +129,7 @@ kw_status dgemm_staged(kw::Queue* q, int tile, size_t m, size_t n, size_t k, dou
                     e = cudaStreamWaitEvent(q->stream, q->ev_bp[j], 0);
                 if (e != cudaSuccess)
                     break;
-                st = launch_tiled(q->stream, tile,
+                st = launch_tiled_dp(q->stream, tile,
                                   make_params(rows, wj, k, alpha, Ad, ldad, Bd + n0, ldbd, beta, Cd + n0, ldcd));
                 if (st != KW_OK)
                     break;
@@ -146,7 +146,7 @@ kw_status dgemm_staged(kw::Queue* q, int tile, size_t m, size_t n, size_t k, dou
                 if (e != cudaSuccess)
                     break;
             }
-            st = launch_tiled(comp, tile, make_params(rows, n, k, alpha, Ad, ldad, Bd, ldbd, beta, Cd, ldcd));
+            st = launch_tiled_dp(comp, tile, make_params(rows, n, k, alpha, Ad, ldad, Bd, ldbd, beta, Cd, ldcd));
             if (st != KW_OK)
                 break;
         }

@@ -48,6 +48,7 @@ GemmParams make_params(size_t m, size_t n, size_t k, double alpha, const double*
 size_t round2(size_t v); // leading dimension rounded up to a 16-byte multiple of doubles
 // One launch of the tiled DGEMM (the CTA tile chosen per problem; tile 64 forces the 64 x 64 one).
 kw_status launch_tiled(cudaStream_t s, int tile, const GemmParams& p);
+kw_status launch_tiled_dp(cudaStream_t s, int tile, const GemmParams& p); // data-parallel configs only
 bool tma_eligible(const GemmParams& p);
 
 // Streamed mode: the configuration the persistent launch uses, its tile and consumer warps
