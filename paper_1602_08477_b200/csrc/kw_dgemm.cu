@@ -1083,8 +1083,8 @@ bool dgemm_pdl()
 // placed beside a short grid's CTAs fixes its SM before the grid drains and unbalances the next
 // launch (measured: the 64 x 64 three-CTA tile at 1024^3 fell from 26.9 to 18.0 TFLOP/s).
 template <class Cfg, bool STREAMED, bool SPLIT, bool KRANGE = false>
-void launch_tma_kernel(unsigned grid, cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb,
-                       const GemmParams& p, bool pdl)
+cudaError_t launch_tma_kernel(unsigned grid, cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb,
+                              const GemmParams& p, bool pdl)
 {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
@@ -1096,7 +1096,7 @@ void launch_tma_kernel(unsigned grid, cudaStream_t s, const CUtensorMap& ma, con
     attr[0].val.programmaticStreamSerializationAllowed = (pdl && dgemm_pdl()) ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, dgemm_tma_kernel<Cfg, STREAMED, SPLIT, KRANGE>, ma, mb, p);
+    return cudaLaunchKernelEx(&cfg, dgemm_tma_kernel<Cfg, STREAMED, SPLIT, KRANGE>, ma, mb, p);
 }
 
 template <class Cfg, bool PERSISTENT = false, bool STREAMED = false>
@@ -1614,10 +1614,13 @@ kw_status launch_tma(cudaStream_t s, const GemmParams& p0)
     const long long resident = static_cast<long long>(sm_count()) * Cfg::MIN_BLOCKS;
     const long long ctas = (tiles + Cfg::GROUPS - 1) / Cfg::GROUPS; // a CTA serves GROUPS tiles at a time
     const unsigned grid = static_cast<unsigned>(PERSISTENT && ctas > resident ? resident : ctas);
-    if constexpr (STREAMED)
+    if constexpr (STREAMED) {
         dgemm_tma_kernel<Cfg, true, false><<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(ma, mb, p);
-    else
-        launch_tma_kernel<Cfg, false, false>(grid, s, ma, mb, p, grid >= resident);
+    }
+    else {
+        if (cudaError_t e = launch_tma_kernel<Cfg, false, false>(grid, s, ma, mb, p, grid >= resident))
+            return kw::cuda_fail("dgemm: launch", e);
+    }
     kw::g_launches.fetch_add(1, std::memory_order_relaxed);
     return KW_OK;
 }
@@ -1770,7 +1773,8 @@ kw_status launch_split(cudaStream_t s, const GemmParams& p0)
                      "dgemm: cudaFuncSetAttribute");
     if (st != KW_OK)
         return st;
-    launch_tma_kernel<Cfg, false, true>(static_cast<unsigned>(G), s, ma, mb, p, true);
+    if (cudaError_t e = launch_tma_kernel<Cfg, false, true>(static_cast<unsigned>(G), s, ma, mb, p, true))
+        return kw::cuda_fail("dgemm (split): launch", e);
     kw::g_launches.fetch_add(1, std::memory_order_relaxed);
     return KW_OK;
 }
@@ -1800,7 +1804,9 @@ kw_status launch_krange(cudaStream_t s, const GemmParams& p0, int kt0, int kt1, 
     p.partial = park;
     p.panel_rows = dgemm_group();
     const long long resident = static_cast<long long>(sm_count()) * Cfg::MIN_BLOCKS;
-    launch_tma_kernel<Cfg, false, false, true>(static_cast<unsigned>(tiles), s, ma, mb, p, tiles >= resident);
+    if (cudaError_t e = launch_tma_kernel<Cfg, false, false, true>(static_cast<unsigned>(tiles), s, ma, mb, p,
+                                                                   tiles >= resident))
+        return kw::cuda_fail("dgemm (k-range): launch", e);
     kw::g_launches.fetch_add(1, std::memory_order_relaxed);
     return KW_OK;
 }
