@@ -24,6 +24,7 @@
 namespace kw {
 int dgemm_pick(size_t m, size_t n, size_t k);
 size_t dgemm_krange_park_bytes(int cfg, size_t m, size_t n);
+bool dgemm_krange_ok(size_t m, size_t n, size_t k, const double* A, size_t lda, const double* B, size_t ldb);
 kw_status dgemm_device_krange(cudaStream_t s, int cfg, size_t m, size_t n, size_t k, double alpha, const double* A,
                               size_t lda, const double* B, size_t ldb, double beta, double* C, size_t ldc, int kt0,
                               int kt1, double* park);
@@ -165,11 +166,13 @@ kw_status rowsharded_kslab(kw_comm_s* c, kw::Queue* q, size_t m_local, size_t n,
 {
     const size_t ldp = panel_ld(n);
     const size_t ktiles = kw::ceil_div(k, static_cast<size_t>(16));
-    const size_t kt_a = first_slab_ktiles(k, panels);
-    const size_t rows_a = kt_a * 16 < k ? kt_a * 16 : k;
     const bool is_root = c->rank == root;
     const bool direct = is_root && ldb == ldp; // the root broadcasts from (and computes on) B itself
     double* bmat = direct ? const_cast<double*>(B) : scratch;
+    // Two passes need the TMA kernel (A with an even pitch, 16-byte aligned); otherwise one launch
+    // after the whole broadcast (the library falls back to its cp.async kernel there).
+    const size_t kt_a = kw::dgemm_krange_ok(m_local, n, k, A, lda, bmat, ldp) ? first_slab_ktiles(k, panels) : ktiles;
+    const size_t rows_a = kt_a * 16 < k ? kt_a * 16 : k;
     const int cfg = kw::dgemm_pick(m_local, n, k);
     double* park = nullptr;
     if (kt_a < ktiles && m_local > 0) {

@@ -2033,6 +2033,12 @@ int dgemm_pick(size_t m, size_t n, size_t k)
     return pick_config(make_params(m, n, k, 1.0, nullptr, k, nullptr, n, 0.0, nullptr, n));
 }
 
+// Whether the k-range launches can run on these operands (TMA-addressable A and B).
+bool dgemm_krange_ok(size_t m, size_t n, size_t k, const double* A, size_t lda, const double* B, size_t ldb)
+{
+    return m > 0 && n > 0 && tma_eligible(make_params(m, n, k, 1.0, A, lda, B, ldb, 0.0, nullptr, n));
+}
+
 // k-range passes for the row-sharded k-slab schedule (configs 16 / 17, the data-parallel ones).
 size_t dgemm_krange_park_bytes(int cfg, size_t m, size_t n)
 {

@@ -154,7 +154,9 @@ def test_rowsharded_kslab_random_cases(gpu):
             align = int(rng.choice([64, 128, 256]))
             alpha, beta = float(rng.choice([1.0, -0.5])), float(rng.choice([0.0, 1.25]))
             a, b, c = rng.standard_normal((m, k)), rng.standard_normal((k, n)), rng.standard_normal((m, n))
-            A, Cw, Cr = dev_mat(gpu, a), dev_mat(gpu, c), dev_mat(gpu, c)
+            A = kw.Buffer(gpu, kw.IndexVec(m, k), 8, int(rng.choice([8, 64])))  # 8: odd pitches -> one pass
+            A.upload(a)
+            Cw, Cr = dev_mat(gpu, c), dev_mat(gpu, c)
             B = kw.Buffer(gpu, kw.IndexVec(k, n), 8, align)
             B.upload(b)
             L.check(lib.kw_dgemm(q.handle(), None, m, n, k, alpha, A.data(), A.leadingDim(), B.data(), B.leadingDim(),
