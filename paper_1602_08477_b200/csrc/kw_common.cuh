@@ -81,14 +81,17 @@ struct Queue {
 };
 
 // RAII device selector: the reference's queues are bound to one device; every entry point
-// makes that device current for its duration.
+// makes that device current for its duration. cudaSetDevice runs even when the device number
+// already matches: it also makes the device's primary context current on a host thread that has
+// not touched CUDA yet, which the driver-API calls behind the runtime (cuTensorMapEncodeTiled,
+// cuStreamWriteValue32) need — without it a first call from a new thread silently fell back from
+// the TMA kernel to the cp.async one (other bits, lower rate).
 struct DeviceGuard {
     int prev = -1;
     explicit DeviceGuard(int dev)
     {
         cudaGetDevice(&prev);
-        if (prev != dev)
-            cudaSetDevice(dev);
+        cudaSetDevice(dev);
     }
     ~DeviceGuard()
     {

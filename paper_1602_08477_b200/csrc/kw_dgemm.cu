@@ -36,6 +36,7 @@
 #include <atomic>
 #include <climits>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -1952,7 +1953,12 @@ kw_status launch_tiled_dp(cudaStream_t s, int tile, const GemmParams& p)
 }
 kw_status launch_tiled(cudaStream_t s, int tile, const GemmParams& p)
 {
-    return kCfgs[tile == 64 ? kCfgSmall : pick_resident(p)].launch(s, p);
+    const int cfg = tile == 64 ? kCfgSmall : pick_resident(p);
+    static const bool log = std::getenv("KW_DGEMM_LOG") != nullptr; // tile-choice trace (debugging)
+    if (log)
+        std::fprintf(stderr, "[kw dgemm] %d x %d x %d tile %d -> config %d (tma %d)\n", p.m, p.n, p.k, tile, cfg,
+                     static_cast<int>(tma_eligible(p)));
+    return kCfgs[cfg].launch(s, p);
 }
 bool tma_eligible(const GemmParams& p)
 {

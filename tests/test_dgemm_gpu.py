@@ -631,3 +631,57 @@ def test_mixed_residency_dgemm(gpu, oracle):
     assert L.lib().kw_dgemm(q.handle(), None, m, n, k, 1.2, A.data(), A.leadingDim(), bh.ctypes.data, n, 0.4,
                             Cd.data(), Cd.leadingDim()) == 0
     assert np.array_equal(Cd.download(), want)
+
+
+def test_concurrent_enqueues_on_one_queue(gpu):
+    """Four host threads enqueue DGEMMs (1024^3: the SPLIT walk with its per-stream ticket, flags
+    and park slots) and AXPYs into ONE Async queue while the main thread waits repeatedly: the
+    enqueue lock serialises them in arrival order and every result equals its own single launch."""
+    import threading
+    lib = L.lib()
+    rng = np.random.default_rng(4)
+    n = 1024
+    a, b = rng.random((n, n)), rng.random((n, n))
+    A, B = mat(gpu, a), mat(gpu, b)
+    cs = [rng.random((n, n)) for _ in range(8)]
+    want = []
+    q0 = kw.Queue(gpu, kw.QueueFlavor.Async)
+    for c in cs:
+        Cw = mat(gpu, c)
+        L.check(lib.kw_dgemm(q0.handle(), None, n, n, n, 1.5, A.data(), A.leadingDim(), B.data(), B.leadingDim(),
+                             0.5, Cw.data(), Cw.leadingDim()))
+        q0.wait()
+        want.append(Cw.download())
+    q = kw.Queue(gpu, kw.QueueFlavor.Async)
+    outs = [mat(gpu, c) for c in cs]
+    xs = [kw.Buffer(gpu, kw.IndexVec(1 << 20), 4) for _ in range(4)]
+    ys = [kw.Buffer(gpu, kw.IndexVec(1 << 20), 4) for _ in range(4)]
+    for v in xs + ys:
+        v.upload(np.ones(1 << 20, np.float32))
+    errors = []
+
+    def worker(t):
+        try:
+            for rep in range(5):
+                for i in (t, t + 4):
+                    Cb = outs[i]
+                    if rep == 0:  # each output from its pristine C exactly once
+                        L.check(lib.kw_dgemm(q.handle(), None, n, n, n, 1.5, A.data(), A.leadingDim(), B.data(),
+                                             B.leadingDim(), 0.5, Cb.data(), Cb.leadingDim()))
+                L.check(lib.kw_axpy_f32(q.handle(), None, 1 << 20, 1.0, xs[t].data(), ys[t].data()))
+        except Exception as ex:  # noqa: BLE001
+            errors.append(ex)
+
+    threads = [threading.Thread(target=worker, args=(t,)) for t in range(4)]
+    for th in threads:
+        th.start()
+    while any(th.is_alive() for th in threads):
+        q.wait()
+    for th in threads:
+        th.join()
+    q.wait()
+    assert not errors, errors
+    for Cb, w in zip(outs, want):
+        assert np.array_equal(Cb.download(), w)
+    for y in ys:
+        assert np.all(y.download() == 6.0)  # five AXPYs of +1 on 1
