@@ -685,3 +685,44 @@ def test_concurrent_enqueues_on_one_queue(gpu):
         assert np.array_equal(Cb.download(), w)
     for y in ys:
         assert np.all(y.download() == 6.0)  # five AXPYs of +1 on 1
+
+
+def test_host_operand_schedules_from_fresh_threads(gpu, monkeypatch):
+    """The streamed host-operand (e2e) DGEMM schedule — driver stream memory operations
+    (cuStreamWriteValue32 / cuStreamWaitValue32) and TMA descriptors — run as the FIRST CUDA work
+    of a fresh host thread, three threads at once on their own queues: bits equal the
+    device-resident launch (regression for the missing-context fallback)."""
+    import threading
+    rng = np.random.default_rng(12)
+    m, n, k = 700, 900, 650
+    a, b, c = rng.random((m, k)) * 10, rng.random((k, n)) * 10, rng.random((m, n)) * 10
+    want = tiled(gpu, 0.8, 1.2, a, b, c)
+    host = kw.Device.host()
+    monkeypatch.setenv("KW_E2E_MIN_INTENSITY", "0")  # streamed at this size
+    results, errors = {}, []
+    bufs = {}
+    for t in range(3):
+        hA, hB, hC = (kw.Buffer(host, kw.IndexVec(*x.shape), 8) for x in (a, b, c))
+        for hb, x in ((hA, a), (hB, b), (hC, c)):
+            hb.host_view()[:, : x.shape[1]] = x
+        bufs[t] = (hA, hB, hC)
+
+    def worker(t):
+        try:
+            hA, hB, hC = bufs[t]
+            q = kw.Queue(gpu, kw.QueueFlavor.Async)
+            q.enqueue(kw.createExec(GPU, kw.gemmTiledWorkDiv(GPU, m, n, 128), kw.GemmTiledKernel(),
+                                    kw.GemmArgs(m, n, k, 0.8, 1.2, hA, hB, hC)))
+            q.wait()
+            results[t] = hC.host_view()[:, :n].copy()
+        except Exception as ex:  # noqa: BLE001
+            errors.append(ex)
+
+    threads = [threading.Thread(target=worker, args=(t,)) for t in range(3)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors
+    for t in range(3):
+        assert np.array_equal(results[t], want), t
