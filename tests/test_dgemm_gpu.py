@@ -726,3 +726,26 @@ def test_host_operand_schedules_from_fresh_threads(gpu, monkeypatch):
     assert not errors, errors
     for t in range(3):
         assert np.array_equal(results[t], want), t
+
+
+@pytest.mark.parametrize("cfg", [18, 20, 24, 25, 26])
+def test_split_and_group_configs_read_c_when_beta_is_zero(gpu, cfg):
+    """gemm.cpp:35 / 115 (beta multiplies C even when 0) on the SPLIT / two-group walks: NaNs
+    planted in C — in head, tail and full tiles — come out as NaN, everything else is finite."""
+    lib = L.lib()
+    rng = np.random.default_rng(cfg)
+    m, n, k = 1100, 1300, 300
+    a, b, c = rng.random((m, k)), rng.random((k, n)), rng.random((m, n))
+    spots = [(0, 0), (63, 127), (64, 128), (517, 733), (1099, 1299), (600, 5)]
+    for r, col in spots:
+        c[r, col] = np.nan
+    A, B, Cb = mat(gpu, a), mat(gpu, b), mat(gpu, c)
+    q = kw.Queue(gpu, kw.QueueFlavor.Async)
+    assert lib.kw_dgemm_with_config(q.handle(), cfg, m, n, k, 1.0, A.data(), A.leadingDim(), B.data(), B.leadingDim(),
+                                    0.0, Cb.data(), Cb.leadingDim()) == 0
+    q.wait()
+    out = Cb.download()
+    mask = np.zeros_like(out, dtype=bool)
+    for r, col in spots:
+        mask[r, col] = True
+    assert np.isnan(out[mask]).all() and np.isfinite(out[~mask]).all()
