@@ -749,3 +749,33 @@ def test_split_and_group_configs_read_c_when_beta_is_zero(gpu, cfg):
     for r, col in spots:
         mask[r, col] = True
     assert np.isnan(out[mask]).all() and np.isfinite(out[~mask]).all()
+
+
+def test_split_scratch_follows_queue_lifetime(gpu):
+    """Queues created and destroyed around SPLIT launches (per-stream ticket / flag / park scratch,
+    released with the queue — a later queue may get the same stream handle), with launches still
+    in flight at destruction: every result equals the one-CTA-per-tile launch."""
+    lib = L.lib()
+    rng = np.random.default_rng(21)
+    n = 1024
+    a, b, c = rng.random((n, n)), rng.random((n, n)), rng.random((n, n))
+    A, B = mat(gpu, a), mat(gpu, b)
+    ref = mat(gpu, c)
+    q0 = kw.Queue(gpu, kw.QueueFlavor.Async)
+    assert lib.kw_dgemm_with_config(q0.handle(), 17, n, n, n, 1.0, A.data(), A.leadingDim(), B.data(), B.leadingDim(),
+                                    0.5, ref.data(), ref.leadingDim()) == 0
+    q0.wait()
+    want = ref.download()
+    outs = []
+    for it in range(12):
+        q = kw.Queue(gpu, kw.QueueFlavor.Async)
+        Cb = mat(gpu, c)
+        for cfg in (18, 25, 21) if it % 2 else (20, 18):
+            q.wait()  # the upload below runs on another queue: the previous launch must be done
+            Cb.upload(c)
+            assert lib.kw_dgemm_with_config(q.handle(), cfg, n, n, n, 1.0, A.data(), A.leadingDim(), B.data(),
+                                            B.leadingDim(), 0.5, Cb.data(), Cb.leadingDim()) == 0
+        del q  # destroyed with the last launch possibly still running (the destructor drains it)
+        outs.append(Cb)
+    for Cb in outs:
+        assert np.array_equal(Cb.download(), want)
