@@ -375,6 +375,9 @@ __device__ __forceinline__ void wait_ready(const uint32_t* flag, uint32_t* abort
     }
 }
 
+#ifndef KW_DGEMM_AHEAD2
+#define KW_DGEMM_AHEAD2 1 // two-step fragment prefetch for small warp tiles (A/B: -DKW_DGEMM_AHEAD2=0)
+#endif
 template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int MIN_BLOCKS_ = 1, bool PAIRED_ = false,
           int GROUPS_ = 1>
 struct TmaCfg {
@@ -836,7 +839,55 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
                 bf[j] = *reinterpret_cast<const double*>(sb + (j >> 1) * 2048 + (b_ev[ks] ^ ((j & 1) ? 64u : 0u)));
         };
         // A pairs double-buffered (one LDS.128 per row block covers two k-steps); B fragments
-        // one k-step ahead.
+        // one k-step ahead — or, for small warp tiles (AHEAD2), two k-steps ahead from four
+        // buffers and the next stage's first A pairs one k-step earlier: 8 DMMAs per k-step
+        // are too few to cover a fragment load issued one step ahead.
+        constexpr bool AHEAD2 = KW_DGEMM_AHEAD2 && Cfg::MT * Cfg::NT <= 8;
+        if constexpr (AHEAD2) {
+        double2 a2[2][Cfg::MT];
+        double bf[4][Cfg::NT];
+        if (nkt > 0) {
+            const int s0 = it0 % Cfg::STAGES;
+            mbar_wait(&full[s0], static_cast<uint32_t>(it0 / Cfg::STAGES) & 1u);
+            load_a2(ring + s0 * Cfg::STAGE_BYTES, 0, a2[0]);
+            load_b(ring + s0 * Cfg::STAGE_BYTES, 0, bf[0]);
+            load_b(ring + s0 * Cfg::STAGE_BYTES, 1, bf[1]);
+        }
+        for (int kt = 0; kt < nkt; ++kt) {
+            const int s = (it0 + kt) % Cfg::STAGES;
+            const uint8_t* sa = ring + s * Cfg::STAGE_BYTES;
+            const uint8_t* sa2 = sa;
+            const bool more = kt + 1 < nkt;
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {
+                const int q = ks >> 1, h = ks & 1;
+                if (ks == 0)
+                    load_a2(sa, 1, a2[1]);
+                if (ks < 2)
+                    load_b(sa, ks + 2, bf[ks + 2]);
+                else if (more) {
+                    if (ks == 2) {
+                        const int s2 = (it0 + kt + 1) % Cfg::STAGES;
+                        mbar_wait(&full[s2], static_cast<uint32_t>((it0 + kt + 1) / Cfg::STAGES) & 1u);
+                        sa2 = ring + s2 * Cfg::STAGE_BYTES;
+                        load_a2(sa2, 0, a2[0]); // a2[0] is idle during k-steps 2 and 3
+                    }
+                    load_b(sa2, ks - 2, bf[ks - 2]);
+                }
+#pragma unroll
+                for (int i = 0; i < Cfg::MT; ++i)
+#pragma unroll
+                    for (int j = 0; j < Cfg::NT; ++j)
+                        dmma_8x8x4(acc[i][j][0], acc[i][j][1], h ? a2[q][i].y : a2[q][i].x, bf[ks][j]);
+                if (ks == 3) {
+                    __syncwarp(); // stage s fully consumed (below)
+                    if (lane == 0)
+                        mbar_arrive(&empty[s]);
+                }
+            }
+        }
+        }
+        else {
         double2 a2[2][Cfg::MT];
         double bf[2][Cfg::NT];
         if (nkt > 0) {
@@ -882,6 +933,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
                         mbar_arrive(&empty[s]);
                 }
             }
+        }
         }
     }
     else {
@@ -1883,10 +1935,12 @@ int pick_config(const GemmParams& p)
 // Resident launches add the SPLIT configurations (one CTA per SM over equal (tile, k-tile)
 // ranges — same paired DMMA sequence, so again no bit changes) where both data-parallel grids
 // quantise badly: the busiest SM of the better of 16 / 17 carries more than 1/0.93 of the mean
-// output (1024^3: 2 of 1.73 tiles, 0.865 -> split 18 at 30.2 vs 26.9 TFLOP/s; 1280^3: 0.90 ->
-// split 20 at 31.9 vs 28.7; profiles/dgemm_split_sweep_r02.txt). Split 20 (64 x 128 tiles, 8
-// warps of 32 x 32) where it still gives every SM a tile, else split 18 (64 x 64, 8 of 32 x 16).
-constexpr int kCfgSplit64 = 18, kCfgSplit128 = 20, kCfgSplitPair = 25;
+// output (1024^3: 2 of 1.73 tiles, 0.865 -> split 18 at 30.8 vs 27.6 TFLOP/s). Split 18 (64 x 64,
+// 8 warps of 32 x 16 with the two-step fragment prefetch) up to 2.5 tiles of 64 x 128 per SM,
+// the two-group split 25 above (1280^3 18: 32.2 vs 20: 31.8; 1664^3 18: 33.0 vs 25: 32.8;
+// 1792^3 25: 33.4 vs 20: 33.1 vs 18: 33.0; profiles/dgemm_split_sweep_r02.txt). Split 20 (64 x 128,
+// 8 warps of 32 x 32) led 18 before the prefetch change and stays selectable (kw_dgemm_with_config).
+constexpr int kCfgSplit64 = 18, kCfgSplitPair = 25;
 int pick_resident(const GemmParams& p)
 {
     const double sms = sm_count();
@@ -1896,7 +1950,7 @@ int pick_resident(const GemmParams& p)
     const double q16 = ideal / (std::ceil(t16 / sms) * 8192.0), q17 = ideal / (std::ceil(t17 / sms) * 4096.0);
     const long long ktiles = (p.k + 15) / 16;
     if (std::max(q16, q17) < 0.93 && t17 >= static_cast<long long>(sms) && ktiles >= 2 && tma_eligible(p))
-        return t16 >= static_cast<long long>(sms) ? kCfgSplit128 : kCfgSplit64;
+        return 2 * t16 >= 5 * static_cast<long long>(sms) ? kCfgSplitPair : kCfgSplit64;
     // Mid-size outputs (2 to 16 tiles of 64 x 128 per consumer group) whose 64 x 128 grid leaves a
     // partial last wave: the two-group SPLIT config (config 16's geometry twice in one CTA, equal
     // k-tile ranges) — 2048^3 34.3 vs 34.0, 3072^3 35.0 vs 34.4, 3584^3 35.1 vs 34.2, 6144^3

@@ -1,4 +1,4 @@
-"""Long soak of the tile configurations the library picks (data-parallel 16/17, SPLIT 18/20/24/25,
+"""Long soak of the tile configurations the library picks (data-parallel 16/17, SPLIT 18/20/23/24/25,
 two-group 26): random shapes (ragged, small and large k, padded leading dimensions), random
 scalars, signed inputs; every configuration must give the bits of config 17, and config 17 must be
 within (K+4)u of gemmReference (scaled by |alpha||A||B| + |beta||C| for signed data) on a subset.
@@ -15,7 +15,7 @@ from oracle import oracle as O  # noqa: E402  (test infrastructure: the checker)
 from paper_1602_08477_b200 import _lib as L  # noqa: E402
 from paper_1602_08477_b200 import kernelweave as kw  # noqa: E402
 
-CFGS = (16, 18, 20, 24, 25, 26)
+CFGS = (16, 18, 20, 23, 24, 25, 26)
 
 
 def main():
