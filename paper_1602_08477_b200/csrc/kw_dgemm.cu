@@ -375,6 +375,12 @@ __device__ __forceinline__ void wait_ready(const uint32_t* flag, uint32_t* abort
     }
 }
 
+#ifndef KW_DGEMM_REG_PREFETCH_C
+#define KW_DGEMM_REG_PREFETCH_C 1 // 1-CTA/SM SPLIT tiles: C read into registers at tile start
+#endif
+#ifndef KW_DGEMM_C_L2PF
+#define KW_DGEMM_C_L2PF 1 // L2 prefetch of the C block at tile start (A/B: -DKW_DGEMM_C_L2PF=0)
+#endif
 #ifndef KW_DGEMM_AHEAD2
 #define KW_DGEMM_AHEAD2 1 // two-step fragment prefetch for small warp tiles (A/B: -DKW_DGEMM_AHEAD2=0)
 #endif
@@ -775,9 +781,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
                 *f = 0; // consumed: the flags are all zero again when the launch ends
         }
     }
-    // One CTA per SM (SPLIT, MIN_BLOCKS 1): no co-resident CTA covers this tile's epilogue, so
-    // its C reads are issued now and land during the main loop (C belongs to this tile alone).
-    constexpr bool PREFETCH_C = SPLIT && Cfg::MIN_BLOCKS == 1 && Cfg::MT * Cfg::NT <= 16; // registers
+    // One CTA per SM (SPLIT, MIN_BLOCKS 1) with a small warp tile: no co-resident CTA covers this
+    // tile's epilogue, so its C reads are issued now into registers and land during the main loop
+    // (C belongs to this tile alone). Larger warp tiles take the L2 prefetch below instead (split
+    // 20 at 1280^3: 32.6 vs 31.8 TFLOP/s with the register copy).
+    constexpr bool PREFETCH_C = KW_DGEMM_REG_PREFETCH_C && SPLIT && Cfg::MIN_BLOCKS == 1 && Cfg::MT * Cfg::NT <= 8;
     double2 cpre[PREFETCH_C ? Cfg::MT : 1][PREFETCH_C ? Cfg::NT : 1];
     if constexpr (PREFETCH_C) {
         if (kt1 == ktiles) {
@@ -795,6 +803,18 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
                         cpre[i][j].y = (row < p.m && col + 1 < p.n) ? crow[col + 1] : 0.0;
                     }
                 }
+            }
+        }
+    }
+    // Other resident configurations: pull this tile's C block into L2 now (prefetch.global.L2,
+    // no registers), so the epilogue's reads return from L2 rather than HBM.
+    if constexpr (!PREFETCH_C && !STREAMED && KW_DGEMM_C_L2PF) {
+        if (kt1 == ktiles) {
+            constexpr int SEGS = Cfg::WN / 16; // 128-byte lines per warp-tile row
+            for (int idx = lane; idx < Cfg::WM * SEGS; idx += 32) {
+                const int row = bm + wm + idx / SEGS, col = bn + wn + (idx % SEGS) * 16;
+                if (row < p.m && col < p.n)
+                    asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p.c + static_cast<size_t>(row) * p.ldc + col));
             }
         }
     }
@@ -1935,12 +1955,11 @@ int pick_config(const GemmParams& p)
 // Resident launches add the SPLIT configurations (one CTA per SM over equal (tile, k-tile)
 // ranges — same paired DMMA sequence, so again no bit changes) where both data-parallel grids
 // quantise badly: the busiest SM of the better of 16 / 17 carries more than 1/0.93 of the mean
-// output (1024^3: 2 of 1.73 tiles, 0.865 -> split 18 at 30.8 vs 27.6 TFLOP/s). Split 18 (64 x 64,
-// 8 warps of 32 x 16 with the two-step fragment prefetch) up to 2.5 tiles of 64 x 128 per SM,
-// the two-group split 25 above (1280^3 18: 32.2 vs 20: 31.8; 1664^3 18: 33.0 vs 25: 32.8;
-// 1792^3 25: 33.4 vs 20: 33.1 vs 18: 33.0; profiles/dgemm_split_sweep_r02.txt). Split 20 (64 x 128,
-// 8 warps of 32 x 32) led 18 before the prefetch change and stays selectable (kw_dgemm_with_config).
-constexpr int kCfgSplit64 = 18, kCfgSplitPair = 25;
+// output (1024^3: 2 of 1.73 tiles, 0.865 -> split 18 at 30.8 vs 27.6 TFLOP/s). By tiles of
+// 64 x 128 per SM: below 1, split 18 (64 x 64, 8 warps of 32 x 16, C prefetched into registers);
+// 1 to 2.5, split 20 (64 x 128, 8 warps of 32 x 32; 1280^3 32.6 vs 18: 32.2); above, the
+// two-group split 25 (1792^3 33.9 vs 20: 33.7). profiles/dgemm_prefetch_ab_r02.txt.
+constexpr int kCfgSplit64 = 18, kCfgSplit128 = 20, kCfgSplitPair = 25;
 int pick_resident(const GemmParams& p)
 {
     const double sms = sm_count();
@@ -1950,7 +1969,9 @@ int pick_resident(const GemmParams& p)
     const double q16 = ideal / (std::ceil(t16 / sms) * 8192.0), q17 = ideal / (std::ceil(t17 / sms) * 4096.0);
     const long long ktiles = (p.k + 15) / 16;
     if (std::max(q16, q17) < 0.93 && t17 >= static_cast<long long>(sms) && ktiles >= 2 && tma_eligible(p))
-        return 2 * t16 >= 5 * static_cast<long long>(sms) ? kCfgSplitPair : kCfgSplit64;
+        return 2 * t16 >= 5 * static_cast<long long>(sms) ? kCfgSplitPair
+               : t16 >= static_cast<long long>(sms)       ? kCfgSplit128
+                                                          : kCfgSplit64;
     // Mid-size outputs (2 to 16 tiles of 64 x 128 per consumer group) whose 64 x 128 grid leaves a
     // partial last wave: the two-group SPLIT config (config 16's geometry twice in one CTA, equal
     // k-tile ranges) — 2048^3 34.3 vs 34.0, 3072^3 35.0 vs 34.4, 3584^3 35.1 vs 34.2, 6144^3

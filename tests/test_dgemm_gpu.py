@@ -556,7 +556,7 @@ def test_paired_configs_are_bitwise_interchangeable(gpu, oracle):
         assert within_tol(outs[0], oracle.gemm(0.9, 1.1, a, b, c), k)[0]
 
 
-@pytest.mark.parametrize("m,n,k", [(1024, 1024, 1024), (1280, 1280, 640), (1100, 1000, 2000), (1792, 1792, 512)])
+@pytest.mark.parametrize("m,n,k", [(1024, 1024, 1024), (1280, 1280, 640), (1100, 1000, 2000), (1792, 1792, 512), (1536, 1408, 700)])
 def test_default_choice_split_is_bitwise_the_one_cta_tile(gpu, oracle, m, n, k):
     """Shapes the library now runs with a SPLIT configuration (badly quantised data-parallel
     grids): the default kw_dgemm result equals the one-CTA-per-tile config 17 bit for bit and the
