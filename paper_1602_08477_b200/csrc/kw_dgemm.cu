@@ -2070,8 +2070,16 @@ uint32_t split_take_abort(cudaStream_t s)
     for (SplitScratch* x : g_split)
         if (x->device == dev && x->stream == s && x->abort_host) {
             const uint32_t v = *reinterpret_cast<volatile uint32_t*>(x->abort_host);
-            if (v)
+            if (v) {
+                // A timed-out wait leaves head flags raised that no tail consumed: clear the
+                // ticket and every flag (not the abort pointer, words 2-3) before the next launch.
                 x->abort_host[0] = 0;
+                cudaStreamSynchronize(s);
+                cudaMemsetAsync(x->flags, 0, 8, s);
+                if (x->flag_words > 4)
+                    cudaMemsetAsync(x->flags + 4, 0, (x->flag_words - 4) * sizeof(uint32_t), s);
+                cudaStreamSynchronize(s);
+            }
             return v;
         }
     return 0;
