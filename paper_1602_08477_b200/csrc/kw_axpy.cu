@@ -408,6 +408,30 @@ kw_status run_staged(kw::Queue* q, uint32_t threads, uint32_t elems, size_t limi
     return kw::after_enqueue(q, "axpy");
 }
 
+// Zero-copy (host-resident operands): the kernel itself loads X and Y from, and stores Y to,
+// page-locked host memory over PCIe (the pinned pages are mapped into the device address space),
+// instead of the copy engines staging chunks through device scratch. Same kernel, same bits.
+// KW_AXPY_ZEROCOPY=0/1 overrides the default (A/B measurements).
+bool axpy_zero_copy_policy()
+{
+    static const bool on = [] {
+        const char* e = std::getenv("KW_AXPY_ZEROCOPY");
+        return e ? e[0] == '1' : false;
+    }();
+    return on;
+}
+
+// Device-side address of a pinned host pointer (nullptr: not pinned-and-mapped).
+const void* mapped_host_ptr(const void* p)
+{
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+}
+
 template <typename T>
 kw_status axpy_entry(kw_queue qh, const kw_workdiv* wd, size_t n, T alpha, const T* x, T* y)
 {
@@ -440,6 +464,14 @@ kw_status axpy_entry(kw_queue qh, const kw_workdiv* wd, size_t n, T alpha, const
     if (x_dev && y_dev) {
         launch_device<T>(q->stream, blocks, threads, elems, limit, alpha, x, y);
         return kw::after_enqueue(q, "axpy");
+    }
+    if (axpy_zero_copy_policy()) {
+        const T* xm = x_dev ? x : static_cast<const T*>(mapped_host_ptr(x));
+        T* ym = y_dev ? y : static_cast<T*>(const_cast<void*>(mapped_host_ptr(y)));
+        if (xm && ym) {
+            launch_device<T>(q->stream, blocks, threads, elems, limit, alpha, xm, ym);
+            return kw::after_enqueue(q, "axpy");
+        }
     }
     return run_staged<T>(q, threads, elems, limit, alpha, x, y, x_dev, y_dev);
 }

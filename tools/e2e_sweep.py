@@ -30,7 +30,7 @@ def main():
         q.wait()
         ts.append(time.perf_counter() - t)
     best, med = min(ts), float(np.median(ts))
-    print(f"chunk_mb={os.environ.get('KW_STAGE_CHUNK_MB', '32')} ramp={os.environ.get('KW_STAGE_RAMP', '1')} median {med*1e3:.2f} ms {12*n/med/1e9:.1f} GB/s "
+    print(f"zerocopy={os.environ.get('KW_AXPY_ZEROCOPY', '0')} chunk_mb={os.environ.get('KW_STAGE_CHUNK_MB', '32')} median {med*1e3:.2f} ms {12*n/med/1e9:.1f} GB/s "
           f"best {12*n/best/1e9:.1f} GB/s")
 
 
