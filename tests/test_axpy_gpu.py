@@ -275,3 +275,43 @@ def test_mixed_host_and_device_operands(gpu, oracle):
     yd = vec(gpu, ys, np.float32)
     assert L.lib().kw_axpy_f32(q.handle(), None, n, float(alpha), xs.ctypes.data, yd.data()) == 0
     assert np.array_equal(yd.download(), want)
+
+
+def test_zero_copy_host_path_matches_oracle(gpu, oracle):
+    """KW_AXPY_ZEROCOPY=1 (read once per process, so in a subprocess): the kernel loads X, Y from
+    and stores Y to the mapped pinned host pages directly. Same bits as the oracle for fp32 and
+    fp64, ragged n, pinned x with pinned y and with a device y; pageable operands still take the
+    staged path."""
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import sys, numpy as np
+sys.path.insert(0, '.')
+from oracle import oracle as O
+from paper_1602_08477_b200 import _lib as L, kernelweave as kw
+gpu = kw.Device.gpu(0); GPU = kw.BackendKind.GpuCudaRt; host = kw.Device.host()
+q = kw.Queue(gpu, kw.QueueFlavor.Async)
+for dt, esz, n in ((np.float32, 4, (1 << 22) + 5), (np.float64, 8, (1 << 21) + 3)):
+    alpha, xs, ys = O.workload_axpy(n, 77, dt == np.float32)
+    want = O.axpy(alpha, xs, ys)
+    x = kw.Buffer(host, kw.IndexVec(n), esz); y = kw.Buffer(host, kw.IndexVec(n), esz)
+    x.host_view()[:n] = xs; y.host_view()[:n] = ys
+    q.enqueue(kw.createExec(GPU, kw.axpyWorkDiv(GPU, n, 256, 4), kw.AxpyKernel(), kw.AxpyArgs(n, alpha, x, y)))
+    q.wait()
+    assert np.array_equal(y.host_view()[:n], want), dt
+    yd = kw.Buffer(gpu, kw.IndexVec(n), esz); yd.upload(ys)
+    q.enqueue(kw.createExec(GPU, kw.axpyWorkDiv(GPU, n, 256, 4), kw.AxpyKernel(), kw.AxpyArgs(n, alpha, x, yd)))
+    q.wait()
+    assert np.array_equal(yd.download(), want), dt
+    xp, yp = np.ascontiguousarray(xs), ys.copy()
+    fn = L.lib().kw_axpy_f32 if esz == 4 else L.lib().kw_axpy_f64
+    assert fn(q.handle(), None, n, float(alpha), xp.ctypes.data, yp.ctypes.data) == 0
+    q.wait()
+    assert np.array_equal(yp, want), dt
+print("ZEROCOPY OK")
+"""
+    env = dict(os.environ, KW_AXPY_ZEROCOPY="1")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                         cwd=str(__import__("pathlib").Path(__file__).resolve().parent.parent), timeout=300)
+    assert "ZEROCOPY OK" in out.stdout, out.stdout + out.stderr
