@@ -1939,8 +1939,13 @@ constexpr int kNumCfgs = sizeof(kCfgs) / sizeof(kCfgs[0]);
 //   16: 64x128 tile, 2 CTAs/SM (best from ~1536 up: 35.4 TFLOP/s at 8192^3, 34.7 at 4096^3)
 //   17: 64x64 tile, 3 CTAs/SM  (best for small outputs: 26.4 at 1024^3, 33.0 at 2048^3)
 // Model: the busiest SM's output count, ceil(tiles / SMs) * tile area; take 17 when that is >3%
-// lower, or when 16 would not give every SM a tile (1 CTA per SM under-feeds the DMMA pipe).
+// lower, or when 16 would not give every SM a tile (1 CTA per SM under-feeds the DMMA pipe), or
+// for short k (< 1408): short k-loops make the per-tile epilogue a larger share, which three
+// co-resident CTAs hide better (8192 x 8192 x 256: 33.1 vs 32.0 TFLOP/s; x 1024: 35.3 vs 34.9;
+// 3000 x 5000 x 700: 32.9 vs 32.1; at k = 1536 16 leads again, 4096^2 x 1536: 35.06 vs 34.96 —
+// profiles/dgemm_rect_r02.txt).
 constexpr int kCfgWide = 16, kCfgSmall = 17;
+constexpr int kShortK = 1408;
 
 int pick_config(const GemmParams& p)
 {
@@ -1948,7 +1953,8 @@ int pick_config(const GemmParams& p)
     const long long rows = (p.m + 63) / 64;
     const long long t16 = rows * ((p.n + 127) / 128), t17 = rows * ((p.n + 63) / 64);
     const long long load16 = (t16 + sms - 1) / sms * 8192, load17 = (t17 + sms - 1) / sms * 4096;
-    const bool small = t16 <= sms || static_cast<double>(load17) < 0.97 * static_cast<double>(load16);
+    const bool small =
+        t16 <= sms || p.k < kShortK || static_cast<double>(load17) < 0.97 * static_cast<double>(load16);
     return small ? kCfgSmall : kCfgWide;
 }
 
@@ -1977,8 +1983,11 @@ int pick_resident(const GemmParams& p)
     // k-tile ranges) — 2048^3 34.3 vs 34.0, 3072^3 35.0 vs 34.4, 3584^3 35.1 vs 34.2, 6144^3
     // 35.4 vs 35.1 TFLOP/s; where config 16's waves come out whole (4096^3: 6.92 of 7) or are many
     // (>= 7168^3) the data-parallel grid stays ahead (profiles/dgemm_split_sweep_r02.txt).
+    // (Not for k < 1536 where config 17's grid quantises well: 2304^2 x 768 17: 33.2 vs 25: 32.0,
+    // 6144^2 x 768 34.8 vs 33.8, 6144^2 x 1280 35.1 vs 34.6, 3000 x 5000 x 1024 33.4 vs 33.1.)
+    const bool short_k_17 = p.k < 1536 && q17 >= 0.95;
     if (t16 >= 2 * static_cast<long long>(sms) && t16 <= 32 * static_cast<long long>(sms) && q16 < 0.985 &&
-        ktiles >= 2 && tma_eligible(p))
+        !short_k_17 && ktiles >= 2 && tma_eligible(p))
         return kCfgSplitPair;
     return pick_config(p);
 }
