@@ -564,8 +564,14 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
             }
         }
         else if constexpr (KRANGE) {
-            kt0 = p.npr;
-            kt1 = p.npc;
+            if (p.panel_cols > 0) { // split-k: slice blockIdx.y of p.panel_cols k-tiles
+                kt0 = static_cast<int>(blockIdx.y) * p.panel_cols;
+                kt1 = kt0 + p.panel_cols < ktiles ? kt0 + p.panel_cols : ktiles;
+            }
+            else {
+                kt0 = p.npr;
+                kt1 = p.npc;
+            }
         }
         else {
             kt0 = 0;
@@ -742,7 +748,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     if constexpr (STREAMED || KRANGE) {
         const size_t tid_tile = static_cast<size_t>(bm / Cfg::BM) * p.tiles_n + bn / Cfg::BN;
         park = reinterpret_cast<double2*>(p.partial) + (tid_tile * Cfg::CONSUMERS + lw) * (Cfg::MT * Cfg::NT) * 32 + lane;
+        if (KRANGE && p.panel_cols > 0) // split-k: slice s parks into its own copy of the tile grid
+            park += static_cast<size_t>(blockIdx.y) * p.tiles_m * p.tiles_n * Cfg::CONSUMERS * (Cfg::MT * Cfg::NT) * 32;
     }
+    // split-k slices start from zero and always park (splitk_reduce sums them and runs the epilogue)
+    const bool splitk = KRANGE && p.panel_cols > 0;
     // SPLIT: a tail piece reloads slot ticket - 1 (its head ran on the previous ticket), a head
     // piece parks into slot ticket.
     uint32_t* split_flags = SPLIT ? p.ready + 4 : nullptr;
@@ -809,7 +819,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     // Other resident configurations: pull this tile's C block into L2 now (prefetch.global.L2,
     // no registers), so the epilogue's reads return from L2 rather than HBM.
     if constexpr (!PREFETCH_C && !STREAMED && KW_DGEMM_C_L2PF) {
-        if (kt1 == ktiles) {
+        if (kt1 == ktiles && !splitk) {
             constexpr int SEGS = Cfg::WN / 16; // 128-byte lines per warp-tile row
             for (int idx = lane; idx < Cfg::WM * SEGS; idx += 32) {
                 const int row = bm + wm + idx / SEGS, col = bn + wn + (idx % SEGS) * 16;
@@ -820,7 +830,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     }
     stamp(2 + 2 * tile);
     if constexpr (STREAMED || KRANGE) {
-        if (kt0 > 0) {
+        if (kt0 > 0 && !splitk) {
 #pragma unroll
             for (int i = 0; i < Cfg::MT; ++i)
 #pragma unroll
@@ -1018,7 +1028,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
         }
     }
     if constexpr (STREAMED || KRANGE) {
-        if (kt1 < ktiles) {
+        if (kt1 < ktiles || splitk) {
             // first pass of a k-split: park the accumulators; the second pass (streamed: same
             // CTA, same thread, later in this loop; k-range: the next launch) reloads them and
             // runs the epilogue
@@ -1157,10 +1167,10 @@ bool dgemm_pdl()
 // launch (measured: the 64 x 64 three-CTA tile at 1024^3 fell from 26.9 to 18.0 TFLOP/s).
 template <class Cfg, bool STREAMED, bool SPLIT, bool KRANGE = false>
 cudaError_t launch_tma_kernel(unsigned grid, cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb,
-                              const GemmParams& p, bool pdl)
+                              const GemmParams& p, bool pdl, unsigned grid_y = 1)
 {
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
+    cfg.gridDim = dim3(grid, grid_y);
     cfg.blockDim = dim3(Cfg::THREADS);
     cfg.dynamicSmemBytes = Cfg::SMEM;
     cfg.stream = s;
@@ -1876,11 +1886,149 @@ kw_status launch_krange(cudaStream_t s, const GemmParams& p0, int kt0, int kt1, 
     p.npc = kt1;
     p.partial = park;
     p.panel_rows = dgemm_group();
+    p.panel_cols = 0; // not split-k (launch_splitk)
     const long long resident = static_cast<long long>(sm_count()) * Cfg::MIN_BLOCKS;
     if (cudaError_t e = launch_tma_kernel<Cfg, false, false, true>(static_cast<unsigned>(tiles), s, ma, mb, p,
                                                                    tiles >= resident))
         return kw::cuda_fail("dgemm (k-range): launch", e);
     kw::g_launches.fetch_add(1, std::memory_order_relaxed);
+    return KW_OK;
+}
+
+// Split-k park (per stream, the SplitScratch entry's park buffer; no tickets or flags involved).
+kw_status splitk_park(cudaStream_t s, size_t bytes, double** park)
+{
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(g_split_mu);
+    SplitScratch* sc = nullptr;
+    for (SplitScratch* x : g_split)
+        if (x->device == dev && x->stream == s)
+            sc = x;
+    if (!sc) {
+        sc = new SplitScratch;
+        sc->device = dev;
+        sc->stream = s;
+        g_split.push_back(sc);
+    }
+    if (sc->park_bytes < bytes) {
+        cudaStreamSynchronize(s); // earlier launches on this stream may still use the old park
+        cudaFree(sc->park);
+        sc->park = nullptr;
+        sc->park_bytes = 0;
+        if (cudaError_t e = cudaMalloc(&sc->park, bytes))
+            return kw::cuda_fail("dgemm split-k: park scratch", e);
+        sc->park_bytes = bytes;
+    }
+    *park = sc->park;
+    return KW_OK;
+}
+
+// Split-k reduction: C = alpha * (P_0 + P_1 + ... + P_{S-1}) + beta * C over the S partial
+// chains of launch_splitk, added in slice order (deterministic); one CTA per tile, one thread per
+// (consumer warp, lane) fragment set of the park layout, the main kernel's epilogue arithmetic.
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::CONSUMERS * 32) splitk_reduce_kernel(GemmParams p, int slices)
+{
+    const int tile = blockIdx.x;
+    const int tr = tile / p.tiles_n, tc = tile - tr * p.tiles_n;
+    const int lw = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const int wm = (lw / Cfg::WARPS_N) * Cfg::WM, wn = (lw % Cfg::WARPS_N) * Cfg::WN;
+    const size_t stride = static_cast<size_t>(p.tiles_m) * p.tiles_n * Cfg::CONSUMERS * (Cfg::MT * Cfg::NT) * 32;
+    const double2* base = reinterpret_cast<const double2*>(p.partial) +
+                          (static_cast<size_t>(tile) * Cfg::CONSUMERS + lw) * (Cfg::MT * Cfg::NT) * 32 + lane;
+    const bool c_vec = (p.ldc % 2 == 0) && (reinterpret_cast<uintptr_t>(p.c) % 16 == 0);
+    for (int i = 0; i < Cfg::MT; ++i) {
+        const int row = tr * Cfg::BM + wm + i * 8 + g;
+        if (row >= p.m)
+            continue;
+        double* crow = p.c + static_cast<size_t>(row) * p.ldc;
+        for (int j = 0; j < Cfg::NT; ++j) {
+            const int col = tc * Cfg::BN + wn + j * 8 + 2 * t;
+            if (col >= p.n)
+                continue;
+            const double2* src = base + (i * Cfg::NT + j) * 32;
+            double2 acc = __ldcs(src);
+            for (int sl = 1; sl < slices; ++sl) {
+                const double2 v = __ldcs(src + sl * stride);
+                acc.x = __dadd_rn(acc.x, v.x);
+                acc.y = __dadd_rn(acc.y, v.y);
+            }
+            double2 old;
+            if (c_vec && col + 1 < p.n)
+                old = *reinterpret_cast<const double2*>(crow + col);
+            else {
+                old.x = crow[col];
+                old.y = col + 1 < p.n ? crow[col + 1] : 0.0;
+            }
+            const double x = __dadd_rn(__dmul_rn(p.alpha, acc.x), __dmul_rn(p.beta, old.x));
+            const double y = __dadd_rn(__dmul_rn(p.alpha, acc.y), __dmul_rn(p.beta, old.y));
+            if (c_vec && col + 1 < p.n)
+                *reinterpret_cast<double2*>(crow + col) = make_double2(x, y);
+            else {
+                crow[col] = x;
+                if (col + 1 < p.n)
+                    crow[col + 1] = y;
+            }
+        }
+    }
+}
+
+// Split-k for small outputs with long k (fewer 64 x 64 tiles than SMs): the one-CTA-per-tile
+// chain leaves most SMs idle (512 x 512 x 16384: 64 tiles, 12.3 TFLOP/s) and the SPLIT walk
+// cannot help (a tile's chain is split at most once). Here the k-tiles are cut into S slices,
+// one k-range launch runs every (tile, slice) as an independent chain from zero (grid tiles x
+// S, parked per slice), and splitk_reduce_kernel adds the S partials in slice order and runs the
+// epilogue. Deterministic, within the same (K+4)u bound, but NOT the bits of the one-CTA chain:
+// this is the one resident path whose bits depend on the configuration.
+template <class Cfg>
+kw_status launch_splitk(cudaStream_t s, const GemmParams& p0)
+{
+    GemmParams p = p0;
+    p.tiles_m = static_cast<int>(kw::ceil_div(p.m, Cfg::BM));
+    p.tiles_n = static_cast<int>(kw::ceil_div(p.n, Cfg::BN));
+    const long long tiles = static_cast<long long>(p.tiles_m) * p.tiles_n;
+    const long long ktiles = kw::ceil_div(p.k, Cfg::BK);
+    const long long resident = static_cast<long long>(sm_count()) * Cfg::MIN_BLOCKS;
+    // Slices: as many as keep every SM at <= 2 CTAs (tiles * S <= 2 * SMs; 16..24 k-tiles per
+    // slice at least/most apart): measured best or within 5 % of the best S on 512^2 x 16384
+    // (S = 4: 27.6 TFLOP/s), 768^2 x 8192 (2: 31.7), 512^2 x 4096 (4: 22.3), 512^2 x 2048 (4:
+    // 17.4 vs 11.6 data-parallel) — profiles/dgemm_splitk_r02.txt. KW_SPLITK_SLICES overrides.
+    static const long long env_s = [] {
+        const char* e = std::getenv("KW_SPLITK_SLICES");
+        return e ? std::atoll(e) : 0ll;
+    }();
+    long long S = env_s > 0 ? env_s
+                            : std::min<long long>(24, 2 * static_cast<long long>(sm_count()) / std::max<long long>(tiles, 1));
+    S = std::max<long long>(2, std::min<long long>(S, ktiles / 16));
+    const long long kts = S > 1 ? kw::ceil_div(ktiles, S) : ktiles;
+    S = kw::ceil_div(ktiles, kts);
+    if (S < 2 || tiles > INT_MAX || !tma_eligible(p))
+        return launch_tma<Tma64x64x3p>(s, p0);
+    CUtensorMap ma, mb;
+    if (!make_map(&ma, p.a, p.m, p.k, p.lda, Cfg::BM) || !make_map(&mb, p.b, p.k, p.n, p.ldb, 16))
+        return launch_tma<Tma64x64x3p>(s, p0);
+    double* park = nullptr;
+    kw_status st = splitk_park(s, static_cast<size_t>(S) * tiles * Cfg::CONSUMERS * Cfg::MT * Cfg::NT * 32 * sizeof(double2),
+                               &park);
+    if (st != KW_OK)
+        return st;
+    st = ensure_smem(reinterpret_cast<const void*>(dgemm_tma_kernel<Cfg, false, false, true>), Cfg::SMEM,
+                     "dgemm: cudaFuncSetAttribute");
+    if (st != KW_OK)
+        return st;
+    p.npr = p.npc = 0;
+    p.panel_cols = static_cast<int>(kts); // > 0: split-k slices (dgemm_tma_kernel KRANGE)
+    p.partial = park;
+    p.panel_rows = dgemm_group();
+    if (cudaError_t e = launch_tma_kernel<Cfg, false, false, true>(static_cast<unsigned>(tiles), s, ma, mb, p, false,
+                                                                   static_cast<unsigned>(S)))
+        return kw::cuda_fail("dgemm (split-k): launch", e);
+    splitk_reduce_kernel<Cfg><<<static_cast<unsigned>(tiles), Cfg::CONSUMERS * 32, 0, s>>>(p, static_cast<int>(S));
+    if (cudaError_t e = cudaGetLastError())
+        return kw::cuda_fail("dgemm (split-k): reduction launch", e);
+    kw::g_launches.fetch_add(2, std::memory_order_relaxed);
     return KW_OK;
 }
 
@@ -1929,6 +2077,8 @@ const CfgInfo kCfgs[] = {
      launch_split<Pair64x128>}, // 25
     {Pair64x128::BM, Pair64x128::BN, Pair64x128::BK, Pair64x128::THREADS, Pair64x128::STAGES,
      launch_tma<Pair64x128>}, // 26
+    {Tma64x64x3p::BM, Tma64x64x3p::BN, Tma64x64x3p::BK, Tma64x64x3p::THREADS, Tma64x64x3p::STAGES,
+     launch_splitk<Tma64x64x3p>}, // 27: split-k over config 17 (NOT bitwise-interchangeable)
 };
 constexpr int kNumCfgs = sizeof(kCfgs) / sizeof(kCfgs[0]);
 // Tile choice for the GPU back-end. The tile work division (gemmTiledWorkDiv) is the coverage
@@ -1965,7 +2115,20 @@ int pick_config(const GemmParams& p)
 // 64 x 128 per SM: below 1, split 18 (64 x 64, 8 warps of 32 x 16, C prefetched into registers);
 // 1 to 2.5, split 20 (64 x 128, 8 warps of 32 x 32; 1280^3 32.6 vs 18: 32.2); above, the
 // two-group split 25 (1792^3 33.9 vs 20: 33.7). profiles/dgemm_prefetch_ab_r02.txt.
-constexpr int kCfgSplit64 = 18, kCfgSplit128 = 20, kCfgSplitPair = 25;
+constexpr int kCfgSplit64 = 18, kCfgSplit128 = 20, kCfgSplitPair = 25, kCfgSplitK = 27;
+// Split-k (config 27) below a full wave of 64 x 64 tiles with a long k — opt-in (KW_DGEMM_SPLITK=1):
+// it is the one configuration whose bits differ from the one-CTA chain, and by default every
+// path (resident, host-staged, streamed, row-sharded) gives the same bits, the GPU analogue of
+// the reference's cross-backend determinism (acceptance criterion 01). See launch_splitk.
+constexpr long long kSplitKMinKtiles = 64;
+bool splitk_default()
+{
+    static const bool on = [] {
+        const char* e = std::getenv("KW_DGEMM_SPLITK");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
 int pick_resident(const GemmParams& p)
 {
     const double sms = sm_count();
@@ -1974,6 +2137,8 @@ int pick_resident(const GemmParams& p)
     const double ideal = static_cast<double>(p.m) * p.n / sms;
     const double q16 = ideal / (std::ceil(t16 / sms) * 8192.0), q17 = ideal / (std::ceil(t17 / sms) * 4096.0);
     const long long ktiles = (p.k + 15) / 16;
+    if (splitk_default() && t17 < static_cast<long long>(sms) && ktiles >= kSplitKMinKtiles && tma_eligible(p))
+        return kCfgSplitK;
     if (std::max(q16, q17) < 0.93 && t17 >= static_cast<long long>(sms) && ktiles >= 2 && tma_eligible(p))
         return 2 * t16 >= 5 * static_cast<long long>(sms) ? kCfgSplitPair
                : t16 >= static_cast<long long>(sms)       ? kCfgSplit128

@@ -34,6 +34,9 @@ def mat(dev, a, rows=None, cols=None, align=64):
     return b
 
 
+SPLITK_CFG = 27  # split-k over config 17: deterministic, within tolerance, not the one-CTA chain's bits
+
+
 def within_tol(got, ref, k):
     err = np.abs(got - ref)
     bound = (k + 4) * U * np.abs(ref)
@@ -538,7 +541,7 @@ def test_paired_configs_are_bitwise_interchangeable(gpu, oracle):
     lets the library pick the tile by problem size without breaking the panel and row-shard
     invariance."""
     lib = L.lib()
-    paired = [c for c in range(lib.kw_dgemm_config_count()) if c >= 14]
+    paired = [c for c in range(lib.kw_dgemm_config_count()) if c >= 14 and c != SPLITK_CFG]
     rng = np.random.default_rng(31)
     q = kw.Queue(gpu, kw.QueueFlavor.Async)
     for (m, n, k) in ((300, 260, 170), (1024, 1024, 1024), (129, 640, 48), (1000, 1100, 333), (700, 2000, 50),
@@ -779,3 +782,99 @@ def test_split_scratch_follows_queue_lifetime(gpu):
         outs.append(Cb)
     for Cb in outs:
         assert np.array_equal(Cb.download(), want)
+
+
+@pytest.mark.parametrize("m,n,k", [(512, 512, 16384), (100, 70, 9000), (1, 2, 4200), (768, 700, 5000),
+                                   (512, 512, 1024)])
+def test_splitk_small_output_long_k(gpu, oracle, m, n, k):
+    """Split-k (config 27, opt-in): S independent k-slice chains parked per slice, added in slice
+    order by the reduction kernel, which runs the epilogue. Within (K+4)u of gemmReference and
+    deterministic (two runs give the same bits); the default path (one-CTA chains) stays within
+    tolerance of it but is not required to equal it."""
+    lib = L.lib()
+    rng = np.random.default_rng(m + n + k)
+    a, b, c = rng.random((m, k)) * 10, rng.random((k, n)) * 10, rng.random((m, n)) * 10
+    ref = oracle.gemm(1.25, 0.75, a, b, c, threads=8)
+    q = kw.Queue(gpu, kw.QueueFlavor.Async)
+    outs = []
+    for cfg in (SPLITK_CFG, SPLITK_CFG, None):
+        A, B, Cb = mat(gpu, a), mat(gpu, b), mat(gpu, c)
+        if cfg is None:
+            st = lib.kw_dgemm(q.handle(), None, m, n, k, 1.25, A.data(), A.leadingDim(), B.data(), B.leadingDim(),
+                              0.75, Cb.data(), Cb.leadingDim())
+        else:
+            st = lib.kw_dgemm_with_config(q.handle(), cfg, m, n, k, 1.25, A.data(), A.leadingDim(), B.data(),
+                                          B.leadingDim(), 0.75, Cb.data(), Cb.leadingDim())
+        assert st == 0, L.last_error()
+        q.wait()
+        outs.append(Cb.download())
+    assert np.array_equal(outs[0], outs[1])  # deterministic
+    for o in (outs[0], outs[2]):
+        ok, worst = within_tol(o, ref, k)
+        assert ok, worst
+
+
+def test_splitk_opt_in_default(gpu):
+    """KW_DGEMM_SPLITK=1 (read once per process, so in a subprocess) makes split-k the default
+    choice for fewer 64 x 64 tiles than SMs and k >= 1024: kw_dgemm then equals config 27 bit for
+    bit; without it kw_dgemm equals config 17 (the one-CTA chain)."""
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import sys, numpy as np
+sys.path.insert(0, '.')
+from paper_1602_08477_b200 import _lib as L, kernelweave as kw
+gpu = kw.Device.gpu(0); lib = L.lib(); q = kw.Queue(gpu, kw.QueueFlavor.Async)
+rng = np.random.default_rng(3); m, n, k = 300, 200, 3000
+a, b, c = rng.random((m, k)), rng.random((k, n)), rng.random((m, n))
+def run(cfg):
+    A, B, Cb = (kw.Buffer(gpu, kw.IndexVec(*x.shape), 8) for x in (a, b, c))
+    for t, x in zip((A, B, Cb), (a, b, c)): t.upload(x)
+    if cfg is None:
+        st = lib.kw_dgemm(q.handle(), None, m, n, k, 1.0, A.data(), A.leadingDim(), B.data(), B.leadingDim(), 1.0, Cb.data(), Cb.leadingDim())
+    else:
+        st = lib.kw_dgemm_with_config(q.handle(), cfg, m, n, k, 1.0, A.data(), A.leadingDim(), B.data(), B.leadingDim(), 1.0, Cb.data(), Cb.leadingDim())
+    assert st == 0; q.wait(); return Cb.download()
+d, s27, s17 = run(None), run(27), run(17)
+want = s27 if sys.argv[1] == "1" else s17
+assert np.array_equal(d, want); print("DEFAULT OK")
+"""
+    root = str(__import__("pathlib").Path(__file__).resolve().parent.parent)
+    for flag in ("1", "0"):
+        env = dict(os.environ, KW_DGEMM_SPLITK=flag)
+        out = subprocess.run([sys.executable, "-c", code, flag], capture_output=True, text=True, env=env, cwd=root,
+                             timeout=300)
+        assert "DEFAULT OK" in out.stdout, (flag, out.stdout + out.stderr)
+
+
+def test_splitk_beta_zero_nan_and_odd_ldc(gpu, oracle):
+    """Split-k's reduction runs the epilogue: beta = 0 still reads C (NaN propagates, gemm.cpp:35),
+    and an odd leading dimension of C (scalar stores) keeps every element outside the product
+    untouched."""
+    lib = L.lib()
+    m, n, k = 130, 67, 6000
+    rng = np.random.default_rng(5)
+    a, b = rng.random((m, k)), rng.random((k, n))
+    q = kw.Queue(gpu, kw.QueueFlavor.Async)
+    A, B = mat(gpu, a), mat(gpu, b)
+    c = np.full((m, n), np.nan)
+    c[::2] = 1.0
+    Cb = mat(gpu, c)
+    assert lib.kw_dgemm_with_config(q.handle(), SPLITK_CFG, m, n, k, 1.0, A.data(), A.leadingDim(), B.data(),
+                                    B.leadingDim(), 0.0, Cb.data(), Cb.leadingDim()) == 0
+    q.wait()
+    out = Cb.download()
+    assert np.isnan(out[1::2]).all() and not np.isnan(out[::2]).any()
+    ldc = n + 2  # 69 columns of storage: an odd leading dimension -> the reduction's scalar path
+    store = np.full((m, ldc), -7.0)
+    store[:, :n] = 2.0
+    Cs = kw.Buffer(gpu, kw.IndexVec(m * ldc), 8)
+    Cs.upload(store.reshape(-1))
+    assert lib.kw_dgemm_with_config(q.handle(), SPLITK_CFG, m, n, k, 1.0, A.data(), A.leadingDim(), B.data(),
+                                    B.leadingDim(), 0.5, Cs.data(), ldc) == 0
+    q.wait()
+    got = Cs.download().reshape(m, ldc)
+    assert (got[:, n:] == -7.0).all()
+    ok, worst = within_tol(got[:, :n], oracle.gemm(1.0, 0.5, a, b, np.full((m, n), 2.0), threads=8), k)
+    assert ok, worst
