@@ -206,7 +206,7 @@ KW_EXPORT kw_status kw_axpy_kernel_name(const kw_workdiv* wd, int elem_size, con
  * chosen per problem among bitwise-identical configurations. Host pointers are streamed through
  * the device inside the task (row panels, or for compute-heavy problems with all three operands
  * pinned, panel uploads feeding one persistent launch); bits equal the resident launch.
- * Environment KW_DGEMM_SPLITK=1 (read once) opts into split-k (config 27) for fewer 64x64 output
+ * Environment KW_DGEMM_SPLITK=1 (read once) opts into split-k (config 27) for fewer 32x32 output
  * tiles than SMs with k >= 1024: faster there, within the same bound, deterministic, but not
  * bitwise equal to the host-streamed / row-sharded paths for those shapes. */
 KW_EXPORT kw_status kw_dgemm(kw_queue q, const kw_workdiv* wd, size_t m, size_t n, size_t k, double alpha,
@@ -223,7 +223,7 @@ KW_EXPORT kw_status kw_dgemm_bitwise(kw_queue q, const kw_workdiv* wd, size_t m,
 
 /* Tile-configuration sweep (BASELINE.json configs[4]): the DMMA kernel's instantiated
  * configurations, info = {BM, BN, BK, threads, stages}; device operands only. Configurations
- * 14..26 are bitwise interchangeable; 27 is split-k (sums of k-slice chains, see kw_dgemm). */
+ * 14..26, 28, 29 are bitwise interchangeable; 27 is split-k (sums of k-slice chains, see kw_dgemm). */
 KW_EXPORT int kw_dgemm_config_count(void);
 KW_EXPORT kw_status kw_dgemm_config_info(int cfg, int info[5]);
 KW_EXPORT kw_status kw_dgemm_with_config(kw_queue q, int cfg, size_t m, size_t n, size_t k, double alpha,

@@ -1725,6 +1725,8 @@ using Split64w8t = TmaCfg<64, 64, 16, 32, 8, 1, true>;      // 23: SPLIT, 8 cons
 // 25 / 26: two consumer groups of config 16's geometry (64 x 128 tiles, 4 warps of 64 x 32) in one
 // CTA per SM, each with its own 4-stage ring and producer lane — SPLIT walk / data-parallel.
 using Pair64x128 = TmaCfg<64, 128, 64, 32, 4, 1, true, 2>;
+using Tma32p = TmaCfg<32, 32, 16, 16, 8, 3, true>;   // 28: 32 x 32 tiles, 4 warps of 16 x 16, 3 CTAs/SM
+using Tma32x64p = TmaCfg<32, 64, 16, 32, 8, 2, true>; // 29: 32 x 64 tiles, 4 warps of 16 x 32, 2 CTAs/SM
 // (16 consumer warps of 32x32 were measured out: 104 registers per consumer spill.)
 
 // ---- SPLIT launches: per-stream scratch (ticket, abort pointer, flags, park slots) ----------
@@ -2079,6 +2081,8 @@ const CfgInfo kCfgs[] = {
      launch_tma<Pair64x128>}, // 26
     {Tma64x64x3p::BM, Tma64x64x3p::BN, Tma64x64x3p::BK, Tma64x64x3p::THREADS, Tma64x64x3p::STAGES,
      launch_splitk<Tma64x64x3p>}, // 27: split-k over config 17 (NOT bitwise-interchangeable)
+    {Tma32p::BM, Tma32p::BN, Tma32p::BK, Tma32p::THREADS, Tma32p::STAGES, launch_tma<Tma32p>},         // 28
+    {Tma32x64p::BM, Tma32x64p::BN, Tma32x64p::BK, Tma32x64p::THREADS, Tma32x64p::STAGES, launch_tma<Tma32x64p>}, // 29
 };
 constexpr int kNumCfgs = sizeof(kCfgs) / sizeof(kCfgs[0]);
 // Tile choice for the GPU back-end. The tile work division (gemmTiledWorkDiv) is the coverage
@@ -2094,7 +2098,11 @@ constexpr int kNumCfgs = sizeof(kCfgs) / sizeof(kCfgs[0]);
 // co-resident CTAs hide better (8192 x 8192 x 256: 33.1 vs 32.0 TFLOP/s; x 1024: 35.3 vs 34.9;
 // 3000 x 5000 x 700: 32.9 vs 32.1; at k = 1536 16 leads again, 4096^2 x 1536: 35.06 vs 34.96 —
 // profiles/dgemm_rect_r02.txt).
-constexpr int kCfgWide = 16, kCfgSmall = 17;
+// Fewer 64 x 64 tiles than SMs: smaller tiles of the same paired k-map (bits unchanged) — 32 x 64
+// (29, two CTAs/SM) from 1.5 of its tiles per SM, else 32 x 32 (28, three CTAs/SM): 512^2 x
+// 16384 12.3 -> 27.4 TFLOP/s (28), 768^2 x 8192 27.4 -> 33.0 (29), 512^2 x 2048 11.6 -> 24.9 (28;
+// cuBLAS 22.8) — profiles/dgemm_small_tiles_r02.txt.
+constexpr int kCfgWide = 16, kCfgSmall = 17, kCfgTiny = 28, kCfgTinyWide = 29;
 constexpr int kShortK = 1408;
 
 int pick_config(const GemmParams& p)
@@ -2102,6 +2110,10 @@ int pick_config(const GemmParams& p)
     const long long sms = sm_count();
     const long long rows = (p.m + 63) / 64;
     const long long t16 = rows * ((p.n + 127) / 128), t17 = rows * ((p.n + 63) / 64);
+    if (t17 < sms) {
+        const long long t29 = ((p.m + 31) / 32) * ((p.n + 63) / 64);
+        return 2 * t29 >= 3 * sms ? kCfgTinyWide : kCfgTiny;
+    }
     const long long load16 = (t16 + sms - 1) / sms * 8192, load17 = (t17 + sms - 1) / sms * 4096;
     const bool small =
         t16 <= sms || p.k < kShortK || static_cast<double>(load17) < 0.97 * static_cast<double>(load16);
@@ -2137,7 +2149,8 @@ int pick_resident(const GemmParams& p)
     const double ideal = static_cast<double>(p.m) * p.n / sms;
     const double q16 = ideal / (std::ceil(t16 / sms) * 8192.0), q17 = ideal / (std::ceil(t17 / sms) * 4096.0);
     const long long ktiles = (p.k + 15) / 16;
-    if (splitk_default() && t17 < static_cast<long long>(sms) && ktiles >= kSplitKMinKtiles && tma_eligible(p))
+    const long long t28 = ((p.m + 31) / 32) * ((p.n + 31) / 32);
+    if (splitk_default() && t28 < static_cast<long long>(sms) && ktiles >= kSplitKMinKtiles && tma_eligible(p))
         return kCfgSplitK;
     if (std::max(q16, q17) < 0.93 && t17 >= static_cast<long long>(sms) && ktiles >= 2 && tma_eligible(p))
         return 2 * t16 >= 5 * static_cast<long long>(sms) ? kCfgSplitPair
@@ -2302,10 +2315,11 @@ bool dgemm_krange_ok(size_t m, size_t n, size_t k, const double* A, size_t lda, 
     return m > 0 && n > 0 && tma_eligible(make_params(m, n, k, 1.0, A, lda, B, ldb, 0.0, nullptr, n));
 }
 
-// k-range passes for the row-sharded k-slab schedule (configs 16 / 17, the data-parallel ones).
+// k-range passes for the row-sharded k-slab schedule: config 16 for its own pick, 17 (64 x 64)
+// for every other data-parallel pick (same bits).
 size_t dgemm_krange_park_bytes(int cfg, size_t m, size_t n)
 {
-    const size_t bm = 64, bn = cfg == kCfgSmall ? 64 : 128;
+    const size_t bm = 64, bn = cfg == kCfgWide ? 128 : 64;
     return kw::ceil_div(m, bm) * bm * kw::ceil_div(n, bn) * bn * sizeof(double);
 }
 
@@ -2316,8 +2330,8 @@ kw_status dgemm_device_krange(cudaStream_t s, int cfg, size_t m, size_t n, size_
     if (m == 0 || n == 0)
         return KW_OK;
     const GemmParams p = make_params(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
-    return cfg == kCfgSmall ? launch_krange<Tma64x64x3p>(s, p, kt0, kt1, park)
-                            : launch_krange<Tma64x128x2p>(s, p, kt0, kt1, park);
+    return cfg == kCfgWide ? launch_krange<Tma64x128x2p>(s, p, kt0, kt1, park)
+                           : launch_krange<Tma64x64x3p>(s, p, kt0, kt1, park);
 }
 
 kw_status dgemm_device_cfg(cudaStream_t s, int cfg, size_t m, size_t n, size_t k, double alpha, const double* A,

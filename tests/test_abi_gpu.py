@@ -56,7 +56,7 @@ def test_dgemm_configuration_table(gpu):
         info = (C.c_int * 5)()
         L.check(lib.kw_dgemm_config_info(cfg, info))
         bm, bn, bk, threads, stages = list(info)
-        assert bm in (64, 128) and bn in (64, 128) and bk in (16, 32) and threads % 32 == 0 and stages >= 2
+        assert bm in (32, 64, 128) and bn in (32, 64, 128) and bk in (16, 32) and threads % 32 == 0 and stages >= 2
     info = (C.c_int * 5)()
     assert lib.kw_dgemm_config_info(count, info) == L.KW_USAGE
 

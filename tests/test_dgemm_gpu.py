@@ -536,7 +536,7 @@ def test_tiled_bitwise_4096(gpu, oracle):
 
 
 def test_paired_configs_are_bitwise_interchangeable(gpu, oracle):
-    """Every TMA configuration with the paired k-slot map (14..17) feeds each output element the
+    """Every TMA configuration with the paired k-slot map (14..29 but split-k 27) feeds each output element the
     same DMMA sequence, so tile shape / CTAs per SM / persistence change no bit — which is what
     lets the library pick the tile by problem size without breaking the panel and row-shard
     invariance."""
@@ -559,7 +559,8 @@ def test_paired_configs_are_bitwise_interchangeable(gpu, oracle):
         assert within_tol(outs[0], oracle.gemm(0.9, 1.1, a, b, c), k)[0]
 
 
-@pytest.mark.parametrize("m,n,k", [(1024, 1024, 1024), (1280, 1280, 640), (1100, 1000, 2000), (1792, 1792, 512), (1536, 1408, 700)])
+@pytest.mark.parametrize("m,n,k", [(1024, 1024, 1024), (1280, 1280, 640), (1100, 1000, 2000), (1792, 1792, 512),
+                                   (1536, 1408, 700), (512, 512, 4096), (768, 700, 2500)])
 def test_default_choice_split_is_bitwise_the_one_cta_tile(gpu, oracle, m, n, k):
     """Shapes the library now runs with a SPLIT configuration (badly quantised data-parallel
     grids): the default kw_dgemm result equals the one-CTA-per-tile config 17 bit for bit and the
@@ -731,7 +732,7 @@ def test_host_operand_schedules_from_fresh_threads(gpu, monkeypatch):
         assert np.array_equal(results[t], want), t
 
 
-@pytest.mark.parametrize("cfg", [18, 20, 24, 25, 26])
+@pytest.mark.parametrize("cfg", [18, 20, 24, 25, 26, 28, 29])
 def test_split_and_group_configs_read_c_when_beta_is_zero(gpu, cfg):
     """gemm.cpp:35 / 115 (beta multiplies C even when 0) on the SPLIT / two-group walks: NaNs
     planted in C — in head, tail and full tiles — come out as NaN, everything else is finite."""

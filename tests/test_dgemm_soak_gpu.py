@@ -126,13 +126,14 @@ def test_split_configs_agree_bitwise_on_random_cases(gpu):
         beta = float(rng.choice([0.0, 1.0, -1.25]))
         a, b, c = rng.standard_normal((m, k)), rng.standard_normal((k, n)), rng.standard_normal((m, n))
         outs = []
-        for cfg in (17, 18 + 2 * (case % 2), 24 + (case % 3)):  # 24: 128 x 128 split, 25/26: two groups
+        # 24: 128 x 128 split, 25/26: two groups, 28/29: 32 x 32 / 32 x 64 tiles
+        for cfg in (17, 18 + 2 * (case % 2), 24 + (case % 3), 28 + (case % 2)):
             A, B, Cd = dev_mat(gpu, a), dev_mat(gpu, b), dev_mat(gpu, c)
             L.check(lib.kw_dgemm_with_config(q.handle(), cfg, m, n, k, alpha, A.data(), A.leadingDim(), B.data(),
                                              B.leadingDim(), beta, Cd.data(), Cd.leadingDim()))
             q.wait()
             outs.append(Cd.download())
-        assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2]), (case, m, n, k)
+        assert all(np.array_equal(outs[0], o) for o in outs[1:]), (case, m, n, k)
 
 
 def test_rowsharded_kslab_random_cases(gpu):

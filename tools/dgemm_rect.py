@@ -17,7 +17,7 @@ from paper_1602_08477_b200 import kernelweave as kw  # noqa: E402
 SHAPES = [(8192, 8192, 256), (8192, 8192, 1024), (256, 8192, 8192), (8192, 256, 8192), (2048, 8192, 2048),
           (8192, 2048, 2048), (1024, 4096, 4096), (4096, 1024, 4096), (512, 512, 16384), (3000, 5000, 700),
           (16384, 1024, 1024), (1024, 16384, 1024)]
-CFGS = (-1, 16, 17, 18, 20, 25, 27)
+CFGS = (-1, 16, 17, 18, 20, 25, 27, 28, 29)
 
 
 def timed(lib, q, go, flops, reps):

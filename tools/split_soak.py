@@ -15,7 +15,7 @@ from oracle import oracle as O  # noqa: E402  (test infrastructure: the checker)
 from paper_1602_08477_b200 import _lib as L  # noqa: E402
 from paper_1602_08477_b200 import kernelweave as kw  # noqa: E402
 
-CFGS = (16, 18, 20, 23, 24, 25, 26)
+CFGS = (16, 18, 20, 23, 24, 25, 26, 28, 29)
 
 
 def main():
