@@ -1,5 +1,6 @@
 """Long soak of the tile configurations the library picks (data-parallel 16/17, SPLIT 18/20/23/24/25,
-two-group 26): random shapes (ragged, small and large k, padded leading dimensions), random
+two-group 26, small tiles 28/29, and kw_dgemm's own choice): random shapes (ragged, small
+outputs, small and large k, padded leading dimensions), random
 scalars, signed inputs; every configuration must give the bits of config 17, and config 17 must be
 within (K+4)u of gemmReference (scaled by |alpha||A||B| + |beta||C| for signed data) on a subset.
 python tools/split_soak.py [cases] [seed]"""
@@ -15,7 +16,7 @@ from oracle import oracle as O  # noqa: E402  (test infrastructure: the checker)
 from paper_1602_08477_b200 import _lib as L  # noqa: E402
 from paper_1602_08477_b200 import kernelweave as kw  # noqa: E402
 
-CFGS = (16, 18, 20, 23, 24, 25, 26, 28, 29)
+CFGS = (16, 18, 20, 23, 24, 25, 26, 28, 29, -1)  # -1: kw_dgemm's own choice (default division)
 
 
 def main():
@@ -30,6 +31,8 @@ def main():
     checked = 0
     for case in range(cases):
         m, n = (int(v) for v in rng.integers(64, 2600, size=2))
+        if case % 4 == 3:  # small outputs with long k: the 32 x 32 / 32 x 64 tile picks
+            m, n = (int(v) for v in rng.integers(1, 700, size=2))
         k = int(rng.choice([int(rng.integers(1, 64)), int(rng.integers(64, 3000))]))
         align = int(rng.choice([64, 128, 256]))
         alpha = float(rng.choice([1.0, -0.5, 0.75, 2.5]))
@@ -41,8 +44,12 @@ def main():
             A.upload(a)
             B.upload(b)
             Cd.upload(c)
-            L.check(lib.kw_dgemm_with_config(q.handle(), cfg, m, n, k, alpha, A.data(), A.leadingDim(), B.data(),
-                                             B.leadingDim(), beta, Cd.data(), Cd.leadingDim()))
+            if cfg < 0:
+                L.check(lib.kw_dgemm(q.handle(), None, m, n, k, alpha, A.data(), A.leadingDim(), B.data(),
+                                     B.leadingDim(), beta, Cd.data(), Cd.leadingDim()))
+            else:
+                L.check(lib.kw_dgemm_with_config(q.handle(), cfg, m, n, k, alpha, A.data(), A.leadingDim(), B.data(),
+                                                 B.leadingDim(), beta, Cd.data(), Cd.leadingDim()))
             q.wait()
             outs[cfg] = Cd.download()
         for cfg in CFGS:
